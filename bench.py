@@ -1,0 +1,499 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 hashing / Count Sketch path (BASELINE.json metric:
+"4-universal hashes/s and Count Sketch updates/s per B200, at 1/2/4/8 GPUs").
+
+Headline workload: config 5 (BASELINE.json configs[4]) -- Count Sketch with
+t = 5 rows x 2^16 int64 counters, degree-3 mod 2^61-1 families, two-for-one
+bucket/sign split, 2^31 Zipf(1.2) items with int32 weights in [-100, 100],
+sharded over the ranks, tables merged by NCCL allreduce, median-of-rows F2.
+One step = zero table + fused hash/split/scatter over the rank's shard +
+allreduce + estimator.  value = items (Count Sketch updates) per second over
+the whole job; each item is t = 5 four-universal hash evaluations.
+
+Configs 1-4 are measured in the same run and reported under "configs".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+S = 1  # master seed (the reference CLI default, commands.cpp:31)
+C5_ITEMS = 1 << 31
+C5_ROWS, C5_WIDTH = 5, 1 << 16
+C1_ITEMS, C2_KEYS, C3_UNITS, C4_KEYS = 1 << 24, 1 << 28, 1 << 28, 1 << 26
+# algorithmic work per unit: bytes of HBM traffic and 32x32->64 limb products
+WORK = {
+    "c1": (4, 6), "c2_k4": (16, 12), "c2_k8": (16, 28), "c3": (32, 6), "c4": (8, 18), "c5": (8, 30),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true", help="skip configs 1-4")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--items", type=int, default=C5_ITEMS, help="config-5 stream length (tests only)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def shard(n, rank, world):
+    """Contiguous shard [lo, hi) of n units for `rank` (every unit exactly once)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- reference arm
+def cpu_reference_c5(sample_items, reps=3, threads=None):
+    """The reference's own CPU path (oracle/_ref = unmodified reference sources):
+    CountSketch(5, 65536, m61, 2^32, Pow2, S)::process over a bounded sample,
+    sharded over host threads + merge() (bit-identical to one serial pass)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import oracle, reference
+
+    ref = reference()
+    kind = "reference"
+    if ref is None:
+        ref, kind = None, "port"
+    orc = oracle()
+    keys, w = orc.gen_zipf_items(S, 0, sample_items)
+    threads = threads or (os.cpu_count() or 1)
+    times = []
+    for rep in range(reps + 1):
+        t0 = time.perf_counter()
+        if ref is not None:
+            ref.cs_run(C5_ROWS, C5_WIDTH, 61, 32, 0, S, keys, w, threads=threads)
+        else:
+            fams = [orc.coeffs(61, 4, s) for s in orc.row_seeds(S, C5_ROWS)]
+            orc.cs_process(C5_ROWS, C5_WIDTH, 61, fams, 32, 0, keys, w)
+        dt = time.perf_counter() - t0
+        if rep:
+            times.append(dt)
+    med = statistics.median(times)
+    return {"value": sample_items / med, "unit": "updates/s", "cores": threads, "kind": kind,
+            "sample": f"config 5 prefix of {sample_items} Zipf items (5 rows x 65536), median of {reps} "
+                      f"after 1 warm-up, {threads} threads, shard + merge()"}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    per_step = 1 << 23
+    cores = os.cpu_count() or 1
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import oracle, reference
+
+    ref = reference()
+    orc = oracle()
+    keys, w = orc.gen_zipf_items(S, 0, per_step)
+    kind = "reference" if ref is not None else "port"
+    fams = [orc.coeffs(61, 4, s) for s in orc.row_seeds(S, C5_ROWS)]
+
+    def step():
+        if ref is not None:
+            ref.cs_run(C5_ROWS, C5_WIDTH, 61, 32, 0, S, keys, w, threads=cores)
+        else:
+            orc.cs_process(C5_ROWS, C5_WIDTH, 61, fams, 32, 0, keys, w)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = per_step * args.steps / dt
+    line = {
+        "impl": "reference", "metric": metric_name(), "value": value, "unit": "updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "config5_countsketch_t5_m65536_zipf1.2", "sample_items_per_step": per_step,
+                   "rows": C5_ROWS, "width": C5_WIDTH, "prime": "2^61-1", "k": 4},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": kind,
+                         "sample": f"{per_step} items of the config-5 stream per step, CountSketch::process "
+                                   f"sharded over {cores} threads + merge()"},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def metric_name():
+    return "Count Sketch updates/s (config 5: t=5 rows of 4-universal 2^61-1 hashes, 2^31 Zipf items)"
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2008_08654_b200 as mb
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    hbm_peak, peak_kind = load_peaks()
+    traffic = load_traffic()
+
+    # ---- integer-pipe peak: independent mad.wide.u32 chains ----
+    sink = torch.zeros(1, dtype=torch.int64, device=dev)
+    blocks, threads, iters = mb_sm_count(torch) * 8, 256, 4096
+    for _ in range(2):
+        mb.probe_imad(blocks, threads, iters, sink)
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        mb.probe_imad(blocks, threads, iters, sink)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    imad_peak = blocks * threads * 8 * iters / best  # IMAD.WIDE.U32 per second
+
+    def roofline(cfg, units, kernel_s, kname):
+        bpu, lpu = WORK[cfg]
+        hbm = units * bpu / kernel_s / 1e9
+        ints = units * lpu / kernel_s
+        frac_h, frac_i = hbm / hbm_peak, ints / imad_peak
+        tr = traffic.get(kname)
+        if frac_h >= frac_i:
+            return {"bound": "hbm", "achieved": hbm, "peak": hbm_peak, "unit": "GB/s", "frac": frac_h,
+                    "traffic": tr, "peak_kind": peak_kind,
+                    "int_pipe": {"achieved": ints / 1e12, "peak": imad_peak / 1e12, "unit": "T IMAD.WIDE/s",
+                                 "frac": frac_i}}
+        return {"bound": "int", "achieved": ints / 1e12, "peak": imad_peak / 1e12, "unit": "T IMAD.WIDE/s",
+                "frac": frac_i, "traffic": tr, "peak_kind": "measured (probe_imad, this run)",
+                "hbm": {"achieved": hbm, "peak": hbm_peak, "unit": "GB/s", "frac": frac_h,
+                        "peak_kind": peak_kind, "frac_of_8TBs": hbm / 8000.0}}
+
+    # ---------------------------------------------------------- config 5 headline
+    n_total = args.items
+    lo, hi = shard(n_total, rank, world)
+    n_local = hi - lo
+    zs = mb.ZipfStream(S)
+    keys = torch.empty(n_local, dtype=torch.int32, device=dev)
+    wts = torch.empty(n_local, dtype=torch.int32, device=dev)
+    zs.generate(lo, n_local, keys, wts)
+    spec = mb.SketchSpec.seeded(C5_ROWS, C5_WIDTH, 61, 32, mb.SPLIT_POW2, S)
+    table = torch.zeros(C5_ROWS * C5_WIDTH, dtype=torch.int64, device=dev)
+    mom = torch.empty((C5_ROWS, 4), dtype=torch.int64, device=dev)
+    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+
+    def c5_step(i=None):
+        table.zero_()
+        if i is not None:
+            k_ev[i][0].record()
+        mb.cs_update(spec, keys, table, wts)
+        if i is not None:
+            k_ev[i][1].record()
+        if world > 1:
+            dist.all_reduce(table)
+        mb.cs_moments(table, C5_ROWS, C5_WIDTH, mom)
+
+    for _ in range(max(3, args.warmup)):
+        c5_step()
+    barrier_sync()
+    t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t_start.record()
+        for i in range(args.steps):
+            c5_step(i)
+        t_stop.record()
+        barrier_sync()
+    elapsed = max_over_ranks(t_start.elapsed_time(t_stop) / 1e3)
+    kern = max_over_ranks(sum(a.elapsed_time(b) for a, b in k_ev) / 1e3 / args.steps)
+    moments = mb.moments_to_python(mom)
+    f2 = mb.lower_median(moments)
+    value = n_total * args.steps / elapsed
+    clocks = clk.summary()
+
+    line = {
+        "metric": metric_name(), "value": value, "unit": "updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": elapsed / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded Zipf(1.2) stream generated on device, DESIGN.md Inputs)",
+        "config": {"workload": "config5_countsketch_t5_m65536_zipf1.2", "items": n_total,
+                   "rows": C5_ROWS, "width": C5_WIDTH, "prime": "2^61-1", "k": 4, "split": "two-for-one pow2",
+                   "weights": "int32 uniform [-100,100]", "parallelism": f"dp{world} (item shards + NCCL allreduce)",
+                   "l2": "inputs 16 GiB >> 126 MB L2 (no flush needed)"},
+        "hashes_per_s": value * C5_ROWS,
+        "f2_median": str(f2[0]),
+        "roofline": roofline("c5", n_local, kern, "cs_update_kernel"),
+        "kernel_ms": kern * 1e3,
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks,
+        "peaks": {"imad_wide_per_s": imad_peak, "hbm_gbs": hbm_peak, "hbm_kind": peak_kind},
+    }
+    del keys, wts
+
+    # ---------------------------------------------------------- e2e through the host API
+    if not args.no_e2e:
+        hk = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
+        hw = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
+        dk = torch.empty(n_local, dtype=torch.int32, device=dev)
+        dw = torch.empty(n_local, dtype=torch.int32, device=dev)
+        zs.generate(lo, n_local, dk, dw)
+        hk.copy_(dk)
+        hw.copy_(dw)
+        del dk, dw
+        torch.cuda.synchronize()
+        sk = mb.CountSketch(C5_ROWS, C5_WIDTH, 61, 32, mb.SPLIT_POW2, S)
+        hk_np, hw_np = hk.numpy(), hw.numpy()
+
+        def e2e_step():
+            sk.set_counters(np.zeros(C5_ROWS * C5_WIDTH, np.int64))
+            sk.process(hk_np, hw_np)            # H2D of keys + weights inside, pipelined
+            if world > 1:
+                t = torch.from_numpy(sk.counters()).to(dev)
+                dist.all_reduce(t)
+            return sk.second_moment(True)       # D2H of the estimator
+
+        e2e_step()
+        barrier_sync()
+        t0 = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, 3))
+        for _ in range(e2e_steps):
+            e2e_step()
+        barrier_sync()
+        dt = max_over_ranks(time.perf_counter() - t0)
+        line["e2e"] = {"value": n_total * e2e_steps / dt, "unit": "updates/s",
+                       "h2d_bytes_per_step": n_local * 8, "d2h_bytes_per_step": C5_ROWS * 32,
+                       "path": "mb200_sketch_process (host buffers, pinned) + mb200_sketch_second_moment",
+                       "steps": e2e_steps}
+        del sk, hk, hw
+
+    # ---------------------------------------------------------- configs 1-4
+    if not args.no_extras:
+        line["configs"] = bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ranks)
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_reference_c5(1 << 23)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def mb_sm_count(torch):
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def timed_steps(torch, steps, warmup, fn, flush=None):
+    """Per-step CUDA-event timing; an L2 flush (outside the events) between steps when given."""
+    for _ in range(max(3, warmup)):
+        fn()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(steps):
+        if flush is not None:
+            flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        tot += a.elapsed_time(b) / 1e3
+    return tot / steps
+
+
+def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ranks):
+    out = {}
+    SK = S ^ mb.SALT_KEYS
+    steps = args.steps
+    flushbuf = torch.empty(1 << 28, dtype=torch.uint8, device=dev)  # 256 MiB > 126 MB L2
+
+    def flush():
+        flushbuf.fill_(1)
+
+    # config 1: CountSketch(1, 1024), 2^24 u32 keys (64 MiB < L2: flushed between steps)
+    lo, hi = shard(C1_ITEMS, rank, world)
+    keys = mb.gen_u32_keys(SK, lo, hi - lo)
+    spec = mb.SketchSpec.seeded(1, 1024, 61, 32, mb.SPLIT_POW2, S)
+    table = torch.zeros(1024, dtype=torch.int64, device=dev)
+    mom = torch.empty((1, 4), dtype=torch.int64, device=dev)
+
+    def c1():
+        table.zero_()
+        mb.cs_update(spec, keys, table)
+        mb.cs_moments(table, 1, 1024, mom)
+
+    t = max_over_ranks(timed_steps(torch, steps, args.warmup, c1, flush))
+    tk = max_over_ranks(timed_steps(torch, steps, args.warmup, lambda: mb.cs_update(spec, keys, table), flush))
+    out["c1"] = {"value": C1_ITEMS / t, "unit": "updates/s", "ms_per_step": t * 1e3,
+                 "workload": "CountSketch(1,1024), 2^24 u32 keys, delta +1", "l2": "flushed between steps",
+                 "roofline": roofline("c1", hi - lo, tk, "cs_update_kernel")}
+    del keys
+
+    # config 2: raw hashing, 2^28 u64 keys uniform in [0, p), k = 4 and 8
+    lo, hi = shard(C2_KEYS, rank, world)
+    keys, bad = mb.gen_below_p61(SK, lo, hi - lo)
+    assert int(bad.item()) == 0
+    outb = torch.empty(hi - lo, dtype=torch.int64, device=dev)
+    for k in (4, 8):
+        coeffs = mb.draw_coeffs(61, k, S)
+        t = max_over_ranks(timed_steps(torch, steps, args.warmup,
+                                       lambda: mb.hash61(keys, coeffs, key_bits=64, out=outb)))
+        out[f"c2_k{k}"] = {"value": C2_KEYS / t, "unit": "hashes/s", "ms_per_step": t * 1e3,
+                           "workload": f"degree-{k-1} mod 2^61-1, 2^28 u64 keys in [0,p)",
+                           "l2": "inputs 2 GiB > L2",
+                           "roofline": roofline(f"c2_k{k}", hi - lo, t, "hash61_key64_kernel")}
+    del keys, outb
+
+    # config 3: div/mod by 2^64 - 59 of 2^28 u128 inputs in [0, p^2)
+    lo, hi = shard(C3_UNITS, rank, world)
+    v, bad = mb.gen_pm_inputs(SK, 59, lo, hi - lo)
+    assert int(bad.item()) == 0
+    q = torch.empty(hi - lo, dtype=torch.int64, device=dev)
+    r = torch.empty(hi - lo, dtype=torch.int64, device=dev)
+    ovf = torch.zeros(1, dtype=torch.int64, device=dev)
+    t = max_over_ranks(timed_steps(torch, steps, args.warmup, lambda: mb.pm_divmod(v, 64, 59, 3, q, r, ovf)))
+    assert int(ovf.item()) == 0
+    out["c3"] = {"value": C3_UNITS / t, "unit": "divmod/s", "ms_per_step": t * 1e3,
+                 "workload": "Alg 4+5 by 2^64-59 (m=3), 2^28 u128 inputs in [0,p^2)", "l2": "inputs 4 GiB > L2",
+                 "roofline": roofline("c3", hi - lo, t, "pm_divmod_kernel")}
+    del v, q, r
+
+    # config 4: 89-bit two-for-one, 2^26 u64 keys -> two rows of 2^16 counters
+    lo, hi = shard(C4_KEYS, rank, world)
+    keys = mb.gen_u64_keys(SK, lo, hi - lo)
+    spec = mb.SketchSpec(2, 1 << 16, 89, [mb.draw_coeffs(89, 4, S)], 64, mb.SPLIT_TWO_FOR_ONE)
+    table = torch.zeros(2 << 16, dtype=torch.int64, device=dev)
+    mom = torch.empty((2, 4), dtype=torch.int64, device=dev)
+
+    def c4():
+        table.zero_()
+        mb.cs_update(spec, keys, table)
+        if world > 1:
+            dist.all_reduce(table)
+        mb.cs_moments(table, 2, 1 << 16, mom)
+
+    t = max_over_ranks(timed_steps(torch, steps, args.warmup, c4))
+    tk = max_over_ranks(timed_steps(torch, steps, args.warmup, lambda: mb.cs_update(spec, keys, table)))
+    out["c4"] = {"value": C4_KEYS / t, "unit": "keys/s", "row_updates_per_s": 2 * C4_KEYS / t,
+                 "ms_per_step": t * 1e3, "workload": "2^89-1 two-for-one, 2^26 u64 keys, 2 x 2^16 counters",
+                 "l2": "inputs 512 MiB > L2", "roofline": roofline("c4", hi - lo, tk, "cs_update_kernel")}
+    del keys, flushbuf
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+/*
+ * mersenne_b200.h -- C-ABI drop-in boundary of the B200 hashing / sketching path.
+ *
+ * The reference (/root/reference/proj) exposes this path only as C++ classes of
+ * a static library.  This header is the flat C boundary a binding
+ * (ctypes, cgo, JNI, N-API, or the reference's own C++ classes) binds to.  Each
+ * entry cites the reference interface it replaces.  Plain pointers and sizes
+ * only; CUDA streams travel as `void*` (a cudaStream_t, NULL = legacy default).
+ *
+ * Two layers:
+ *   1. device-array entries (mb200_hash61, mb200_cs_update, ...): inputs and
+ *      outputs are device pointers; the call is asynchronous on `stream` unless
+ *      a data-dependent domain check is required (see each entry).
+ *   2. object entries (mb200_sketch_*): the reference's CountSketch API on
+ *      host buffers; host<->device copies are inside the call.
+ *
+ * Errors: every entry returns a status code; the code names the reference
+ * exception class it stands for and mb200_last_error() returns the
+ * reference's message (thread-local).  There is no CPU fallback: when no
+ * sm_100 device is present every device entry returns MB200_CUDA_ERROR.
+ */
+#ifndef MERSENNE_B200_H
+#define MERSENNE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MB200_ABI_VERSION 1
+
+#define MB200_OK 0
+#define MB200_INVALID_ARGUMENT 1 /* std::invalid_argument (construction-time checks) */
+#define MB200_DOMAIN_ERROR 2     /* std::domain_error (polyhash.cpp:60, field.cpp:210, :262) */
+#define MB200_LOGIC_ERROR 3      /* std::logic_error (sketch.cpp:197) */
+#define MB200_CUDA_ERROR 4       /* CUDA runtime failure / no usable device */
+#define MB200_UNSUPPORTED 5      /* valid for the reference, not implemented on the GPU path */
+
+/* key widths */
+#define MB200_KEY_U32 32
+#define MB200_KEY_U64 64
+/* weight kinds (NULL weights = every delta is +1) */
+#define MB200_W_NONE 0
+#define MB200_W_I32 32
+#define MB200_W_I64 64
+/* splitters: sketch.hpp:33-37, plus the config-4 two-for-one row layout */
+#define MB200_SPLIT_POW2 0         /* split_pow2, sketch.cpp:13-19 */
+#define MB200_SPLIT_UNIFORM_ARB 1  /* split_arb_uniform, sketch.cpp:21-29 */
+#define MB200_SPLIT_MERSENNE_ARB 2 /* split_arb_mersenne, sketch.cpp:31-34 */
+#define MB200_SPLIT_TWO_FOR_ONE 3  /* one hash -> two rows */
+
+const char* mb200_last_error(void);
+int mb200_abi_version(void);
+/* number of visible sm_100 devices (0 when none) */
+int mb200_device_count(void);
+
+/* ---------------------------------------------------------------- field --- */
+/* MersenneModulus(b, require_prime) validation: field.cpp:197-206 */
+int mb200_mersenne_modulus_check(unsigned b, int require_prime);
+/* PseudoMersenneModulus(b, c, m_iters) ctor: field.cpp:224-244 (default
+ * iteration count field.cpp:158-171, domain threshold :176-193).  c < 2^64. */
+int mb200_pm_modulus(unsigned b, uint64_t c, unsigned m_iters, unsigned* iterations,
+                     uint64_t max_input[4]);
+
+/* ------------------------------------------------------------- hashing --- */
+/* PolyHashFamily(modulus, k, u, seed) coefficient draw: polyhash.cpp:12-35.
+ * lo/hi receive a_0..a_{k-1} (hi only for b > 64; may be NULL otherwise). */
+int mb200_draw_coeffs(unsigned b, unsigned k, uint64_t seed, uint64_t* lo, uint64_t* hi);
+/* CountSketch row seeds: successive SplitMix64(master).next(), sketch.cpp:72-77 */
+int mb200_row_seeds(uint64_t master, unsigned rows, uint64_t* out);
+
+/* K1 -- Alg 1 for p = 2^b - 1, b <= 61: replaces PolyHashFamily::operator()
+ * native path (polyhash.cpp:59-76) over a batch.  coeffs: host array a_0..a_{k-1}
+ * (k <= 16, each < p).  Keys must lie in [0, 2^key_bits) (domain_error otherwise,
+ * all-or-nothing: checked before any output is written; the check synchronizes
+ * `stream` and only runs when key_bits < key_width).  For b == 61 any
+ * key_bits <= 64 is accepted (keys beyond the reference's u <= 2^60 are reduced
+ * exactly); for b < 61 the reference domain p >= 2u - 1 applies.  d_out: n u64. */
+int mb200_hash61(const void* d_keys, int key_width, uint64_t n, unsigned b, const uint64_t* coeffs,
+                 unsigned k, unsigned key_bits, uint64_t* d_out, void* stream);
+
+/* K2 -- Alg 1 for p = 2^89 - 1: replaces the generic path (polyhash.cpp:78-88 with
+ * wide_mul uwide.hpp:148-163 and mersenne_reduce_partial field.hpp:66-73).
+ * u64 keys; outputs split into low 64 bits and high 25 bits (two dense arrays). */
+int mb200_hash89(const uint64_t* d_keys, uint64_t n, const uint64_t* coeffs_lo,
+                 const uint64_t* coeffs_hi, unsigned k, unsigned key_bits, uint64_t* d_out_lo,
+                 uint64_t* d_out_hi, void* stream);
+
+/* ------------------------------------------------------------ division --- */
+/* K6 -- Alg 4 + Alg 5 for p = 2^b - c (2 <= b <= 64, 1 <= c < 2^(b-1)):
+ * replaces pseudo_mersenne_div (field.cpp:260-265) + pseudo_mersenne_mod
+ * (:267-273).  d_v: n u128 as interleaved (lo, hi) u64 pairs; d_q, d_r: n u64.
+ * m_iters = 0 picks the reference default.  Inputs above max_input raise
+ * domain_error (checked, synchronizing, only when max_input < 2^128).
+ * d_overflow (nullable, device u64, accumulated): number of warps that met a
+ * quotient >= 2^64 (possible only for v >= 2^64 p). */
+int mb200_pm_divmod(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, unsigned m_iters,
+                    uint64_t* d_q, uint64_t* d_r, uint64_t* d_overflow, void* stream);
+
+/* --------------------------------------------------------- count sketch --- */
+typedef struct {
+    unsigned rows;             /* counter rows t (<= 16) */
+    uint64_t width;            /* counters per row */
+    unsigned b;                /* Mersenne exponent: <= 61 or 89 */
+    unsigned k;                /* coefficients per family (independence, <= 16) */
+    unsigned key_bits;         /* key domain is [0, 2^key_bits) */
+    int splitter;              /* MB200_SPLIT_* */
+    const uint64_t* coeffs_lo; /* host, families x k (families = rows, or ceil(rows/2) for TWO_FOR_ONE) */
+    const uint64_t* coeffs_hi; /* host, families x k, b > 64 only (else NULL) */
+} mb200_sketch_desc;
+
+/* K3+K4 -- fused hash -> split -> scatter-add: replaces CountSketch::process
+ * (sketch.cpp:133-140) over a batch.  d_counters: rows x width i64, row-major
+ * (sketch.hpp:75 layout), accumulated in place with wrapping adds.  Keys are
+ * domain-checked all-or-nothing (see mb200_hash61). */
+int mb200_cs_update(const mb200_sketch_desc* desc, const void* d_keys, int key_width,
+                    const void* d_weights, int weight_kind, uint64_t n, int64_t* d_counters,
+                    void* stream);
+/* K5 -- row_second_moment for every row (sketch.cpp:142-158): d_out receives
+ * rows x 4 u64 = (value lo, value hi, saturated, 0).  The lower median over rows
+ * (second_moment(true), sketch.cpp:160-168) is taken on the host. */
+int mb200_cs_moments(const int64_t* d_counters, unsigned rows, uint64_t width, uint64_t* d_out,
+                     void* stream);
+/* CountSketch::merge counter sum (sketch.cpp:182-193), wrapping */
+int mb200_cs_merge(int64_t* d_dst, const int64_t* d_src, uint64_t count, void* stream);
+/* CountSketch::point_query (sketch.cpp:170-180) over a batch of keys */
+int mb200_cs_point_query(const mb200_sketch_desc* desc, const int64_t* d_counters,
+                         const void* d_keys, int key_width, uint64_t n, int64_t* d_out,
+                         void* stream);
+
+/* ---------------------------------------------- sketch object (host API) --- */
+typedef struct mb200_sketch mb200_sketch;
+/* CountSketch(rows, width, MersenneModulus(b, true), 2^key_bits, splitter, seed,
+ * independence): sketch.cpp:68-82.  Counters live in HBM on the current device. */
+int mb200_sketch_create(unsigned rows, uint64_t width, unsigned b, unsigned key_bits, int splitter,
+                        uint64_t seed, unsigned independence, mb200_sketch** out);
+/* CountSketch(width, splitter, families): sketch.cpp:84-95 (families x k coefficients) */
+int mb200_sketch_create_families(uint64_t width, int splitter, unsigned b, unsigned key_bits,
+                                 unsigned families, unsigned k, const uint64_t* coeffs_lo,
+                                 const uint64_t* coeffs_hi, unsigned rows, mb200_sketch** out);
+void mb200_sketch_destroy(mb200_sketch* s);
+/* process(key, delta) for every item of a HOST batch: copies are pipelined in
+ * chunks against the scatter kernel; returns after the batch is applied. */
+int mb200_sketch_process(mb200_sketch* s, const void* h_keys, int key_width, const void* h_weights,
+                         int weight_kind, uint64_t n);
+/* same on DEVICE arrays, asynchronous on `stream` */
+int mb200_sketch_process_device(mb200_sketch* s, const void* d_keys, int key_width,
+                                const void* d_weights, int weight_kind, uint64_t n, void* stream);
+int mb200_sketch_row_second_moment(mb200_sketch* s, unsigned row, uint64_t* lo, uint64_t* hi,
+                                   int* saturated);
+int mb200_sketch_second_moment(mb200_sketch* s, int median_rows, uint64_t* lo, uint64_t* hi,
+                               int* saturated);
+int mb200_sketch_point_query(mb200_sketch* s, const void* h_keys, int key_width, uint64_t n,
+                             int64_t* h_out);
+int mb200_sketch_merge(mb200_sketch* dst, const mb200_sketch* src);
+int mb200_sketch_counters(mb200_sketch* s, int64_t* h_out);
+int mb200_sketch_set_counters(mb200_sketch* s, const int64_t* h_in);
+int64_t* mb200_sketch_device_counters(mb200_sketch* s);
+int mb200_sketch_info(const mb200_sketch* s, unsigned* rows, uint64_t* width, unsigned* b,
+                      unsigned* k, unsigned* key_bits, int* splitter);
+/* seeds() (sketch.hpp:73): logic_error for injected families */
+int mb200_sketch_seeds(const mb200_sketch* s, uint64_t* out);
+/* families x k coefficients actually used on the device */
+int mb200_sketch_coeffs(const mb200_sketch* s, uint64_t* lo, uint64_t* hi);
+
+/* ------------------------------------- workload generators (bench harness) --- */
+int mb200_gen_u32_keys(uint64_t seed, uint64_t start, uint64_t n, uint32_t* d_out, void* stream);
+int mb200_gen_u64_keys(uint64_t seed, uint64_t start, uint64_t n, uint64_t* d_out, void* stream);
+int mb200_gen_below_p61(uint64_t seed, uint64_t start, uint64_t n, uint64_t* d_out,
+                        uint64_t* d_bad, void* stream);
+int mb200_gen_pm_inputs(uint64_t seed, uint64_t c, uint64_t start, uint64_t n, uint64_t* d_out,
+                        uint64_t* d_bad, void* stream);
+int mb200_zipf_table(double alpha, uint32_t T, double universe, uint64_t* h_cdf, double* tail_c1);
+int mb200_gen_zipf_items(uint64_t master_seed, const uint64_t* d_cdf, uint32_t T, double tail_c1,
+                         double universe, uint64_t start, uint64_t n, uint32_t* d_keys,
+                         int32_t* d_weights, void* stream);
+
+/* ------------------------------------------------------------- probes --- */
+/* blocks x threads threads each issue 8 x iters independent mad.wide.u32 */
+int mb200_probe_imad(int blocks, int threads, int iters, uint64_t* d_sink, void* stream);
+int mb200_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* d_buf,
+                        uint64_t span, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

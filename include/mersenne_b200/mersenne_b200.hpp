@@ -1,0 +1,171 @@
+// mersenne_b200.hpp -- C++ host API of the B200 path, keeping the reference
+// library's names and semantics (/root/reference/proj/include/mersenne/
+// {field,polyhash,sketch}.hpp) and adding batched device methods.  It reaches
+// the GPU only through the C-ABI in <mersenne_b200.h>.
+//
+// Error behaviour mirrors the reference: std::invalid_argument at
+// construction, std::domain_error at call (all-or-nothing for batches),
+// std::logic_error for serializing injected families; CUDA failures raise
+// std::runtime_error.  There is no CPU fallback.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "../mersenne_b200.h"
+
+namespace mersenne::b200 {
+
+using u64 = std::uint64_t;
+using i64 = std::int64_t;
+using u128 = unsigned __int128;
+
+// throws the reference exception class for an mb200 status code
+void throw_status(int status);
+
+// field.hpp:20-33
+class MersenneModulus {
+public:
+    explicit MersenneModulus(unsigned b, bool require_prime = false);
+    unsigned b() const { return b_; }
+    u128 p() const { return (u128(1) << b_) - 1; }
+    bool prime_exponent() const { return prime_; }
+
+private:
+    unsigned b_;
+    bool prime_;
+};
+
+// field.hpp:38-63 (c < 2^64 on this path)
+class PseudoMersenneModulus {
+public:
+    PseudoMersenneModulus(unsigned b, u64 c, unsigned m_iters = 0);
+    unsigned b() const { return b_; }
+    u64 c() const { return c_; }
+    u128 p() const { return (u128(1) << b_) - c_; }
+    unsigned iterations() const { return m_; }
+    const std::array<u64, 4>& max_input() const { return max_input_; }
+
+    // pseudo_mersenne_div + pseudo_mersenne_mod over device arrays (field.cpp:260-273):
+    // d_v holds n u128 as (lo, hi) pairs; d_q, d_r receive n u64 each.
+    void divmod_device(const u64* d_v, u64 n, u64* d_q, u64* d_r, void* stream = nullptr) const;
+    // host-buffer convenience: copies in, divides, copies out
+    void divmod(const u64* h_v, u64 n, u64* h_q, u64* h_r) const;
+
+private:
+    unsigned b_;
+    u64 c_;
+    unsigned m_;
+    std::array<u64, 4> max_input_;
+};
+
+enum class HashFinish { ConditionalSubtract, BranchFree };  // polyhash.hpp:10-13 (same values)
+
+// polyhash.hpp:18-43
+class PolyHashFamily {
+public:
+    PolyHashFamily(const MersenneModulus& modulus, unsigned k, u128 key_domain, u64 seed,
+                   HashFinish finish = HashFinish::ConditionalSubtract);
+    PolyHashFamily(const MersenneModulus& modulus, std::vector<u128> coefficients, u128 key_domain,
+                   HashFinish finish = HashFinish::ConditionalSubtract);
+
+    // one key (API parity; launches a one-element batch)
+    u128 operator()(u128 x) const;
+    // batch over device keys (u32 or u64): out_lo gets the low 64 bits, out_hi (b > 64 only) the rest
+    void hash_device(const void* d_keys, int key_width, u64 n, u64* d_out_lo, u64* d_out_hi = nullptr,
+                     void* stream = nullptr) const;
+    // batch over host keys
+    std::vector<u128> hash(const std::vector<u64>& keys) const;
+
+    const MersenneModulus& modulus() const { return modulus_; }
+    const std::vector<u128>& coefficients() const { return coeffs_; }
+    unsigned independence() const { return unsigned(coeffs_.size()); }
+    u128 key_domain() const { return key_domain_; }
+    unsigned key_bits() const;
+    HashFinish finish() const { return finish_; }
+
+private:
+    void validate() const;
+    MersenneModulus modulus_;
+    std::vector<u128> coeffs_;
+    u128 key_domain_;
+    HashFinish finish_;
+};
+
+enum class Splitter : uint32_t { Pow2 = 0, UniformArb = 1, MersenneArb = 2, TwoForOne = 3 };
+
+struct SignIndexPair {
+    u128 index;
+    int sign;
+    friend bool operator==(const SignIndexPair&, const SignIndexPair&) = default;
+};
+// sketch.cpp:13-19 (host helper, the kernels apply the same rule in registers)
+SignIndexPair split_pow2(u128 h, unsigned b, unsigned l);
+
+// sketch.hpp:40-92 with counters resident in HBM of the current device
+class CountSketch {
+public:
+    CountSketch(unsigned rows, u64 width, const MersenneModulus& modulus, u128 key_domain, Splitter splitter,
+                u64 seed, unsigned independence = 4);
+    // Injected families: one per row (or one per two rows for Splitter::TwoForOne).
+    CountSketch(u64 width, Splitter splitter, std::vector<PolyHashFamily> families, unsigned rows = 0);
+    CountSketch(const CountSketch&) = delete;
+    CountSketch& operator=(const CountSketch&) = delete;
+    CountSketch(CountSketch&&) noexcept;
+    ~CountSketch();
+
+    void process(u128 x, i64 delta);  // API parity (one-item batch)
+    // host batch: key_width 32/64, weight_kind MB200_W_* (h_weights may be null = +1)
+    void process_batch(const void* h_keys, int key_width, const void* h_weights, int weight_kind, u64 n);
+    // device batch, asynchronous on `stream`
+    void process_device(const void* d_keys, int key_width, const void* d_weights, int weight_kind, u64 n,
+                        void* stream = nullptr);
+
+    struct Moment {
+        u128 value;
+        bool saturated;
+        friend bool operator==(const Moment&, const Moment&) = default;
+    };
+    Moment row_second_moment(unsigned row) const;
+    Moment second_moment(bool median_rows = false) const;
+    std::vector<Moment> row_moments() const;
+
+    i64 point_query(u128 x) const;
+    std::vector<i64> point_query_batch(const void* h_keys, int key_width, u64 n) const;
+
+    CountSketch& merge(const CountSketch& other);  // requires identical seeds (sketch.cpp:182-193)
+
+    unsigned rows() const { return rows_; }
+    u64 width() const { return width_; }
+    Splitter splitter() const { return splitter_; }
+    const MersenneModulus& modulus() const { return families_.front().modulus(); }
+    u128 key_domain() const { return families_.front().key_domain(); }
+    unsigned independence() const { return families_.front().independence(); }
+    const std::vector<u64>& seeds() const { return seeds_; }
+    const std::vector<PolyHashFamily>& families() const { return families_; }
+    std::vector<i64> counters() const;         // D2H copy (row-major, sketch.hpp:75)
+    void set_counters(const std::vector<i64>& c);
+    i64* device_counters() { return d_counters_; }
+    const i64* device_counters() const { return d_counters_; }
+    void synchronize() const;
+
+private:
+    void validate() const;
+    void init_device();
+    mb200_sketch_desc desc() const;
+
+    unsigned rows_;
+    u64 width_;
+    Splitter splitter_;
+    std::vector<PolyHashFamily> families_;
+    std::vector<u64> seeds_;
+    mutable std::vector<u64> clo_, chi_;  // coefficient cache for the C-ABI descriptor
+    i64* d_counters_ = nullptr;
+    void* stream_ = nullptr;  // cudaStream_t owned by the sketch
+    struct Staging;
+    std::unique_ptr<Staging> staging_;
+};
+
+}  // namespace mersenne::b200

@@ -1,0 +1,133 @@
+"""ctypes binding of the C-ABI boundary (include/mersenne_b200.h).
+
+The product path has no CPU fallback: importing this module without the built
+library raises ImportError, and every device entry fails with CudaError when
+no sm_100 GPU is visible.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmersenne_b200.so")
+
+MB200_OK = 0
+MB200_INVALID_ARGUMENT = 1
+MB200_DOMAIN_ERROR = 2
+MB200_LOGIC_ERROR = 3
+MB200_CUDA_ERROR = 4
+MB200_UNSUPPORTED = 5
+
+KEY_U32, KEY_U64 = 32, 64
+W_NONE, W_I32, W_I64 = 0, 32, 64
+SPLIT_POW2, SPLIT_UNIFORM_ARB, SPLIT_MERSENNE_ARB, SPLIT_TWO_FOR_ONE = 0, 1, 2, 3
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument of the reference (construction-time checks)."""
+
+
+class DomainError(ValueError):
+    """std::domain_error of the reference (key / dividend outside the domain)."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error of the reference."""
+
+
+class CudaError(RuntimeError):
+    """CUDA failure, or no usable sm_100 device (there is no CPU fallback)."""
+
+
+class Unsupported(NotImplementedError):
+    """Valid for the reference but not implemented on the GPU path."""
+
+
+_EXC = {
+    MB200_INVALID_ARGUMENT: InvalidArgument,
+    MB200_DOMAIN_ERROR: DomainError,
+    MB200_LOGIC_ERROR: LogicError,
+    MB200_CUDA_ERROR: CudaError,
+    MB200_UNSUPPORTED: Unsupported,
+}
+
+u64, u32, i64, i32 = C.c_uint64, C.c_uint32, C.c_int64, C.c_int32
+P, U, I, D = C.c_void_p, C.c_uint, C.c_int, C.c_double
+
+
+class SketchDesc(C.Structure):
+    _fields_ = [
+        ("rows", U),
+        ("width", u64),
+        ("b", U),
+        ("k", U),
+        ("key_bits", U),
+        ("splitter", I),
+        ("coeffs_lo", P),
+        ("coeffs_hi", P),
+    ]
+
+
+# (name, restype, argtypes) of every exported entry in include/mersenne_b200.h
+SIGNATURES = [
+    ("mb200_last_error", C.c_char_p, []),
+    ("mb200_abi_version", I, []),
+    ("mb200_device_count", I, []),
+    ("mb200_mersenne_modulus_check", I, [U, I]),
+    ("mb200_pm_modulus", I, [U, u64, U, P, P]),
+    ("mb200_draw_coeffs", I, [U, U, u64, P, P]),
+    ("mb200_row_seeds", I, [u64, U, P]),
+    ("mb200_hash61", I, [P, I, u64, U, P, U, U, P, P]),
+    ("mb200_hash89", I, [P, u64, P, P, U, U, P, P, P]),
+    ("mb200_pm_divmod", I, [P, u64, U, u64, U, P, P, P, P]),
+    ("mb200_cs_update", I, [P, P, I, P, I, u64, P, P]),
+    ("mb200_cs_moments", I, [P, U, u64, P, P]),
+    ("mb200_cs_merge", I, [P, P, u64, P]),
+    ("mb200_cs_point_query", I, [P, P, P, I, u64, P, P]),
+    ("mb200_sketch_create", I, [U, u64, U, U, I, u64, U, P]),
+    ("mb200_sketch_create_families", I, [u64, I, U, U, U, U, P, P, U, P]),
+    ("mb200_sketch_destroy", None, [P]),
+    ("mb200_sketch_process", I, [P, P, I, P, I, u64]),
+    ("mb200_sketch_process_device", I, [P, P, I, P, I, u64, P]),
+    ("mb200_sketch_row_second_moment", I, [P, U, P, P, P]),
+    ("mb200_sketch_second_moment", I, [P, I, P, P, P]),
+    ("mb200_sketch_point_query", I, [P, P, I, u64, P]),
+    ("mb200_sketch_merge", I, [P, P]),
+    ("mb200_sketch_counters", I, [P, P]),
+    ("mb200_sketch_set_counters", I, [P, P]),
+    ("mb200_sketch_device_counters", P, [P]),
+    ("mb200_sketch_info", I, [P, P, P, P, P, P, P]),
+    ("mb200_sketch_seeds", I, [P, P]),
+    ("mb200_sketch_coeffs", I, [P, P, P]),
+    ("mb200_gen_u32_keys", I, [u64, u64, u64, P, P]),
+    ("mb200_gen_u64_keys", I, [u64, u64, u64, P, P]),
+    ("mb200_gen_below_p61", I, [u64, u64, u64, P, P, P]),
+    ("mb200_gen_pm_inputs", I, [u64, u64, u64, u64, P, P, P]),
+    ("mb200_zipf_table", I, [D, u32, D, P, P]),
+    ("mb200_gen_zipf_items", I, [u64, P, u32, D, D, u64, u64, P, P, P]),
+    ("mb200_probe_imad", I, [I, I, I, P, P]),
+    ("mb200_probe_atomics", I, [I, I, I, I, P, u64, P]),
+]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "or `make lib` (the B200 path has no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int) -> None:
+    if status != MB200_OK:
+        msg = lib.mb200_last_error().decode()
+        raise _EXC.get(status, RuntimeError)(msg)

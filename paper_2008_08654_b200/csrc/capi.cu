@@ -1,0 +1,345 @@
+// capi.cu -- device-array entries of the C-ABI boundary (include/mersenne_b200.h):
+// argument validation with the reference's exception classes and messages,
+// data-dependent domain checks, and kernel dispatch.  No CPU fallback.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mersenne_b200.h"
+#include "mb200_capi_util.h"
+#include "mb200_internal.h"
+
+using namespace mb200;
+
+namespace mb200 {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(MB200_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool prime_exponent(unsigned b) {
+    static const unsigned kPrimes[] = {2, 3, 5, 7, 13, 17, 19, 31, 61, 89, 107, 127};  // field.cpp:12
+    for (unsigned p : kPrimes)
+        if (p == b) return true;
+    return false;
+}
+
+// Synchronous device counter read used by the all-or-nothing domain checks.
+int count_on_device(const std::function<cudaError_t(unsigned long long*, cudaStream_t)>& launch,
+                    cudaStream_t s, unsigned long long* out) {
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMallocAsync(&d, sizeof(*d), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    e = cudaMemsetAsync(d, 0, sizeof(*d), s);
+    if (e == cudaSuccess) e = launch(d, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, sizeof(*d), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "domain check");
+    return MB200_OK;
+}
+
+int check_keys(const void* d_keys, int key_width, uint64_t n, unsigned key_bits, cudaStream_t s) {
+    if (key_bits >= (unsigned)key_width || n == 0) return MB200_OK;
+    unsigned long long bad = 0;
+    int rc = count_on_device(
+        [&](unsigned long long* d, cudaStream_t st) {
+            return launch_count_out_of_domain(d_keys, key_width, n, key_bits, d, st);
+        },
+        s, &bad);
+    if (rc) return rc;
+    if (bad) return fail(MB200_DOMAIN_ERROR, "key outside domain");  // polyhash.cpp:60
+    return MB200_OK;
+}
+
+int build_sketch_params(const mb200_sketch_desc* d, SketchParams& sp) {
+    if (!d) return fail(MB200_INVALID_ARGUMENT, "null sketch descriptor");
+    if (d->rows == 0) return fail(MB200_INVALID_ARGUMENT, "need at least one row");  // sketch.cpp:71
+    if (d->rows > (unsigned)kMaxFamilies) return fail(MB200_UNSUPPORTED, "GPU path supports at most 16 rows");
+    if (d->k == 0) return fail(MB200_INVALID_ARGUMENT, "independence degree must be at least 1");
+    if (d->k > (unsigned)kMaxK) return fail(MB200_UNSUPPORTED, "GPU path supports independence <= 16");
+    if (d->b < 2 || d->b > 127) return fail(MB200_INVALID_ARGUMENT, "exponent must be in [2, 127]");
+    if (d->b > 61 && d->b != 89) return fail(MB200_UNSUPPORTED, "GPU path supports b <= 61 and b == 89");
+    if (d->width < 2) return fail(MB200_INVALID_ARGUMENT, "width must be at least 2");  // sketch.cpp:99
+    const bool pow2 = (d->width & (d->width - 1)) == 0;
+    switch (d->splitter) {
+        case MB200_SPLIT_POW2:
+        case MB200_SPLIT_TWO_FOR_ONE:
+            // sketch.cpp:101-107 (b >= 64 always admits a 64-bit width)
+            if (!pow2 || (d->b < 64 && d->width >= (1ull << d->b)))
+                return fail(MB200_INVALID_ARGUMENT, "width must be a power of two strictly inside the hash range");
+            break;
+        case MB200_SPLIT_UNIFORM_ARB:
+        case MB200_SPLIT_MERSENNE_ARB:
+            if (d->b < 64 && d->width > (1ull << (d->b - 1)))
+                return fail(MB200_INVALID_ARGUMENT, "width exceeds half the hash range");  // sketch.cpp:109-113
+            if (d->b > 64) return fail(MB200_UNSUPPORTED, "arbitrary-width splitters run for b <= 61 on the GPU");
+            break;
+        default:
+            return fail(MB200_INVALID_ARGUMENT, "unknown splitter");
+    }
+    if ((unsigned __int128)d->rows * d->width > ((unsigned __int128)1 << 34))
+        return fail(MB200_INVALID_ARGUMENT, "sketch dimensions too large");  // sketch.cpp:116-118
+    // key domain: polyhash.cpp:48-57 (p >= 2u - 1); b == 61 also admits full 64-bit keys
+    if (d->key_bits > 64) return fail(MB200_UNSUPPORTED, "keys wider than 64 bits");
+    if (d->b != 61 && d->b < 64 && d->key_bits > d->b - 1)
+        return fail(MB200_INVALID_ARGUMENT, "modulus too small for key domain");
+    const unsigned lw = (unsigned)__builtin_ctzll(d->width);
+    const unsigned families = d->splitter == MB200_SPLIT_TWO_FOR_ONE ? (d->rows + 1) / 2 : d->rows;
+    if (d->splitter == MB200_SPLIT_TWO_FOR_ONE) {
+        // row j uses index bits [l j, l j + l) and sign bit b-1-j (disjoint, in the low word)
+        if (2 * lw + 2 > d->b || 2 * lw > 64)
+            return fail(MB200_INVALID_ARGUMENT, "two-for-one split needs 2 log2(width) + 2 <= b");
+    }
+    if (families * d->k > (unsigned)kMaxCoeffs) return fail(MB200_UNSUPPORTED, "too many coefficients");
+    if (!d->coeffs_lo) return fail(MB200_INVALID_ARGUMENT, "null coefficients");
+    std::memset(&sp, 0, sizeof(sp));
+    sp.rows = d->rows;
+    sp.families = families;
+    sp.k = d->k;
+    sp.b = d->b;
+    sp.lw = lw;
+    sp.splitter = (uint32_t)d->splitter;
+    sp.width = d->width;
+    sp.p = d->b < 64 ? (1ull << d->b) - 1 : ~0ull;
+    for (unsigned i = 0; i < families * d->k; ++i) {
+        sp.lo[i] = d->coeffs_lo[i];
+        sp.hi[i] = d->coeffs_hi ? d->coeffs_hi[i] : 0;
+        const bool reduced = d->b < 64 ? sp.lo[i] < sp.p && sp.hi[i] == 0
+                                       : (sp.hi[i] < (1ull << (d->b - 64)) - 1) ||
+                                             (sp.hi[i] == (1ull << (d->b - 64)) - 1 && sp.lo[i] != ~0ull);
+        if (!reduced) return fail(MB200_INVALID_ARGUMENT, "coefficient not reduced");  // polyhash.cpp:43
+    }
+    return MB200_OK;
+}
+
+int cs_update_nocheck(const mb200_sketch_desc* desc, const void* d_keys, int key_width, const void* d_weights,
+                      int weight_kind, uint64_t n, int64_t* d_counters, void* stream) {
+    SketchParams sp;
+    if (int rc = build_sketch_params(desc, sp)) return rc;
+    if (n == 0) return MB200_OK;
+    cudaError_t e = launch_cs_update(sp, d_keys, key_width, d_weights, weight_kind, n, d_counters, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_cs_update");
+}
+
+}  // namespace mb200
+
+extern "C" {
+
+const char* mb200_last_error(void) { return g_last_error.c_str(); }
+int mb200_abi_version(void) { return MB200_ABI_VERSION; }
+
+int mb200_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int good = 0;
+    for (int d = 0; d < n; ++d) {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major == 10) ++good;
+    }
+    return good;
+}
+
+int mb200_mersenne_modulus_check(unsigned b, int require_prime) {
+    if (b < 2 || b > 127) return fail(MB200_INVALID_ARGUMENT, "exponent must be in [2, 127]");
+    if (require_prime && !prime_exponent(b))
+        return fail(MB200_INVALID_ARGUMENT, "2^b - 1 is not prime for this exponent");
+    return MB200_OK;
+}
+
+int mb200_hash61(const void* d_keys, int key_width, uint64_t n, unsigned b, const uint64_t* coeffs, unsigned k,
+                 unsigned key_bits, uint64_t* d_out, void* stream) {
+    if (b < 2 || b > 61) return fail(MB200_INVALID_ARGUMENT, "mb200_hash61 needs 2 <= b <= 61");
+    if (k == 0) return fail(MB200_INVALID_ARGUMENT, "independence degree must be at least 1");
+    if (k > (unsigned)kMaxK) return fail(MB200_UNSUPPORTED, "GPU path supports independence <= 16");
+    if (key_width != 32 && key_width != 64) return fail(MB200_INVALID_ARGUMENT, "key width must be 32 or 64");
+    if (key_bits > 64) return fail(MB200_INVALID_ARGUMENT, "key domain exceeds 64 bits");
+    if (b != 61 && key_bits > b - 1) return fail(MB200_INVALID_ARGUMENT, "modulus too small for key domain");
+    if (!coeffs) return fail(MB200_INVALID_ARGUMENT, "null coefficients");
+    HashParams hp;
+    std::memset(&hp, 0, sizeof(hp));
+    hp.b = b;
+    hp.k = k;
+    hp.p = (1ull << b) - 1;
+    for (unsigned i = 0; i < k; ++i) {
+        if (coeffs[i] >= hp.p) return fail(MB200_INVALID_ARGUMENT, "coefficient not reduced");
+        hp.lo[i] = coeffs[i];
+    }
+    if (n == 0) return MB200_OK;
+    if (!d_keys || !d_out) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = check_keys(d_keys, key_width, n, key_bits, s)) return rc;
+    cudaError_t e;
+    if (b == 61 && key_width == 32) e = launch_hash61_key32((const uint32_t*)d_keys, n, hp, d_out, s);
+    else if (b == 61) e = launch_hash61_key64((const uint64_t*)d_keys, n, hp, d_out, s);
+    else e = launch_hash_generic(d_keys, key_width, n, hp, d_out, s);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_hash61");
+}
+
+int mb200_hash89(const uint64_t* d_keys, uint64_t n, const uint64_t* coeffs_lo, const uint64_t* coeffs_hi,
+                 unsigned k, unsigned key_bits, uint64_t* d_out_lo, uint64_t* d_out_hi, void* stream) {
+    if (k == 0) return fail(MB200_INVALID_ARGUMENT, "independence degree must be at least 1");
+    if (k > (unsigned)kMaxK) return fail(MB200_UNSUPPORTED, "GPU path supports independence <= 16");
+    if (key_bits > 64) return fail(MB200_UNSUPPORTED, "keys wider than 64 bits");
+    if (!coeffs_lo || !coeffs_hi) return fail(MB200_INVALID_ARGUMENT, "null coefficients");
+    HashParams hp;
+    std::memset(&hp, 0, sizeof(hp));
+    hp.b = 89;
+    hp.k = k;
+    for (unsigned i = 0; i < k; ++i) {
+        const bool reduced = coeffs_hi[i] < (1ull << 25) - 1 || (coeffs_hi[i] == (1ull << 25) - 1 && coeffs_lo[i] != ~0ull);
+        if (!reduced) return fail(MB200_INVALID_ARGUMENT, "coefficient not reduced");
+        hp.lo[i] = coeffs_lo[i];
+        hp.hi[i] = coeffs_hi[i];
+    }
+    if (n == 0) return MB200_OK;
+    if (!d_keys || !d_out_lo || !d_out_hi) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = check_keys(d_keys, 64, n, key_bits, s)) return rc;
+    cudaError_t e = launch_hash89(d_keys, n, hp, d_out_lo, d_out_hi, s);
+    if (e == cudaErrorMisalignedAddress) return fail(MB200_INVALID_ARGUMENT, "mb200_hash89 needs 16-byte aligned buffers");
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_hash89");
+}
+
+int mb200_pm_divmod(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, unsigned m_iters, uint64_t* d_q,
+                    uint64_t* d_r, uint64_t* d_overflow, void* stream) {
+    if (b < 2 || b > 64) {
+        if (b >= 2 && b <= 127) return fail(MB200_UNSUPPORTED, "GPU division supports b <= 64");
+        return fail(MB200_INVALID_ARGUMENT, "width must be in [2, 127]");
+    }
+    unsigned m = 0;
+    uint64_t max_input[4];
+    if (int rc = mb200_pm_modulus(b, c, m_iters, &m, max_input)) return rc;
+    if (n == 0) return MB200_OK;
+    if (!d_v || !d_q || !d_r) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (max_input[2] == 0 && max_input[3] == 0) {  // domain narrower than u128: check
+        unsigned long long bad = 0;
+        int rc = count_on_device(
+            [&](unsigned long long* d, cudaStream_t st) {
+                return launch_count_above(d_v, n, max_input[0], max_input[1], d, st);
+            },
+            s, &bad);
+        if (rc) return rc;
+        if (bad) return fail(MB200_DOMAIN_ERROR, "input exceeds division domain for m iterations");  // field.cpp:262
+    }
+    unsigned long long* flags = reinterpret_cast<unsigned long long*>(d_overflow);
+    unsigned long long* scratch = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (!flags) {
+        e = cudaMallocAsync(&scratch, sizeof(*scratch), s);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+        flags = scratch;
+    }
+    e = launch_pm_divmod(d_v, n, b, c, m, d_q, d_r, flags, s);
+    if (scratch) cudaFreeAsync(scratch, s);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_pm_divmod");
+}
+
+int mb200_cs_update(const mb200_sketch_desc* desc, const void* d_keys, int key_width, const void* d_weights,
+                    int weight_kind, uint64_t n, int64_t* d_counters, void* stream) {
+    SketchParams sp;
+    if (int rc = build_sketch_params(desc, sp)) return rc;
+    if (key_width != 32 && key_width != 64) return fail(MB200_INVALID_ARGUMENT, "key width must be 32 or 64");
+    if (weight_kind != MB200_W_NONE && weight_kind != MB200_W_I32 && weight_kind != MB200_W_I64)
+        return fail(MB200_INVALID_ARGUMENT, "unknown weight kind");
+    if (weight_kind != MB200_W_NONE && !d_weights) return fail(MB200_INVALID_ARGUMENT, "null weights");
+    if (n == 0) return MB200_OK;
+    if (!d_keys || !d_counters) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = check_keys(d_keys, key_width, n, desc->key_bits, s)) return rc;
+    cudaError_t e = launch_cs_update(sp, d_keys, key_width, d_weights, weight_kind, n, d_counters, s);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_cs_update");
+}
+
+int mb200_cs_moments(const int64_t* d_counters, unsigned rows, uint64_t width, uint64_t* d_out, void* stream) {
+    if (!d_counters || !d_out) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaError_t e = launch_cs_moments(d_counters, rows, width, d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_cs_moments");
+}
+
+int mb200_cs_merge(int64_t* d_dst, const int64_t* d_src, uint64_t count, void* stream) {
+    if (count && (!d_dst || !d_src)) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaError_t e = launch_cs_merge(d_dst, d_src, count, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_cs_merge");
+}
+
+int mb200_cs_point_query(const mb200_sketch_desc* desc, const int64_t* d_counters, const void* d_keys, int key_width,
+                         uint64_t n, int64_t* d_out, void* stream) {
+    SketchParams sp;
+    if (int rc = build_sketch_params(desc, sp)) return rc;
+    if (key_width != 32 && key_width != 64) return fail(MB200_INVALID_ARGUMENT, "key width must be 32 or 64");
+    if (n == 0) return MB200_OK;
+    if (!d_keys || !d_counters || !d_out) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = check_keys(d_keys, key_width, n, desc->key_bits, s)) return rc;
+    cudaError_t e = launch_cs_point_query(sp, d_counters, d_keys, key_width, n, d_out, s);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_cs_point_query");
+}
+
+// ---------------------------------------------------------------- generators
+int mb200_gen_u32_keys(uint64_t seed, uint64_t start, uint64_t n, uint32_t* d_out, void* stream) {
+    cudaError_t e = launch_gen_u32(seed, start, n, d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "gen");
+}
+int mb200_gen_u64_keys(uint64_t seed, uint64_t start, uint64_t n, uint64_t* d_out, void* stream) {
+    cudaError_t e = launch_gen_u64(seed, start, n, d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "gen");
+}
+int mb200_gen_below_p61(uint64_t seed, uint64_t start, uint64_t n, uint64_t* d_out, uint64_t* d_bad, void* stream) {
+    cudaError_t e = launch_gen_below_p61(seed, start, n, d_out, (unsigned long long*)d_bad, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "gen");
+}
+int mb200_gen_pm_inputs(uint64_t seed, uint64_t c, uint64_t start, uint64_t n, uint64_t* d_out, uint64_t* d_bad,
+                        void* stream) {
+    cudaError_t e = launch_gen_pm_inputs(seed, c, start, n, d_out, (unsigned long long*)d_bad, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "gen");
+}
+
+int mb200_zipf_table(double alpha, uint32_t T, double universe, uint64_t* h_cdf, double* tail_c1) {
+    if (alpha != 1.2) return fail(MB200_UNSUPPORTED, "zipf generator implements alpha = 1.2 (tail exponent 5)");
+    if (T < 2 || !h_cdf || !tail_c1) return fail(MB200_INVALID_ARGUMENT, "bad zipf table arguments");
+    double head = 0;
+    for (uint32_t r = 1; r <= T; ++r) head += std::pow((double)r, -alpha);
+    const double tail = (std::pow(T + 0.5, 1 - alpha) - std::pow(universe + 0.5, 1 - alpha)) / (alpha - 1);
+    const double total = head + tail;
+    double acc = 0;
+    for (uint32_t r = 1; r <= T; ++r) {
+        acc += std::pow((double)r, -alpha);
+        const double sc = (acc / total) * 18446744073709551616.0;
+        h_cdf[r - 1] = sc >= 18446744073709551615.0 ? ~0ull : (sc <= 0 ? 0 : (uint64_t)sc);
+    }
+    *tail_c1 = 1.0 - std::pow((universe + 0.5) / (T + 0.5), 1 - alpha);
+    return MB200_OK;
+}
+
+int mb200_gen_zipf_items(uint64_t master_seed, const uint64_t* d_cdf, uint32_t T, double tail_c1, double universe,
+                         uint64_t start, uint64_t n, uint32_t* d_keys, int32_t* d_weights, void* stream) {
+    cudaError_t e = launch_gen_zipf(master_seed, d_cdf, T, tail_c1, universe, start, n, d_keys, d_weights,
+                                    (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "gen");
+}
+
+int mb200_probe_imad(int blocks, int threads, int iters, uint64_t* d_sink, void* stream) {
+    cudaError_t e = launch_probe_imad(blocks, threads, iters, d_sink, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "probe");
+}
+int mb200_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* d_buf, uint64_t span, void* stream) {
+    cudaError_t e = launch_probe_atomics(mode, blocks, threads, iters, d_buf, span, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "probe");
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// kernels_probe.cu -- microbenchmarks that measure the roofline denominators
+// this path needs and MEASURED_PEAKS.json does not carry ("measured
+// peak IMAD.WIDE.U32 rate ... microbenchmark it on the same box"), plus the
+// atomic throughputs that decide the Count Sketch privatisation strategy.
+#include "mb200_device.cuh"
+#include "mb200_internal.h"
+#include "mb200_mem.cuh"
+
+namespace mb200 {
+
+namespace {
+
+constexpr int kChains = 8;
+
+// kChains independent mad.wide.u32 accumulation chains per thread.
+__global__ void probe_imad_kernel(int iters, u64* sink) {
+    u64 acc[kChains];
+    const u32 a = threadIdx.x | 1u;
+    const u32 b = blockIdx.x * 2654435761u + 12345u;
+#pragma unroll
+    for (int j = 0; j < kChains; ++j) acc[j] = j;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < kChains; ++j)
+            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc[j]) : "r"(a + (u32)j), "r"(b));
+    }
+    u64 s = 0;
+#pragma unroll
+    for (int j = 0; j < kChains; ++j) s ^= acc[j];
+    if (s == 0x123456789ull) sink[0] = s;
+}
+
+__device__ __forceinline__ u32 scramble(u32 x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
+// mode 0: shared red.u64 on random cells of a 4096-entry table
+// mode 1: shared red.u32 on random cells
+// mode 2: global red.u64 on random cells of [0, span)
+// mode 3: global red.u64, every thread the same cell (worst-case hot key)
+// mode 4: global red.u64, warp-aggregated hot cell (one red per warp)
+__global__ void probe_atomics_kernel(int mode, int iters, u64* buf, u64 span) {
+    __shared__ unsigned long long t64[4096];
+    __shared__ unsigned t32[4096];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) {
+        t64[i] = 0;
+        t32[i] = 0;
+    }
+    __syncthreads();
+    u32 h = scramble(blockIdx.x * blockDim.x + threadIdx.x);
+    for (int i = 0; i < iters; ++i) {
+        h = scramble(h + i);
+        switch (mode) {
+            case 0: atomicAdd(&t64[h & 4095], 1ull); break;
+            case 1: atomicAdd(&t32[h & 4095], 1u); break;
+            case 2: red_add_u64(buf + (h % span), 1); break;
+            case 3: red_add_u64(buf, 1); break;
+            default:
+                if ((threadIdx.x & 31) == 0) red_add_u64(buf, 32);
+                break;
+        }
+    }
+    __syncthreads();
+    if (mode <= 1 && threadIdx.x == 0) buf[blockIdx.x % span] += t64[0] + t32[0];
+}
+
+}  // namespace
+
+cudaError_t launch_probe_imad(int blocks, int threads, int iters, uint64_t* sink, cudaStream_t s) {
+    probe_imad_kernel<<<blocks, threads, 0, s>>>(iters, sink);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* buf, uint64_t span,
+                                 cudaStream_t s) {
+    probe_atomics_kernel<<<blocks, threads, 0, s>>>(mode, iters, buf, span ? span : 1);
+    return cudaGetLastError();
+}
+
+}  // namespace mb200

@@ -1,0 +1,461 @@
+// kernels_sketch.cu -- K3 + K4 (fused hash -> two-for-one split -> Count
+// Sketch scatter-add), K5 (exact 128-bit second-moment estimator), merge and
+// point query.
+//
+// Reference: CountSketch::process sketch.cpp:133-140 (per row: h = family(x);
+// (i, s) = split(h); c[row][i] += s * delta, wrapping u64), split_pow2
+// sketch.cpp:13-19, row_second_moment sketch.cpp:142-158, merge :182-193,
+// point_query :170-180.
+//
+// HBM layout: counters i64 [rows][width] row-major, exactly the reference's
+// counters_ vector (sketch.hpp:75), so a D2H copy is byte-identical to it.
+//
+// Strategies (chosen by the launcher from the table size):
+//   SMEM32 / SMEM64 : the whole table privatised per CTA in shared memory
+//                     (config 1: 1 x 1024), shared atomics, one merge of the
+//                     non-zero counters into HBM per CTA at the end.
+//   GLOBAL          : tables larger than shared memory (configs 4, 5: 1 MiB,
+//                     2.5 MiB, L2-resident): fire-and-forget red.global.add.u64,
+//                     optionally preceded by warp-level aggregation of equal
+//                     keys (__match_any_sync) so heavy hitters of a skewed
+//                     stream cost one hash + one red per warp, not per item.
+// Integer addition is associative and commutative, so every strategy and every
+// grid produces bit-identical tables (the reference's merge-equals-
+// concatenation property, test_sketch.cpp:239-261).
+#include "mb200_device.cuh"
+#include "mb200_internal.h"
+#include "mb200_mem.cuh"
+
+namespace mb200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kSlots = 4;  // items per lane per warp-iteration (loads in flight)
+constexpr unsigned kFull = 0xffffffffu;
+
+enum Mode { M61_K32 = 0, M61_K64 = 1, M89 = 2, MGEN = 3 };
+enum Strat { SMEM32 = 0, SMEM64 = 1, GLOBAL = 2 };
+
+template <typename T>
+__device__ __forceinline__ T ld_nc(const T* p) {
+    return __ldcs(p);
+}
+
+// 61-bit (or <= 61-bit generic) hash of family f, fully reduced.
+template <int MODE, int K>
+__device__ __forceinline__ u64 hash_small(const SketchParams& sp, uint32_t f, u64 x) {
+    const u64* c = sp.lo + (size_t)f * sp.k;
+    if (MODE == M61_K32) {
+        const u32 xs = (u32)x;
+        if (K > 0) {
+            u64 y = c[K - 1];
+#pragma unroll
+            for (int i = K - 2; i >= 0; --i) y = h61_step32(y, xs, c[i]);
+            return h61_finish(y);
+        }
+        u64 y = c[sp.k - 1];
+#pragma unroll 1
+        for (int i = (int)sp.k - 2; i >= 0; --i) y = h61_step32(y, xs, c[i]);
+        return h61_finish(y);
+    } else if (MODE == M61_K64) {
+        const u64 xr = h61_key64(x);
+        if (K > 0) {
+            u64 y = c[K - 1];
+#pragma unroll
+            for (int i = K - 2; i >= 0; --i) y = h61_step64(y, xr, c[i]);
+            return h61_finish(y);
+        }
+        u64 y = c[sp.k - 1];
+#pragma unroll 1
+        for (int i = (int)sp.k - 2; i >= 0; --i) y = h61_step64(y, xr, c[i]);
+        return h61_finish(y);
+    } else {
+        u64 y = c[sp.k - 1];
+#pragma unroll 1
+        for (int i = (int)sp.k - 2; i >= 0; --i) y = hgen_step(y, x, c[i], sp.b, sp.p);
+        return hgen_finish(y, sp.b, sp.p);
+    }
+}
+
+// 89-bit hash of family f as (lo 64 bits, hi 25 bits).
+template <int K>
+__device__ __forceinline__ void hash89(const SketchParams& sp, uint32_t f, u64 x, u64& lo, u64& hi) {
+    const u64* cl = sp.lo + (size_t)f * sp.k;
+    const u64* ch = sp.hi + (size_t)f * sp.k;
+    const int k = K > 0 ? K : (int)sp.k;
+    u32 y0 = lo32(cl[k - 1]), y1 = hi32(cl[k - 1]), y2 = lo32(ch[k - 1]);
+    const u32 x0 = lo32(x), x1 = hi32(x);
+    if (K > 0) {
+#pragma unroll
+        for (int i = K - 2; i >= 0; --i)
+            h89_step(y0, y1, y2, x0, x1, lo32(cl[i]), hi32(cl[i]), lo32(ch[i]));
+    } else {
+#pragma unroll 1
+        for (int i = k - 2; i >= 0; --i)
+            h89_step(y0, y1, y2, x0, x1, lo32(cl[i]), hi32(cl[i]), lo32(ch[i]));
+    }
+    h89_finish(y0, y1, y2);
+    lo = ((u64)y1 << 32) | y0;
+    hi = y2;
+}
+
+// Alg 2 and the arbitrary-width splitters on a hash h < 2^b (b <= 64 path).
+// Returns the counter index within the row and writes the sign bit
+// (1 means "subtract delta").
+__device__ __forceinline__ u64 split_small(const SketchParams& sp, u64 h, uint32_t sub, bool& neg) {
+    const u32 b = sp.b;
+    switch (sp.splitter) {
+        case SPLIT_POW2:  // sketch.cpp:13-19: index = low l bits, sign = 1 - 2 * top bit
+            neg = (h >> (b - 1)) & 1;
+            return h & (sp.width - 1);
+        case SPLIT_TWO_FOR_ONE:  // bits [l sub, l sub + l), sign bit b-1-sub
+            neg = (h >> (b - 1 - sub)) & 1;
+            return (h >> (sp.lw * sub)) & (sp.width - 1);
+        default: {  // sketch.cpp:21-34: j = low b-1 bits (+1 for Mersenne), (j r) >> (b-1)
+            u64 hh = h + (sp.splitter == SPLIT_MERSENNE_ARB ? 1 : 0);
+            neg = !((hh >> (b - 1)) & 1);  // sign = 2a - 1: top bit set -> +1
+            const u64 j = hh & ((1ull << (b - 1)) - 1);
+            const u64 plo = j * sp.width, phi = __umul64hi(j, sp.width);
+            const u32 s = b - 1;
+            return (phi << (64 - s)) | (plo >> s);
+        }
+    }
+}
+
+__device__ __forceinline__ u64 split89(const SketchParams& sp, u64 lo, u64 hi, uint32_t sub, bool& neg) {
+    // b = 89: sign bit 88 - sub lives in the high word (bits 64..88)
+    if (sp.splitter == SPLIT_POW2) {
+        neg = (hi >> 24) & 1;
+        return lo & (sp.width - 1);
+    }
+    neg = (hi >> (24 - sub)) & 1;
+    return (lo >> (sp.lw * sub)) & (sp.width - 1);
+}
+
+template <int WK>
+__device__ __forceinline__ i64 load_weight(const void* w, uint64_t i) {
+    if (WK == W_NONE) return 1;
+    if (WK == W_I32) return (i64)ld_nc(reinterpret_cast<const i32*>(w) + i);
+    return ld_nc(reinterpret_cast<const i64*>(w) + i);
+}
+
+template <int STRAT>
+__device__ __forceinline__ void table_add(void* smem, i64* table, u64 cell, u64 sd) {
+    if (STRAT == SMEM32) {
+        atomicAdd(reinterpret_cast<unsigned*>(smem) + cell, (unsigned)sd);
+    } else if (STRAT == SMEM64) {
+        red_add_shared_u64(reinterpret_cast<uint64_t*>(smem) + cell, sd);
+    } else {
+        red_add_u64(reinterpret_cast<uint64_t*>(table) + cell, sd);
+    }
+}
+
+// One item: every family, every sub-row.  delta is applied with the
+// reference's wrapping sign convention (sketch.cpp:136-138).
+template <int MODE, int K, int STRAT>
+__device__ __forceinline__ void process_item(const SketchParams& sp, u64 x, i64 delta, void* smem,
+                                             i64* table) {
+    const u64 d = (u64)delta;
+    if (MODE == M89) {
+        const uint32_t subs = sp.splitter == SPLIT_TWO_FOR_ONE ? 2 : 1;
+#pragma unroll 1
+        for (uint32_t f = 0; f < sp.families; ++f) {
+            u64 hlo, hhi;
+            hash89<K>(sp, f, x, hlo, hhi);
+            for (uint32_t s = 0; s < subs; ++s) {
+                const uint32_t row = subs * f + s;
+                if (row >= sp.rows) break;
+                bool neg;
+                const u64 idx = split89(sp, hlo, hhi, s, neg);
+                table_add<STRAT>(smem, table, (u64)row * sp.width + idx, neg ? (0ull - d) : d);
+            }
+        }
+    } else {
+        if (sp.splitter == SPLIT_TWO_FOR_ONE) {
+#pragma unroll 1
+            for (uint32_t f = 0; f < sp.families; ++f) {
+                const u64 h = hash_small<MODE, K>(sp, f, x);
+                for (uint32_t s = 0; s < 2; ++s) {
+                    const uint32_t row = 2 * f + s;
+                    if (row >= sp.rows) break;
+                    bool neg;
+                    const u64 idx = split_small(sp, h, s, neg);
+                    table_add<STRAT>(smem, table, (u64)row * sp.width + idx, neg ? (0ull - d) : d);
+                }
+            }
+        } else {
+#pragma unroll 1
+            for (uint32_t f = 0; f < sp.families; ++f) {
+                const u64 h = hash_small<MODE, K>(sp, f, x);
+                bool neg;
+                const u64 idx = split_small(sp, h, 0, neg);
+                table_add<STRAT>(smem, table, (u64)f * sp.width + idx, neg ? (0ull - d) : d);
+            }
+        }
+    }
+}
+
+template <int MODE, int K, typename KeyT, int WK, int STRAT>
+__global__ void __launch_bounds__(kThreads) cs_update_kernel(const SketchParams sp,
+                                                             const KeyT* __restrict__ keys,
+                                                             const void* __restrict__ w, uint64_t n,
+                                                             i64* __restrict__ table, int aggregate) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ i64 scratch[kWarps][32];
+    void* smem = smem_raw;
+    const uint64_t cells = (uint64_t)sp.rows * sp.width;
+    if (STRAT != GLOBAL) {
+        const uint64_t words = STRAT == SMEM32 ? cells : 2 * cells;
+        for (uint64_t i = threadIdx.x; i < words; i += kThreads) reinterpret_cast<u32*>(smem)[i] = 0;
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t warps_total = (uint64_t)gridDim.x * kWarps;
+    const uint64_t gw = (uint64_t)blockIdx.x * kWarps + warp;
+    const uint64_t tile = 32ull * kSlots;
+    for (uint64_t base = gw * tile; base < n; base += warps_total * tile) {
+        KeyT kx[kSlots];
+        i64 dx[kSlots];
+#pragma unroll
+        for (int u = 0; u < kSlots; ++u) {
+            const uint64_t i = base + u * 32 + lane;
+            kx[u] = i < n ? ld_nc(keys + i) : KeyT(0);
+            dx[u] = i < n ? load_weight<WK>(w, i) : 0;
+        }
+#pragma unroll 1
+        for (int u = 0; u < kSlots; ++u) {
+            const uint64_t i = base + u * 32 + lane;
+            const bool valid = i < n;
+            if (STRAT == GLOBAL && aggregate) {
+                const unsigned vmask = __ballot_sync(kFull, valid);
+                if (valid) {
+                    const unsigned peers = __match_any_sync(vmask, kx[u]);
+                    const int leader = __ffs(peers) - 1;
+                    i64 d = dx[u];
+                    if (__popc(peers) > 1) {
+                        scratch[warp][lane] = d;
+                        __syncwarp(peers);
+                        if (lane == leader) {
+                            u64 s = 0;
+                            for (unsigned m = peers; m; m &= m - 1) s += (u64)scratch[warp][__ffs(m) - 1];
+                            d = (i64)s;
+                        }
+                        __syncwarp(peers);
+                    }
+                    if (lane == leader) process_item<MODE, K, STRAT>(sp, (u64)kx[u], d, smem, table);
+                }
+            } else if (valid) {
+                process_item<MODE, K, STRAT>(sp, (u64)kx[u], dx[u], smem, table);
+            }
+        }
+    }
+    if (STRAT != GLOBAL) {
+        __syncthreads();
+        for (uint64_t c = threadIdx.x; c < cells; c += kThreads) {
+            u64 v;
+            if (STRAT == SMEM32) v = (u64)(i64)(i32)reinterpret_cast<u32*>(smem)[c];
+            else v = reinterpret_cast<u64*>(smem)[c];
+            if (v) red_add_u64(reinterpret_cast<uint64_t*>(table) + c, v);
+        }
+    }
+}
+
+// ---- K5: exact sum of squares per row, 192-bit accumulation ------------------
+struct U192 {
+    u64 w0, w1, w2;
+};
+__device__ __forceinline__ void add192(U192& a, u64 b0, u64 b1, u64 b2) {
+    asm("add.cc.u64  %0, %0, %3;\n\t"
+        "addc.cc.u64 %1, %1, %4;\n\t"
+        "addc.u64    %2, %2, %5;"
+        : "+l"(a.w0), "+l"(a.w1), "+l"(a.w2)
+        : "l"(b0), "l"(b1), "l"(b2));
+}
+
+__global__ void __launch_bounds__(1024) cs_moments_kernel(const i64* __restrict__ table, uint64_t width,
+                                                          u64* __restrict__ out) {
+    const uint32_t row = blockIdx.x;
+    const i64* base = table + (uint64_t)row * width;
+    U192 acc = {0, 0, 0};
+    for (uint64_t i = threadIdx.x; i < width; i += blockDim.x) {
+        const i64 c = base[i];
+        const u64 mag = c < 0 ? 0ull - (u64)c : (u64)c;  // sketch.cpp:149 (INT64_MIN-safe)
+        add192(acc, mag * mag, __umul64hi(mag, mag), 0);
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const u64 b0 = __shfl_xor_sync(kFull, acc.w0, off);
+        const u64 b1 = __shfl_xor_sync(kFull, acc.w1, off);
+        const u64 b2 = __shfl_xor_sync(kFull, acc.w2, off);
+        add192(acc, b0, b1, b2);
+    }
+    __shared__ U192 part[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) part[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        U192 t = {0, 0, 0};
+        for (int wdx = 0; wdx < (int)(blockDim.x >> 5); ++wdx) add192(t, part[wdx].w0, part[wdx].w1, part[wdx].w2);
+        // sketch.cpp:150-154: saturate at 2^128 - 1 and flag it
+        const bool sat = t.w2 != 0;
+        out[4 * row + 0] = sat ? ~0ull : t.w0;
+        out[4 * row + 1] = sat ? ~0ull : t.w1;
+        out[4 * row + 2] = sat ? 1 : 0;
+        out[4 * row + 3] = 0;
+    }
+}
+
+__global__ void cs_merge_kernel(u64* __restrict__ dst, const u64* __restrict__ src, uint64_t count) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
+        dst[i] += src[i];  // sketch.cpp:189-191, wrapping
+}
+
+// point_query: lower median over rows of sign * counter (sketch.cpp:170-180)
+template <int MODE, typename KeyT>
+__global__ void cs_point_query_kernel(const SketchParams sp, const i64* __restrict__ table,
+                                      const KeyT* __restrict__ keys, uint64_t n, i64* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const u64 x = (u64)keys[i];
+        i64 est[kMaxFamilies * 2];
+        uint32_t ne = 0;
+        for (uint32_t f = 0; f < sp.families; ++f) {
+            const uint32_t subs = sp.splitter == SPLIT_TWO_FOR_ONE ? 2 : 1;
+            u64 hlo = 0, hhi = 0;
+            if (MODE == M89) hash89<0>(sp, f, x, hlo, hhi);
+            else hlo = hash_small<MODE, 0>(sp, f, x);
+            for (uint32_t s = 0; s < subs; ++s) {
+                const uint32_t row = subs * f + s;
+                if (row >= sp.rows) break;
+                bool neg;
+                const u64 idx = MODE == M89 ? split89(sp, hlo, hhi, s, neg) : split_small(sp, hlo, s, neg);
+                const i64 c = table[(u64)row * sp.width + idx];
+                est[ne++] = neg ? (i64)(0ull - (u64)c) : c;
+            }
+        }
+        for (uint32_t a = 1; a < ne; ++a) {  // insertion sort, ne <= 32
+            const i64 v = est[a];
+            int j = (int)a - 1;
+            while (j >= 0 && est[j] > v) {
+                est[j + 1] = est[j];
+                --j;
+            }
+            est[j + 1] = v;
+        }
+        out[i] = est[(ne - 1) / 2];
+    }
+}
+
+int blocks_per_sm_cache(const void* fn, size_t smem) {
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, kThreads, smem);
+    return v > 0 ? v : 1;
+}
+
+template <int MODE, int K, typename KeyT, int WK, int STRAT>
+cudaError_t launch_strat(const SketchParams& sp, const void* keys, const void* w, uint64_t n, int64_t* table,
+                         cudaStream_t s, bool aggregate) {
+    auto fn = cs_update_kernel<MODE, K, KeyT, WK, STRAT>;
+    const uint64_t cells = (uint64_t)sp.rows * sp.width;
+    const size_t smem = STRAT == GLOBAL ? 0 : (size_t)cells * (STRAT == SMEM32 ? 4 : 8);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int per_sm = blocks_per_sm_cache((const void*)fn, smem);
+    const uint64_t tile = 32ull * kSlots * kWarps;
+    uint64_t grid = (n + tile - 1) / tile;
+    const uint64_t cap = (uint64_t)sm_count() * per_sm;
+    if (grid > cap) grid = cap;
+    if (grid == 0) grid = 1;
+    fn<<<(unsigned)grid, kThreads, smem, s>>>(sp, (const KeyT*)keys, w, n, table, aggregate ? 1 : 0);
+    return cudaGetLastError();
+}
+
+template <int MODE, int K, typename KeyT, int WK>
+cudaError_t launch_w(const SketchParams& sp, const void* keys, const void* w, uint64_t n, int64_t* table,
+                     cudaStream_t s) {
+    const uint64_t cells = (uint64_t)sp.rows * sp.width;
+    // 32-bit private counters are exact when every increment is +-1 and a CTA
+    // sees fewer than 2^31 items; 64-bit otherwise.
+    if (WK == W_NONE && cells * 4 <= 64 * 1024 && n < (1ull << 31))
+        return launch_strat<MODE, K, KeyT, WK, SMEM32>(sp, keys, w, n, table, s, false);
+    if (cells * 8 <= 64 * 1024) return launch_strat<MODE, K, KeyT, WK, SMEM64>(sp, keys, w, n, table, s, false);
+    // aggregation pays off for weighted (typically skewed) streams
+    return launch_strat<MODE, K, KeyT, WK, GLOBAL>(sp, keys, w, n, table, s, WK != W_NONE);
+}
+
+template <int MODE, int K, typename KeyT>
+cudaError_t launch_k(const SketchParams& sp, const void* keys, const void* w, int w_kind, uint64_t n,
+                     int64_t* table, cudaStream_t s) {
+    switch (w_kind) {
+        case W_NONE: return launch_w<MODE, K, KeyT, W_NONE>(sp, keys, w, n, table, s);
+        case W_I32: return launch_w<MODE, K, KeyT, W_I32>(sp, keys, w, n, table, s);
+        case W_I64: return launch_w<MODE, K, KeyT, W_I64>(sp, keys, w, n, table, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int MODE, typename KeyT>
+cudaError_t launch_mode(const SketchParams& sp, const void* keys, const void* w, int w_kind, uint64_t n,
+                        int64_t* table, cudaStream_t s) {
+    if (MODE != MGEN && sp.k == 4) return launch_k<MODE, 4, KeyT>(sp, keys, w, w_kind, n, table, s);
+    return launch_k<MODE, 0, KeyT>(sp, keys, w, w_kind, n, table, s);
+}
+
+}  // namespace
+
+cudaError_t launch_cs_update(const SketchParams& sp, const void* keys, int key_width, const void* w,
+                             int w_kind, uint64_t n, int64_t* table, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (sp.b == 89) {
+        if (key_width == 32) return launch_mode<M89, u32>(sp, keys, w, w_kind, n, table, s);
+        return launch_mode<M89, u64>(sp, keys, w, w_kind, n, table, s);
+    }
+    if (sp.b == 61) {
+        if (key_width == 32) return launch_mode<M61_K32, u32>(sp, keys, w, w_kind, n, table, s);
+        return launch_mode<M61_K64, u64>(sp, keys, w, w_kind, n, table, s);
+    }
+    if (sp.b > 61) return cudaErrorInvalidValue;
+    if (key_width == 32) return launch_mode<MGEN, u32>(sp, keys, w, w_kind, n, table, s);
+    return launch_mode<MGEN, u64>(sp, keys, w, w_kind, n, table, s);
+}
+
+cudaError_t launch_cs_moments(const int64_t* table, uint32_t rows, uint64_t width, uint64_t* out,
+                              cudaStream_t s) {
+    if (rows == 0) return cudaSuccess;
+    cs_moments_kernel<<<rows, 1024, 0, s>>>(table, width, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cs_merge(int64_t* dst, const int64_t* src, uint64_t count, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    uint64_t grid = (count + 255) / 256;
+    if (grid > (uint64_t)sm_count() * 8) grid = (uint64_t)sm_count() * 8;
+    cs_merge_kernel<<<(unsigned)grid, 256, 0, s>>>((u64*)dst, (const u64*)src, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cs_point_query(const SketchParams& sp, const int64_t* table, const void* keys, int key_width,
+                                  uint64_t n, int64_t* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    uint64_t grid = (n + 255) / 256;
+    if (grid > (uint64_t)sm_count() * 8) grid = (uint64_t)sm_count() * 8;
+    const unsigned g = (unsigned)grid;
+    if (sp.b == 89) {
+        if (key_width == 32) cs_point_query_kernel<M89, u32><<<g, 256, 0, s>>>(sp, table, (const u32*)keys, n, out);
+        else cs_point_query_kernel<M89, u64><<<g, 256, 0, s>>>(sp, table, (const u64*)keys, n, out);
+    } else if (sp.b == 61) {
+        if (key_width == 32) cs_point_query_kernel<M61_K32, u32><<<g, 256, 0, s>>>(sp, table, (const u32*)keys, n, out);
+        else cs_point_query_kernel<M61_K64, u64><<<g, 256, 0, s>>>(sp, table, (const u64*)keys, n, out);
+    } else {
+        if (key_width == 32) cs_point_query_kernel<MGEN, u32><<<g, 256, 0, s>>>(sp, table, (const u32*)keys, n, out);
+        else cs_point_query_kernel<MGEN, u64><<<g, 256, 0, s>>>(sp, table, (const u64*)keys, n, out);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace mb200

@@ -1,0 +1,155 @@
+// mb200_device.cuh -- register-level integer arithmetic for sm_100a.
+//
+// Every multi-word product is built from 32x32->64 limb products
+// (mul.wide.u32 -> IMAD.WIDE.U32) and every reduction is a branch-free
+// shift/mask/add fold.  No u128 emulation from the compiler, no division.
+//
+// Reference semantics being reproduced (file:line under /root/reference/proj):
+//   Alg 1 Horner mod 2^61-1   polyhash.cpp:64-76
+//   Alg 1 Horner mod 2^89-1   polyhash.cpp:78-88, field.hpp:66-73
+//   Alg 2 two-for-one split   sketch.cpp:13-19
+//   Alg 4/5 pseudo-Mersenne   field.cpp:246-273
+#pragma once
+#include <cstdint>
+
+namespace mb200 {
+
+typedef uint64_t u64;
+typedef uint32_t u32;
+typedef int64_t i64;
+typedef int32_t i32;
+
+constexpr u64 kP61 = (1ull << 61) - 1;
+constexpr u32 kP89Top = (1u << 25) - 1;  // limb 2 of 2^89-1 (bits 64..88)
+
+__device__ __forceinline__ u64 mulw(u32 a, u32 b) { return (u64)a * (u64)b; }
+__device__ __forceinline__ u32 lo32(u64 v) { return (u32)v; }
+__device__ __forceinline__ u32 hi32(u64 v) { return (u32)(v >> 32); }
+
+// ---------------------------------------------------------------------------
+// p = 2^61 - 1, 32-bit keys (the reference's classic setup, bench.cpp:54-58).
+// One Horner step y <- y x + a, lazily reduced:
+//   in  y < 2^63, x < 2^32, a < p
+//   out (yx & p) + (yx >> 61) + a  <  2^61 + 2^34 + 2^61  <  2^63   (closed)
+// Two limb products (IMAD.WIDE.U32), ~5 ALU ops.
+__device__ __forceinline__ u64 h61_step32(u64 y, u32 x, u64 a) {
+    const u64 p0 = mulw(lo32(y), x);                 // bits 0..63 of y0 x
+    const u64 p1 = mulw(hi32(y), x) + (p0 >> 32);    // y x >> 32, < 2^63 + 2^32
+    const u64 lo = (((p1 << 32) | lo32(p0))) & kP61; // (y x) & p
+    const u64 hi = p1 >> 29;                         // (y x) >> 61
+    return lo + hi + a;
+}
+
+// Full reduction of a lazily reduced value y < 2^63 to [0, p): one fold to
+// < 2^61 + 4 < 2p, then the reference's branch-free finish
+// z = (y + 1) >> b; (y + z) & p   (polyhash.cpp:74-75).
+__device__ __forceinline__ u64 h61_finish(u64 y) {
+    y = (y & kP61) + (y >> 61);
+    const u64 z = (y + 1) >> 61;
+    return (y + z) & kP61;
+}
+
+// ---------------------------------------------------------------------------
+// p = 2^61 - 1, any 64-bit key (config 2 draws keys from [0, p), beyond the
+// reference's u <= 2^60 domain; SURVEY 7.3 hard part 2).  Keys are folded once
+// to x < 2^61 + 8; the step keeps y < 2^62 with a second (3-bit) fold:
+//   in  y < 2^62, x < 2^61 + 8, a < p;  y x < 2^123.02
+//   s = (yx & p) + (yx >> 61) + a < 2^63.02;  out (s & p) + (s >> 61) < 2^61 + 8
+// Four limb products.
+__device__ __forceinline__ u64 h61_key64(u64 x) { return (x & kP61) + (x >> 61); }
+
+__device__ __forceinline__ u64 h61_step64(u64 y, u64 x, u64 a) {
+    const u32 y0 = lo32(y), y1 = hi32(y), x0 = lo32(x), x1 = hi32(x);
+    const u64 A = mulw(y0, x0);
+    const u64 B = mulw(y0, x1) + (A >> 32);
+    const u64 Cc = mulw(y1, x0) + (u64)lo32(B);
+    const u64 D = mulw(y1, x1) + (B >> 32) + (Cc >> 32);  // y x >> 64
+    const u64 tlo = (Cc << 32) | lo32(A);                  // y x mod 2^64
+    const u64 s = (tlo & kP61) + ((D << 3) | (tlo >> 61)) + a;
+    return (s & kP61) + (s >> 61);
+}
+
+// ---------------------------------------------------------------------------
+// Generic Mersenne p = 2^b - 1 with b <= 61 and runtime b, valid on the
+// reference's domain x < u <= 2^(b-1) (polyhash.cpp:48-57): exactly the
+// reference's native Horner (u128 t = y x + a; y = (t & p) + (t >> b);
+// invariant y < 2p), the u128 built from two 64-bit halves.
+__device__ __forceinline__ u64 hgen_step(u64 y, u64 x, u64 a, u32 b, u64 p) {
+    const u64 lo = y * x;
+    u64 hi = __umul64hi(y, x);
+    const u64 tl = lo + a;
+    hi += (tl < lo);
+    return (tl & p) + ((hi << (64 - b)) | (tl >> b));
+}
+__device__ __forceinline__ u64 hgen_finish(u64 y, u32 b, u64 p) {
+    const u64 z = (y + 1) >> b;  // y < 2p: the carry is the top bit
+    return (y + z) & p;
+}
+
+// ---------------------------------------------------------------------------
+// p = 2^89 - 1 on 32-bit limbs (y0,y1,y2), y < 2p (y2 < 2^26), x < 2^64,
+// a < p.  t = y x + a < 2^154 + 2^89 in five limbs via a PTX carry chain
+// (six limb products, each a mad.lo/mad.hi pair), then the reference's single
+// partial fold (t & p) + (t >> 89) < 2^89 + 2^65 < 2p (field.hpp:66-73).
+__device__ __forceinline__ void h89_step(u32& y0, u32& y1, u32& y2, u32 x0, u32 x1, u32 a0,
+                                         u32 a1, u32 a2) {
+    u32 t0, t1, t2, t3, t4;
+    asm("mad.lo.cc.u32  %0, %5, %8, %10;\n\t"
+        "madc.lo.cc.u32 %1, %6, %8, %11;\n\t"
+        "madc.lo.cc.u32 %2, %7, %8, %12;\n\t"
+        "addc.u32       %3, 0, 0;\n\t"
+        "mad.hi.cc.u32  %1, %5, %8, %1;\n\t"
+        "madc.hi.cc.u32 %2, %6, %8, %2;\n\t"
+        "madc.hi.u32    %3, %7, %8, %3;\n\t"
+        "mad.lo.cc.u32  %1, %5, %9, %1;\n\t"
+        "madc.lo.cc.u32 %2, %6, %9, %2;\n\t"
+        "madc.lo.cc.u32 %3, %7, %9, %3;\n\t"
+        "addc.u32       %4, 0, 0;\n\t"
+        "mad.hi.cc.u32  %2, %5, %9, %2;\n\t"
+        "madc.hi.cc.u32 %3, %6, %9, %3;\n\t"
+        "madc.hi.u32    %4, %7, %9, %4;"
+        : "=&r"(t0), "=&r"(t1), "=&r"(t2), "=&r"(t3), "=&r"(t4)
+        : "r"(y0), "r"(y1), "r"(y2), "r"(x0), "r"(x1), "r"(a0), "r"(a1), "r"(a2));
+    const u32 l2 = t2 & kP89Top;
+    const u32 h0 = __funnelshift_r(t2, t3, 25);
+    const u32 h1 = __funnelshift_r(t3, t4, 25);
+    const u32 h2 = t4 >> 25;
+    asm("add.cc.u32  %0, %3, %6;\n\t"
+        "addc.cc.u32 %1, %4, %7;\n\t"
+        "addc.u32    %2, %5, %8;"
+        : "=r"(y0), "=r"(y1), "=r"(y2)
+        : "r"(t0), "r"(t1), "r"(l2), "r"(h0), "r"(h1), "r"(h2));
+}
+
+// Branch-free finish for y < 2p: z = (y + 1) >> 89; (y + z) & p.
+__device__ __forceinline__ void h89_finish(u32& y0, u32& y1, u32& y2) {
+    u32 s2;
+    asm("{\n\t.reg .u32 t0, t1;\n\t"
+        "add.cc.u32  t0, %1, 1;\n\t"
+        "addc.cc.u32 t1, %2, 0;\n\t"
+        "addc.u32    %0, %3, 0;\n\t}"
+        : "=r"(s2)
+        : "r"(y0), "r"(y1), "r"(y2));
+    const u32 z = s2 >> 25;
+    asm("add.cc.u32  %0, %0, %3;\n\t"
+        "addc.cc.u32 %1, %1, 0;\n\t"
+        "addc.u32    %2, %2, 0;"
+        : "+r"(y0), "+r"(y1), "+r"(y2)
+        : "r"(z));
+    y2 &= kP89Top;
+}
+
+// ---------------------------------------------------------------------------
+// SplitMix64 (prng.hpp:10-38) in counter form: the i-th next() of
+// SplitMix64(seed) is mix(seed + (i+1) * golden).
+constexpr u64 kGolden = 0x9E3779B97F4A7C15ull;
+__host__ __device__ __forceinline__ u64 mix64(u64 z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ u64 splitmix_at(u64 seed, u64 i) {
+    return mix64(seed + (i + 1) * kGolden);
+}
+
+}  // namespace mb200

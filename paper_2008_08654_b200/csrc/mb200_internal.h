@@ -1,0 +1,85 @@
+// mb200_internal.h -- launchers shared between the kernel translation units
+// and the C-ABI layer (capi.cu).  Not part of the public boundary.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mb200 {
+
+constexpr int kMaxK = 16;        // coefficients per family
+constexpr int kMaxFamilies = 16; // hash families per sketch
+constexpr int kMaxCoeffs = 128;  // families x k
+
+enum KeyWidth { KEY32 = 32, KEY64 = 64 };
+enum WeightKind { W_NONE = 0, W_I32 = 32, W_I64 = 64 };
+enum SplitKind { SPLIT_POW2 = 0, SPLIT_UNIFORM_ARB = 1, SPLIT_MERSENNE_ARB = 2, SPLIT_TWO_FOR_ONE = 3 };
+
+struct HashParams {
+    uint32_t b, k;
+    uint64_t p;
+    uint64_t lo[kMaxK];
+    uint64_t hi[kMaxK];
+};
+
+struct SketchParams {
+    uint32_t rows;       // counter rows t
+    uint32_t families;   // hash families (rows, or ceil(rows/2) for two-for-one)
+    uint32_t k;          // coefficients per family
+    uint32_t b;          // Mersenne exponent
+    uint32_t lw;         // log2 width (Pow2 / two-for-one)
+    uint32_t splitter;   // SplitKind
+    uint64_t width;      // counters per row
+    uint64_t p;
+    uint64_t lo[kMaxCoeffs];
+    uint64_t hi[kMaxCoeffs];
+};
+
+// hashing (kernels_hash.cu)
+cudaError_t launch_hash61_key32(const uint32_t* keys, uint64_t n, const HashParams& hp, uint64_t* out,
+                                cudaStream_t s);
+cudaError_t launch_hash61_key64(const uint64_t* keys, uint64_t n, const HashParams& hp, uint64_t* out,
+                                cudaStream_t s);
+cudaError_t launch_hash_generic(const void* keys, int key_width, uint64_t n, const HashParams& hp,
+                                uint64_t* out, cudaStream_t s);
+cudaError_t launch_hash89(const uint64_t* keys, uint64_t n, const HashParams& hp, uint64_t* out_lo,
+                          uint64_t* out_hi, cudaStream_t s);
+// domain validation: counts keys >= 2^key_bits into *d_count (pre-zeroed)
+cudaError_t launch_count_out_of_domain(const void* keys, int key_width, uint64_t n, uint32_t key_bits,
+                                       unsigned long long* d_count, cudaStream_t s);
+
+// sketch (kernels_sketch.cu)
+cudaError_t launch_cs_update(const SketchParams& sp, const void* keys, int key_width, const void* w,
+                             int w_kind, uint64_t n, int64_t* table, cudaStream_t s);
+cudaError_t launch_cs_moments(const int64_t* table, uint32_t rows, uint64_t width, uint64_t* out,
+                              cudaStream_t s);
+cudaError_t launch_cs_merge(int64_t* dst, const int64_t* src, uint64_t count, cudaStream_t s);
+cudaError_t launch_cs_point_query(const SketchParams& sp, const int64_t* table, const void* keys,
+                                  int key_width, uint64_t n, int64_t* out, cudaStream_t s);
+
+// division (kernels_divmod.cu)
+cudaError_t launch_pm_divmod(const uint64_t* v, uint64_t n, uint32_t b, uint64_t c, uint32_t iters,
+                             uint64_t* q, uint64_t* r, unsigned long long* d_flags, cudaStream_t s);
+cudaError_t launch_count_above(const uint64_t* v, uint64_t n, uint64_t max_lo, uint64_t max_hi,
+                               unsigned long long* d_count, cudaStream_t s);
+
+// workload generators (kernels_gen.cu)
+cudaError_t launch_gen_u32(uint64_t seed, uint64_t start, uint64_t n, uint32_t* out, cudaStream_t s);
+cudaError_t launch_gen_u64(uint64_t seed, uint64_t start, uint64_t n, uint64_t* out, cudaStream_t s);
+cudaError_t launch_gen_below_p61(uint64_t seed, uint64_t start, uint64_t n, uint64_t* out,
+                                 unsigned long long* d_bad, cudaStream_t s);
+cudaError_t launch_gen_pm_inputs(uint64_t seed, uint64_t c, uint64_t start, uint64_t n, uint64_t* out,
+                                 unsigned long long* d_bad, cudaStream_t s);
+cudaError_t launch_gen_zipf(uint64_t master, const uint64_t* cdf, uint32_t T, double c1,
+                            double universe, uint64_t start, uint64_t n, uint32_t* keys,
+                            int32_t* weights, cudaStream_t s);
+
+// probes (kernels_probe.cu)
+cudaError_t launch_probe_imad(int blocks, int threads, int iters, uint64_t* sink, cudaStream_t s);
+cudaError_t launch_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* buf,
+                                 uint64_t span, cudaStream_t s);
+
+int sm_count();
+int device_id();
+
+}  // namespace mb200

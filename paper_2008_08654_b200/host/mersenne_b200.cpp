@@ -1,0 +1,399 @@
+// mersenne_b200.cpp -- the reference's C++ API (field / polyhash / sketch)
+// re-hosted on the GPU path.  Every per-key computation goes through the
+// C-ABI kernels; this file only validates, owns device memory and streams,
+// pipelines host<->device copies and applies the host-side median.
+#include "../../include/mersenne_b200/mersenne_b200.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "../csrc/mb200_capi_util.h"
+
+namespace mersenne::b200 {
+
+void throw_status(int status) {
+    if (status == MB200_OK) return;
+    const std::string msg = mb200_last_error();
+    switch (status) {
+        case MB200_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case MB200_DOMAIN_ERROR: throw std::domain_error(msg);
+        case MB200_LOGIC_ERROR: throw std::logic_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+unsigned log2_pow2(u128 v) {
+    const u64 hi = u64(v >> 64);
+    if (hi) return 64 + unsigned(__builtin_ctzll(hi));
+    return unsigned(__builtin_ctzll(u64(v)));
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    explicit DevBuf(size_t n) { cuda_check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc"); }
+    ~DevBuf() { cudaFree(p); }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ field --
+MersenneModulus::MersenneModulus(unsigned b, bool require_prime) : b_(b) {
+    throw_status(mb200_mersenne_modulus_check(b, 0));
+    prime_ = mb200_mersenne_modulus_check(b, 1) == MB200_OK;
+    if (require_prime && !prime_) throw std::invalid_argument("2^b - 1 is not prime for this exponent");
+}
+
+PseudoMersenneModulus::PseudoMersenneModulus(unsigned b, u64 c, unsigned m_iters) : b_(b), c_(c) {
+    throw_status(mb200_pm_modulus(b, c, m_iters, &m_, max_input_.data()));
+}
+
+void PseudoMersenneModulus::divmod_device(const u64* d_v, u64 n, u64* d_q, u64* d_r, void* stream) const {
+    DevBuf<u64> ovf(1);
+    cuda_check(cudaMemsetAsync(ovf.p, 0, sizeof(u64), (cudaStream_t)stream), "memset");
+    throw_status(mb200_pm_divmod(d_v, n, b_, c_, m_, d_q, d_r, ovf.p, stream));
+    u64 o = 0;
+    cuda_check(cudaMemcpyAsync(&o, ovf.p, sizeof(u64), cudaMemcpyDeviceToHost, (cudaStream_t)stream), "copy");
+    cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "sync");
+    if (o) throw std::domain_error("quotient exceeds 64 bits");
+}
+
+void PseudoMersenneModulus::divmod(const u64* h_v, u64 n, u64* h_q, u64* h_r) const {
+    if (n == 0) return;
+    DevBuf<u64> v(2 * n), q(n), r(n);
+    cuda_check(cudaMemcpy(v.p, h_v, 2 * n * sizeof(u64), cudaMemcpyHostToDevice), "H2D");
+    divmod_device(v.p, n, q.p, r.p, nullptr);
+    cuda_check(cudaMemcpy(h_q, q.p, n * sizeof(u64), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(h_r, r.p, n * sizeof(u64), cudaMemcpyDeviceToHost), "D2H");
+}
+
+// --------------------------------------------------------------- polyhash --
+PolyHashFamily::PolyHashFamily(const MersenneModulus& modulus, unsigned k, u128 key_domain, u64 seed,
+                               HashFinish finish)
+    : modulus_(modulus), key_domain_(key_domain), finish_(finish) {
+    if (k == 0) throw std::invalid_argument("independence degree must be at least 1");
+    std::vector<u64> lo(k), hi(k);
+    throw_status(mb200_draw_coeffs(modulus.b(), k, seed, lo.data(), hi.data()));
+    coeffs_.resize(k);
+    for (unsigned i = 0; i < k; ++i) coeffs_[i] = (u128(hi[i]) << 64) | lo[i];
+    validate();
+}
+
+PolyHashFamily::PolyHashFamily(const MersenneModulus& modulus, std::vector<u128> coefficients, u128 key_domain,
+                               HashFinish finish)
+    : modulus_(modulus), coeffs_(std::move(coefficients)), key_domain_(key_domain), finish_(finish) {
+    if (coeffs_.empty()) throw std::invalid_argument("independence degree must be at least 1");
+    for (u128 a : coeffs_)
+        if (a >= modulus_.p()) throw std::invalid_argument("coefficient not reduced");  // polyhash.cpp:43
+    validate();
+}
+
+void PolyHashFamily::validate() const {  // polyhash.cpp:48-57
+    if (key_domain_ == 0 || (key_domain_ & (key_domain_ - 1)) != 0)
+        throw std::invalid_argument("key domain must be a power of two");
+    if (modulus_.p() < 2 * key_domain_ - 1) throw std::invalid_argument("modulus too small for key domain");
+}
+
+unsigned PolyHashFamily::key_bits() const { return log2_pow2(key_domain_); }
+
+void PolyHashFamily::hash_device(const void* d_keys, int key_width, u64 n, u64* d_out_lo, u64* d_out_hi,
+                                 void* stream) const {
+    const unsigned b = modulus_.b();
+    const unsigned k = independence();
+    std::vector<u64> lo(k), hi(k);
+    for (unsigned i = 0; i < k; ++i) {
+        lo[i] = u64(coeffs_[i]);
+        hi[i] = u64(coeffs_[i] >> 64);
+    }
+    const unsigned kb = std::min(key_bits(), 64u);
+    if (b <= 61) {
+        throw_status(mb200_hash61(d_keys, key_width, n, b, lo.data(), k, kb, d_out_lo, stream));
+    } else if (b == 89) {
+        if (key_width != 64) throw std::invalid_argument("the 89-bit path takes u64 keys");
+        if (!d_out_hi) throw std::invalid_argument("b > 64 needs a high-word output");
+        throw_status(mb200_hash89((const u64*)d_keys, n, lo.data(), hi.data(), k, kb, d_out_lo, d_out_hi, stream));
+    } else {
+        throw std::invalid_argument("GPU path supports b <= 61 and b == 89");
+    }
+}
+
+std::vector<u128> PolyHashFamily::hash(const std::vector<u64>& keys) const {
+    const u64 n = keys.size();
+    std::vector<u128> out(n);
+    if (n == 0) return out;
+    for (u64 x : keys)
+        if (key_bits() < 64 && x >= (u64(1) << key_bits())) throw std::domain_error("key outside domain");
+    DevBuf<u64> dk(n), dlo(n), dhi(n);
+    cuda_check(cudaMemcpy(dk.p, keys.data(), n * sizeof(u64), cudaMemcpyHostToDevice), "H2D");
+    hash_device(dk.p, 64, n, dlo.p, dhi.p, nullptr);
+    std::vector<u64> lo(n), hi(n, 0);
+    cuda_check(cudaMemcpy(lo.data(), dlo.p, n * sizeof(u64), cudaMemcpyDeviceToHost), "D2H");
+    if (modulus_.b() > 64) cuda_check(cudaMemcpy(hi.data(), dhi.p, n * sizeof(u64), cudaMemcpyDeviceToHost), "D2H");
+    for (u64 i = 0; i < n; ++i) out[i] = (u128(hi[i]) << 64) | lo[i];
+    return out;
+}
+
+u128 PolyHashFamily::operator()(u128 x) const {
+    if (x >= key_domain_) throw std::domain_error("key outside domain");  // polyhash.cpp:60
+    return hash(std::vector<u64>{u64(x)})[0];
+}
+
+SignIndexPair split_pow2(u128 h, unsigned b, unsigned l) {
+    const u128 i = h & ((u128(1) << l) - 1);
+    const int a = int(h >> (b - 1));
+    return {i, 1 - 2 * a};
+}
+
+// ----------------------------------------------------------------- sketch --
+struct CountSketch::Staging {
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ready[2] = {nullptr, nullptr};
+    cudaEvent_t freed[2] = {nullptr, nullptr};
+    void* d_keys[2] = {nullptr, nullptr};
+    void* d_w[2] = {nullptr, nullptr};
+    u64 chunk = 0;
+    ~Staging() {
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(d_keys[i]);
+            cudaFree(d_w[i]);
+            if (ready[i]) cudaEventDestroy(ready[i]);
+            if (freed[i]) cudaEventDestroy(freed[i]);
+        }
+        if (copy) cudaStreamDestroy(copy);
+    }
+};
+
+CountSketch::CountSketch(unsigned rows, u64 width, const MersenneModulus& modulus, u128 key_domain,
+                         Splitter splitter, u64 seed, unsigned independence)
+    : rows_(rows), width_(width), splitter_(splitter) {
+    if (rows == 0) throw std::invalid_argument("need at least one row");  // sketch.cpp:71
+    const unsigned fams = splitter == Splitter::TwoForOne ? (rows + 1) / 2 : rows;
+    seeds_.resize(fams);
+    throw_status(mb200_row_seeds(seed, fams, seeds_.data()));  // sketch.cpp:72-77
+    for (unsigned f = 0; f < fams; ++f) families_.emplace_back(modulus, independence, key_domain, seeds_[f]);
+    validate();
+    init_device();
+}
+
+CountSketch::CountSketch(u64 width, Splitter splitter, std::vector<PolyHashFamily> families, unsigned rows)
+    : width_(width), splitter_(splitter), families_(std::move(families)) {
+    if (families_.empty()) throw std::invalid_argument("need at least one row");
+    for (const PolyHashFamily& f : families_) {
+        if (f.modulus().b() != families_.front().modulus().b() || f.key_domain() != families_.front().key_domain())
+            throw std::invalid_argument("rows must share modulus and key domain");
+        if (f.independence() != families_.front().independence())
+            throw std::invalid_argument("GPU path needs equal independence across rows");
+    }
+    rows_ = rows ? rows : (splitter == Splitter::TwoForOne ? 2 * unsigned(families_.size()) : unsigned(families_.size()));
+    validate();
+    init_device();
+}
+
+CountSketch::CountSketch(CountSketch&& o) noexcept
+    : rows_(o.rows_), width_(o.width_), splitter_(o.splitter_), families_(std::move(o.families_)),
+      seeds_(std::move(o.seeds_)), clo_(std::move(o.clo_)), chi_(std::move(o.chi_)), d_counters_(o.d_counters_),
+      stream_(o.stream_), staging_(std::move(o.staging_)) {
+    o.d_counters_ = nullptr;
+    o.stream_ = nullptr;
+}
+
+CountSketch::~CountSketch() {
+    staging_.reset();
+    if (d_counters_) cudaFree(d_counters_);
+    if (stream_) cudaStreamDestroy((cudaStream_t)stream_);
+}
+
+void CountSketch::validate() const {
+    mb200_sketch_desc d = desc();
+    // reuse the C-ABI validation (sketch.cpp:97-119 + GPU coverage) with a dry run
+    int64_t dummy = 0;
+    throw_status(mb200_cs_update(&d, &dummy, 64, nullptr, MB200_W_NONE, 0, &dummy, nullptr));
+}
+
+mb200_sketch_desc CountSketch::desc() const {
+    clo_.clear();
+    chi_.clear();
+    for (const PolyHashFamily& f : families_)
+        for (u128 a : f.coefficients()) {
+            clo_.push_back(u64(a));
+            chi_.push_back(u64(a >> 64));
+        }
+    mb200_sketch_desc d;
+    d.rows = rows_;
+    d.width = width_;
+    d.b = families_.front().modulus().b();
+    d.k = families_.front().independence();
+    d.key_bits = std::min(families_.front().key_bits(), 64u);
+    d.splitter = int(splitter_);
+    d.coeffs_lo = clo_.data();
+    d.coeffs_hi = chi_.data();
+    return d;
+}
+
+void CountSketch::init_device() {
+    cudaStream_t s;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    stream_ = s;
+    const size_t bytes = size_t(rows_) * width_ * sizeof(i64);
+    cuda_check(cudaMalloc(&d_counters_, bytes), "cudaMalloc counters");
+    cuda_check(cudaMemsetAsync(d_counters_, 0, bytes, s), "memset");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+}
+
+void CountSketch::synchronize() const { cuda_check(cudaStreamSynchronize((cudaStream_t)stream_), "sync"); }
+
+void CountSketch::process_device(const void* d_keys, int key_width, const void* d_weights, int weight_kind, u64 n,
+                                 void* stream) {
+    mb200_sketch_desc d = desc();
+    throw_status(mb200_cs_update(&d, d_keys, key_width, d_weights, weight_kind, n, d_counters_,
+                                 stream ? stream : stream_));
+}
+
+void CountSketch::process_batch(const void* h_keys, int key_width, const void* h_weights, int weight_kind, u64 n) {
+    if (n == 0) return;
+    if (key_width != 32 && key_width != 64) throw std::invalid_argument("key width must be 32 or 64");
+    const unsigned kb = families_.front().key_bits();
+    if (kb < unsigned(key_width)) {  // all-or-nothing domain check before any update (polyhash.cpp:60)
+        const u64 lim = u64(1) << kb;
+        for (u64 i = 0; i < n; ++i) {
+            const u64 x = key_width == 32 ? ((const uint32_t*)h_keys)[i] : ((const u64*)h_keys)[i];
+            if (x >= lim) throw std::domain_error("key outside domain");
+        }
+    }
+    const size_t kbytes = key_width / 8;
+    const size_t wbytes = weight_kind == MB200_W_NONE ? 0 : size_t(weight_kind) / 8;
+    if (!staging_) staging_ = std::make_unique<Staging>();
+    Staging& st = *staging_;
+    const u64 want = std::min<u64>(n, u64(1) << 24);
+    if (st.chunk < want) {
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(st.d_keys[i]);
+            cudaFree(st.d_w[i]);
+            st.d_keys[i] = st.d_w[i] = nullptr;
+            cuda_check(cudaMalloc(&st.d_keys[i], want * 8), "cudaMalloc staging");
+            cuda_check(cudaMalloc(&st.d_w[i], want * 8), "cudaMalloc staging");
+        }
+        st.chunk = want;
+    }
+    if (!st.copy) {
+        cuda_check(cudaStreamCreateWithFlags(&st.copy, cudaStreamNonBlocking), "stream");
+        for (int i = 0; i < 2; ++i) {
+            cuda_check(cudaEventCreateWithFlags(&st.ready[i], cudaEventDisableTiming), "event");
+            cuda_check(cudaEventCreateWithFlags(&st.freed[i], cudaEventDisableTiming), "event");
+        }
+    }
+    const mb200_sketch_desc d = desc();
+    cudaStream_t cs = (cudaStream_t)stream_;
+    const u64 chunks = (n + st.chunk - 1) / st.chunk;
+    for (u64 c = 0; c < chunks; ++c) {
+        const int slot = int(c & 1);
+        const u64 off = c * st.chunk;
+        const u64 m = std::min<u64>(st.chunk, n - off);
+        if (c >= 2) cuda_check(cudaStreamWaitEvent(st.copy, st.freed[slot], 0), "wait");
+        cuda_check(cudaMemcpyAsync(st.d_keys[slot], (const char*)h_keys + off * kbytes, m * kbytes,
+                                   cudaMemcpyHostToDevice, st.copy),
+                   "H2D keys");
+        if (wbytes)
+            cuda_check(cudaMemcpyAsync(st.d_w[slot], (const char*)h_weights + off * wbytes, m * wbytes,
+                                       cudaMemcpyHostToDevice, st.copy),
+                       "H2D weights");
+        cuda_check(cudaEventRecord(st.ready[slot], st.copy), "record");
+        cuda_check(cudaStreamWaitEvent(cs, st.ready[slot], 0), "wait");
+        // keys were validated on the host above: skip the per-chunk device check
+        throw_status(mb200::cs_update_nocheck(&d, st.d_keys[slot], key_width, wbytes ? st.d_w[slot] : nullptr, weight_kind,
+                                     m, d_counters_, cs));
+        cuda_check(cudaEventRecord(st.freed[slot], cs), "record");
+    }
+    cuda_check(cudaStreamSynchronize(cs), "sync");
+}
+
+void CountSketch::process(u128 x, i64 delta) {
+    if (x >= key_domain()) throw std::domain_error("key outside domain");
+    const u64 k = u64(x);
+    process_batch(&k, 64, &delta, MB200_W_I64, 1);
+}
+
+std::vector<CountSketch::Moment> CountSketch::row_moments() const {
+    DevBuf<u64> out(4 * size_t(rows_));
+    cudaStream_t s = (cudaStream_t)stream_;
+    throw_status(mb200_cs_moments(d_counters_, rows_, width_, out.p, s));
+    std::vector<u64> h(4 * size_t(rows_));
+    cuda_check(cudaMemcpyAsync(h.data(), out.p, h.size() * sizeof(u64), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    std::vector<Moment> m(rows_);
+    for (unsigned r = 0; r < rows_; ++r) m[r] = {(u128(h[4 * r + 1]) << 64) | h[4 * r], h[4 * r + 2] != 0};
+    return m;
+}
+
+CountSketch::Moment CountSketch::row_second_moment(unsigned row) const {
+    if (row >= rows_) throw std::invalid_argument("row out of range");
+    return row_moments()[row];
+}
+
+CountSketch::Moment CountSketch::second_moment(bool median_rows) const {  // sketch.cpp:160-168
+    std::vector<Moment> all = row_moments();
+    if (!median_rows || rows_ == 1) return all[0];
+    std::sort(all.begin(), all.end(), [](const Moment& a, const Moment& b) { return a.value < b.value; });
+    return all[(all.size() - 1) / 2];
+}
+
+std::vector<i64> CountSketch::point_query_batch(const void* h_keys, int key_width, u64 n) const {
+    std::vector<i64> out(n);
+    if (n == 0) return out;
+    const size_t kbytes = key_width / 8;
+    DevBuf<unsigned char> dk(n * kbytes);
+    DevBuf<i64> dout(n);
+    cudaStream_t s = (cudaStream_t)stream_;
+    cuda_check(cudaMemcpyAsync(dk.p, h_keys, n * kbytes, cudaMemcpyHostToDevice, s), "H2D");
+    mb200_sketch_desc d = desc();
+    throw_status(mb200_cs_point_query(&d, d_counters_, dk.p, key_width, n, dout.p, s));
+    cuda_check(cudaMemcpyAsync(out.data(), dout.p, n * sizeof(i64), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    return out;
+}
+
+i64 CountSketch::point_query(u128 x) const {
+    if (x >= key_domain()) throw std::domain_error("key outside domain");
+    const u64 k = u64(x);
+    return point_query_batch(&k, 64, 1)[0];
+}
+
+CountSketch& CountSketch::merge(const CountSketch& other) {  // sketch.cpp:182-193
+    if (width_ != other.width_ || splitter_ != other.splitter_ || rows_ != other.rows_ ||
+        families_.size() != other.families_.size() || seeds_ != other.seeds_ ||
+        modulus().b() != other.modulus().b() || key_domain() != other.key_domain() ||
+        independence() != other.independence() || seeds_.empty()) {
+        throw std::invalid_argument("sketches differ in geometry or seeds");
+    }
+    other.synchronize();
+    throw_status(mb200_cs_merge(d_counters_, other.d_counters_, u64(rows_) * width_, stream_));
+    synchronize();
+    return *this;
+}
+
+std::vector<i64> CountSketch::counters() const {
+    std::vector<i64> h(size_t(rows_) * width_);
+    cudaStream_t s = (cudaStream_t)stream_;
+    cuda_check(cudaMemcpyAsync(h.data(), d_counters_, h.size() * sizeof(i64), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    return h;
+}
+
+void CountSketch::set_counters(const std::vector<i64>& c) {
+    if (c.size() != size_t(rows_) * width_) throw std::invalid_argument("counter count mismatch");
+    cudaStream_t s = (cudaStream_t)stream_;
+    cuda_check(cudaMemcpyAsync(d_counters_, c.data(), c.size() * sizeof(i64), cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+}
+
+}  // namespace mersenne::b200

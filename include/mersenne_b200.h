@@ -182,6 +182,10 @@ int mb200_gen_zipf_items(uint64_t master_seed, const uint64_t* d_cdf, uint32_t T
 int mb200_probe_imad(int blocks, int threads, int iters, uint64_t* d_sink, void* stream);
 int mb200_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* d_buf,
                         uint64_t span, void* stream);
+/* cluster-of-`cluster` CTAs each owning `words` u32 cells in shared memory:
+ * mode 0 random remote-or-local red.shared::cluster, 1 local only, 2 one hot cell */
+int mb200_probe_dsmem(int cluster, int mode, int blocks, int threads, int iters, uint32_t words,
+                      uint64_t* d_out, void* stream);
 
 #ifdef __cplusplus
 }

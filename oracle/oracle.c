@@ -569,7 +569,15 @@ u64 orc_cs_process(unsigned rows, u64 width, unsigned b, unsigned k, const u64* 
             i64 delta = w64 ? w64[i] : (w32 ? (i64)w32[i] : 1);
             for (unsigned f = 0; f < fams; ++f) {
                 u128 h = 0;
-                hash_one(b, clo + (size_t)f * k, chi + (size_t)f * k, k, 128, x, 0, &h);
+                if (b <= 61 && key_bits > b - 1) {
+                    /* beyond the reference domain (u > 2^(b-1)): the GPU path reduces keys
+                     * exactly; restated as Horner with Alg-3 full reduction per step */
+                    u64 xr = mod_full61(b, x), y = clo[(size_t)f * k + k - 1];
+                    for (unsigned j = k - 1; j-- > 0;) y = mod_full61(b, (u128)y * xr + clo[(size_t)f * k + j]);
+                    h = y;
+                } else {
+                    hash_one(b, clo + (size_t)f * k, chi + (size_t)f * k, k, 128, x, 0, &h);
+                }
                 unsigned subs = splitter == 3 ? 2 : 1;
                 for (unsigned s = 0; s < subs; ++s) {
                     unsigned row = splitter == 3 ? 2 * f + s : f;

@@ -281,6 +281,11 @@ def probe_atomics(mode: int, blocks: int, threads: int, iters: int, buf, span: i
     check(lib.mb200_probe_atomics(mode, blocks, threads, iters, _dptr(buf), span, _stream(stream)))
 
 
+def probe_dsmem(cluster: int, mode: int, blocks: int, threads: int, iters: int, words: int, out,
+                stream=None):
+    check(lib.mb200_probe_dsmem(cluster, mode, blocks, threads, iters, words, _dptr(out), _stream(stream)))
+
+
 # ------------------------------------------------------------------ host object
 class CountSketch:
     """mersenne::CountSketch (sketch.hpp:40-92) with counters in HBM; host-buffer API."""

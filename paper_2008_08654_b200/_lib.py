@@ -108,6 +108,7 @@ SIGNATURES = [
     ("mb200_gen_zipf_items", I, [u64, P, u32, D, D, u64, u64, P, P, P]),
     ("mb200_probe_imad", I, [I, I, I, P, P]),
     ("mb200_probe_atomics", I, [I, I, I, I, P, u64, P]),
+    ("mb200_probe_dsmem", I, [I, I, I, I, I, u32, P, P]),
 ]
 
 

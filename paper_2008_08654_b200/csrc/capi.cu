@@ -342,4 +342,10 @@ int mb200_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* 
     return e == cudaSuccess ? MB200_OK : cuda_fail(e, "probe");
 }
 
+int mb200_probe_dsmem(int cluster, int mode, int blocks, int threads, int iters, uint32_t words, uint64_t* d_out,
+                      void* stream) {
+    cudaError_t e = launch_probe_dsmem(cluster, mode, blocks, threads, iters, words, d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "probe");
+}
+
 }  // extern "C"

@@ -2,6 +2,8 @@
 // this path needs and MEASURED_PEAKS.json does not carry ("measured
 // peak IMAD.WIDE.U32 rate ... microbenchmark it on the same box"), plus the
 // atomic throughputs that decide the Count Sketch privatisation strategy.
+#include <cooperative_groups.h>
+
 #include "mb200_device.cuh"
 #include "mb200_internal.h"
 #include "mb200_mem.cuh"
@@ -60,6 +62,17 @@ __global__ void probe_atomics_kernel(int mode, int iters, u64* buf, u64 span) {
             case 1: atomicAdd(&t32[h & 4095], 1u); break;
             case 2: red_add_u64(buf + (h % span), 1); break;
             case 3: red_add_u64(buf, 1); break;
+            case 5: {  // global red.u32 on random cells
+                unsigned* b32 = reinterpret_cast<unsigned*>(buf);
+                asm volatile("red.global.add.u32 [%0], %1;" ::"l"(b32 + (h % span)), "r"(1u) : "memory");
+                break;
+            }
+            case 6: atomicCAS(&t32[h & 4095], 0u, h); break;  // shared CAS, random cells
+            case 7: {  // shared u64 atomic on 2 u32 halves (carry via returned old value)
+                const unsigned old = atomicAdd(&t32[h & 4095], 1u);
+                if (old == 0xffffffffu) atomicAdd(&t32[(h + 1) & 4095], 1u);
+                break;
+            }
             default:
                 if ((threadIdx.x & 31) == 0) red_add_u64(buf, 32);
                 break;
@@ -69,7 +82,52 @@ __global__ void probe_atomics_kernel(int mode, int iters, u64* buf, u64 span) {
     if (mode <= 1 && threadIdx.x == 0) buf[blockIdx.x % span] += t64[0] + t32[0];
 }
 
+// Distributed-shared-memory reductions inside a cluster of CS CTAs, each CTA
+// owning `words` u32 counters: mode 0 random (rank, cell) -- (CS-1)/CS remote;
+// mode 1 random cell of the own CTA; mode 2 one hot cell in rank 0.
+template <int CS>
+__global__ void __cluster_dims__(CS, 1, 1) probe_dsmem_kernel(int mode, int iters, u32 words, u64* out) {
+    extern __shared__ u32 tab[];
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    for (u32 i = threadIdx.x; i < words; i += blockDim.x) tab[i] = 0;
+    cl.sync();
+    u32 h = scramble(blockIdx.x * blockDim.x + threadIdx.x);
+    const u32 me = cl.block_rank();
+    for (int i = 0; i < iters; ++i) {
+        h = scramble(h + i);
+        u32 rank = mode == 0 ? (h >> 24) % CS : (mode == 1 ? me : 0);
+        u32 off = mode == 2 ? 0 : (h & 0xFFFFFF) % words;
+        u32* remote = cl.map_shared_rank(tab, rank);
+        atomicAdd(remote + off, 1u);
+    }
+    cl.sync();
+    if (threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)tab[0]);
+}
+
 }  // namespace
+
+cudaError_t launch_probe_dsmem(int cluster, int mode, int blocks, int threads, int iters, uint32_t words,
+                               uint64_t* out, cudaStream_t s) {
+    const size_t smem = (size_t)words * 4;
+    cudaError_t e = cudaSuccess;
+    switch (cluster) {
+#define MB200_DS(CS)                                                                                    \
+    case CS:                                                                                            \
+        e = cudaFuncSetAttribute(probe_dsmem_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)smem);                                                           \
+        if (e != cudaSuccess) return e;                                                                \
+        probe_dsmem_kernel<CS><<<blocks, threads, smem, s>>>(mode, iters, words, out);                 \
+        break;
+        MB200_DS(1)
+        MB200_DS(2)
+        MB200_DS(4)
+        MB200_DS(8)
+#undef MB200_DS
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_probe_imad(int blocks, int threads, int iters, uint64_t* sink, cudaStream_t s) {
     probe_imad_kernel<<<blocks, threads, 0, s>>>(iters, sink);

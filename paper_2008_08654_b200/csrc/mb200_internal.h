@@ -51,6 +51,10 @@ cudaError_t launch_count_out_of_domain(const void* keys, int key_width, uint64_t
 // sketch (kernels_sketch.cu)
 cudaError_t launch_cs_update(const SketchParams& sp, const void* keys, int key_width, const void* w,
                              int w_kind, uint64_t n, int64_t* table, cudaStream_t s);
+// heavy-hitter pipeline for tables larger than shared memory (kernels_hot.cu);
+// requires |delta| < 2^31 (w_kind W_NONE or W_I32)
+cudaError_t launch_cs_hot(const SketchParams& sp, const void* keys, int key_width, const void* w, int w_kind,
+                          uint64_t n, int64_t* table, cudaStream_t s);
 cudaError_t launch_cs_moments(const int64_t* table, uint32_t rows, uint64_t width, uint64_t* out,
                               cudaStream_t s);
 cudaError_t launch_cs_merge(int64_t* dst, const int64_t* src, uint64_t count, cudaStream_t s);
@@ -78,6 +82,9 @@ cudaError_t launch_gen_zipf(uint64_t master, const uint64_t* cdf, uint32_t T, do
 cudaError_t launch_probe_imad(int blocks, int threads, int iters, uint64_t* sink, cudaStream_t s);
 cudaError_t launch_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* buf,
                                  uint64_t span, cudaStream_t s);
+
+cudaError_t launch_probe_dsmem(int cluster, int mode, int blocks, int threads, int iters, uint32_t words,
+                               uint64_t* out, cudaStream_t s);
 
 int sm_count();
 int device_id();

@@ -275,6 +275,41 @@ def test_sketch_random_vs_oracle(cuda, mb, orc, case):
     assert mb.lower_median(m) == orc.second_moment(exp, rows, width, True)
 
 
+HOT_CASES = [
+    # rows, width, b, key_bits, splitter, key kind, weights: batches >= 2^22 take the
+    # heavy-hitter path (shared-memory accumulation of sampled hot keys)
+    (5, 65536, 61, 32, 0, "zipf", np.int32),
+    (5, 65536, 61, 32, 0, "zipf", None),
+    (5, 65536, 61, 32, 0, "uniform32", np.int32),
+    (2, 65536, 89, 64, 3, "zipf64", None),
+    (3, 4096, 61, 64, 0, "zipf64", np.int32),
+    (16, 8192, 61, 32, 2, "zipf", np.int32),
+]
+
+
+@pytest.mark.parametrize("case", HOT_CASES, ids=[f"r{c[0]}b{c[2]}{c[5]}" for c in HOT_CASES])
+def test_hot_path_large_batches(cuda, mb, orc, case):
+    import torch
+
+    rows, width, b, kb, sp, kind, wdt = case
+    spec, fams = make_spec(mb, orc, rows, width, b, kb, sp, 0xB16 + rows)
+    n = (1 << 22) + 12345
+    zk, zw = orc.gen_zipf_items(7, 0, n)
+    if kind == "uniform32":
+        zk = orc.gen_u32_keys(7, 0, n)
+    keys = zk if kind != "zipf64" else (zk.astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15))
+    if kind == "zipf64" and kb < 64:
+        keys = keys >> np.uint64(64 - kb)
+    keys[:3] = [0, np.iinfo(keys.dtype).max if kb >= 32 else 1, 0]  # the empty-slot sentinel key
+    w = None if wdt is None else zw.astype(wdt)
+    if w is not None:
+        w[:4] = [np.iinfo(np.int32).min, np.iinfo(np.int32).max, -1, 1]
+    cnt = torch.zeros(rows * width, dtype=torch.int64, device="cuda")
+    mb.cs_update(spec, dev(keys), cnt, None if w is None else dev(w))
+    exp = orc.cs_process(rows, width, b, fams, kb, sp, keys, w)
+    assert (cnt.cpu().numpy() == exp).all()
+
+
 def test_sketch_empty_and_single(cuda, mb, orc):
     import torch
 

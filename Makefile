@@ -38,9 +38,10 @@ $(LIB): $(CU_OBJS) $(CPP_OBJS)
 oracle:
 	$(MAKE) -C oracle all
 
-cpptest: $(LIB) tests/cpp/test_host_api.cpp
+cpptest: $(LIB) tests/cpp/test_host_api.cpp oracle
 	g++ $(CXXFLAGS) -Iinclude -o tests/cpp/test_host_api tests/cpp/test_host_api.cpp \
-	    -L$(PKG) -lmersenne_b200 -L$(CUDA)/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+	    -L$(PKG) -lmersenne_b200 -Loracle -loracle -L$(CUDA)/lib64 -lcudart \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle'
 
 clean:
 	rm -rf $(BUILD) $(LIB) tests/cpp/test_host_api

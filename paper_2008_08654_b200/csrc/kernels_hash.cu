@@ -53,25 +53,29 @@ __global__ void __launch_bounds__(kThreads) hash61_key64_kernel(const u64* __res
     ulonglong2* o2 = reinterpret_cast<ulonglong2*>(out);
     const uint64_t npairs = n >> 1;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // software pipeline: the next round's kUnroll vectors are in flight while
+    // the current round is hashed
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; i + (kUnroll - 1) * stride < npairs; i += kUnroll * stride) {
-        ulonglong2 v[kUnroll];
+    ulonglong2 v[kUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(k2 + i + u * stride);
+    for (int u = 0; u < kUnroll; ++u)
+        if (i + u * stride < npairs) v[u] = ld_stream(k2 + i + u * stride);
+    for (; i < npairs; i += kUnroll * stride) {
+        ulonglong2 nx[kUnroll];
+        const uint64_t j = i + kUnroll * stride;
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (j + u * stride < npairs) nx[u] = ld_stream(k2 + j + u * stride);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            ulonglong2 h;
-            h.x = eval61_key64<K>(a, v[u].x);
-            h.y = eval61_key64<K>(a, v[u].y);
-            st_stream(o2 + i + u * stride, h);
+            if (i + u * stride < npairs) {
+                ulonglong2 h;
+                h.x = eval61_key64<K>(a, v[u].x);
+                h.y = eval61_key64<K>(a, v[u].y);
+                st_stream(o2 + i + u * stride, h);
+            }
+            v[u] = nx[u];
         }
-    }
-    for (; i < npairs; i += stride) {
-        const ulonglong2 v = ld_stream(k2 + i);
-        ulonglong2 h;
-        h.x = eval61_key64<K>(a, v.x);
-        h.y = eval61_key64<K>(a, v.y);
-        st_stream(o2 + i, h);
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[n - 1] = eval61_key64<K>(a, keys[n - 1]);
 }

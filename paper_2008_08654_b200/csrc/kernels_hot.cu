@@ -40,7 +40,7 @@ constexpr int kHotWarps = kHotThreads / 32;
 constexpr uint32_t kHotSample = 1u << 18;
 constexpr uint32_t kCountLog2 = 20;
 constexpr uint32_t kCountSlots = 1u << kCountLog2;
-constexpr int kQueue = 64;
+constexpr int kQueue = 64;  // < 32 queued + one slot of 32 misses
 constexpr int kTileSlots = 4;  // items per lane per tile
 constexpr uint64_t kTile = 32ull * kTileSlots;
 
@@ -51,6 +51,7 @@ struct HotGeom<u32> {
     static constexpr uint32_t kLog2 = 14;  // 16384 slots x 12 B = 192 KiB
     static constexpr uint32_t kCap = 8192;
     static constexpr u32 kEmpty = 0xffffffffu;
+    static constexpr uint32_t kWays = 4;  // keys per 16-byte bucket
     using Cas = unsigned;
 };
 template <>
@@ -58,6 +59,7 @@ struct HotGeom<u64> {
     static constexpr uint32_t kLog2 = 13;  // 8192 slots x 16 B = 128 KiB
     static constexpr uint32_t kCap = 4096;
     static constexpr u64 kEmpty = ~0ull;
+    static constexpr uint32_t kWays = 2;
     using Cas = unsigned long long;
 };
 
@@ -131,6 +133,46 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
     }
 }
 
+// bucket choices of the shared hot table (4096 buckets of 16 bytes)
+constexpr uint32_t kBucketLog2 = 12;
+__device__ __forceinline__ u32 fmix32(u32 h) {
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    return h ^ (h >> 16);
+}
+__device__ __forceinline__ u32 bucket1(u32 key) { return (key * 0x9E3779B1u) >> (32 - kBucketLog2); }
+__device__ __forceinline__ u32 bucket2(u32 key) { return fmix32(key) >> (32 - kBucketLog2); }
+__device__ __forceinline__ u32 bucket1(u64 key) { return (u32)(mix64(key) >> (64 - kBucketLog2)); }
+__device__ __forceinline__ u32 bucket2(u64 key) { return (u32)(mix64(key) >> 20) & ((1u << kBucketLog2) - 1); }
+
+// slot of `key` in the bucketed table, or -1
+__device__ __forceinline__ int find_slot(const u32* hk, u32 key) {
+    const u32 b1 = bucket1(key);
+    const uint4 v = *reinterpret_cast<const uint4*>(hk + 4 * b1);
+    int s = v.x == key ? 0 : v.y == key ? 1 : v.z == key ? 2 : v.w == key ? 3 : -1;
+    if (s >= 0) return (int)(4 * b1) + s;
+    const bool full = (v.x != 0xffffffffu) & (v.y != 0xffffffffu) & (v.z != 0xffffffffu) & (v.w != 0xffffffffu);
+    if (!full) return -1;
+    const u32 b2 = bucket2(key);
+    const uint4 q = *reinterpret_cast<const uint4*>(hk + 4 * b2);
+    s = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
+    return s >= 0 ? (int)(4 * b2) + s : -1;
+}
+__device__ __forceinline__ int find_slot(const u64* hk, u64 key) {
+    const u32 b1 = bucket1(key);
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(hk + 2 * b1);
+    if (v.x == key) return (int)(2 * b1);
+    if (v.y == key) return (int)(2 * b1) + 1;
+    if (v.x == ~0ull || v.y == ~0ull) return -1;
+    const u32 b2 = bucket2(key);
+    const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(hk + 2 * b2);
+    if (q.x == key) return (int)(2 * b2);
+    if (q.y == key) return (int)(2 * b2) + 1;
+    return -1;
+}
+
 // exact 64-bit accumulation in two u32 words (|d| <= 2^31): the low word carries
 // a 2^31 bias so a sum hovering around zero never wraps; the high word counts wraps
 __device__ __forceinline__ void hot_accumulate(u32* lo, u32* hi, u32 h, i32 d) {
@@ -174,7 +216,13 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
     const u32 nhot = min(*hot_count, G::kCap);
-    // hottest first: they take their home slots, so most hits need one probe
+    // Two-choice bucketed table: a key lives in one of the 16-byte buckets b1/b2
+    // (4 u32 or 2 u64 keys each), so a lookup is at most two vector loads and
+    // never a divergent probe loop.  Hottest keys first, into b1 while it has
+    // room; a key reaches b2 only once b1 is full, so a lookup whose b1 still
+    // has an empty slot is a miss without reading b2.  Keys that find both
+    // buckets full stay cold (exactness does not depend on the hot set).
+    // hi[] doubles as the per-bucket fill counter during the build.
     const u32 bands[3] = {64u, 8u, 0u};
     u32 upper = 0xffffffffu;
     for (int r = 0; r < 3; ++r) {
@@ -182,13 +230,19 @@ __global__ void __launch_bounds__(kHotThreads, 1)
             const u32 c = hot_cnt[j];
             if (c < bands[r] || c >= upper) continue;
             const KeyT key = hot[j];
-            u32 h = home<G::kLog2>(key);
-            while ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + h), (C)G::kEmpty, (C)key) != G::kEmpty)
-                h = (h + 1) & (S - 1);
+            const u32 b1 = bucket1(key), b2 = bucket2(key);
+            u32 pos = atomicAdd(hi + b1, 1u);
+            if (pos < G::kWays) {
+                hk[b1 * G::kWays + pos] = key;
+            } else if ((pos = atomicAdd(hi + b2, 1u)) < G::kWays) {
+                hk[b2 * G::kWays + pos] = key;
+            }
         }
         upper = bands[r];
         __syncthreads();
     }
+    for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) hi[s] = 0;
+    __syncthreads();
 
     const uint64_t lo_item = n * blockIdx.x / gridDim.x, hi_item = n * (blockIdx.x + 1) / gridDim.x;
     const uint64_t ntiles = (hi_item - lo_item + kTile - 1) / kTile;
@@ -213,14 +267,9 @@ __global__ void __launch_bounds__(kHotThreads, 1)
             const bool valid = base + u * 32 + lane < hi_item;
             bool hit = false;
             if (valid && kx[u] != G::kEmpty) {
-                u32 h = home<G::kLog2>(kx[u]);
-                KeyT cur = hk[h];
-                while (cur != kx[u] && cur != G::kEmpty) {
-                    h = (h + 1) & (S - 1);
-                    cur = hk[h];
-                }
-                hit = cur == kx[u];
-                if (hit) hot_accumulate(lo, hi, h, dx[u]);
+                const int h = find_slot(hk, kx[u]);
+                hit = h >= 0;
+                if (hit) hot_accumulate(lo, hi, (u32)h, dx[u]);
             }
             const bool miss = valid && !hit;
             const unsigned m = __ballot_sync(kFull, miss);
@@ -231,7 +280,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
             }
             qn += __popc(m);
             __syncwarp();
-            if (qn >= 32) {
+            if (qn >= 32) {  // a full warp of misses
                 process_item<MODE, K, GLOBAL>(sp, (u64)wqk[lane], (i64)wqd[lane], nullptr, table);
                 __syncwarp();
                 if (lane < qn - 32) {

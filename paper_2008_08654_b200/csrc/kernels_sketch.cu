@@ -65,6 +65,14 @@ __global__ void __launch_bounds__(kThreads) cs_update_kernel(const SketchParams 
             kx[u] = i < n ? ld_nc(keys + i) : KeyT(0);
             dx[u] = i < n ? load_weight<WK>(w, i) : 0;
         }
+        if (STRAT != GLOBAL || !aggregate) {
+            // independent items: the slots' Horner chains interleave
+            unsigned valid = 0;
+#pragma unroll
+            for (int u = 0; u < kSlots; ++u) valid |= (base + u * 32 + lane < n ? 1u : 0u) << u;
+            process_items<MODE, K, STRAT, kSlots>(sp, kx, dx, valid, smem, table);
+            continue;
+        }
 #pragma unroll 1
         for (int u = 0; u < kSlots; ++u) {
             const uint64_t i = base + u * 32 + lane;

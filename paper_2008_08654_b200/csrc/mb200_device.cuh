@@ -58,15 +58,43 @@ __device__ __forceinline__ u64 h61_finish(u64 y) {
 // Four limb products.
 __device__ __forceinline__ u64 h61_key64(u64 x) { return (x & kP61) + (x >> 61); }
 
+// y x = P00 + (y0 x1 + y1 x0) 2^32 + P11 2^64 where the middle sum M < 2^63 fits
+// one 64-bit mad.wide (y1 < 2^30, x1 <= 2^29): four IMAD.WIDE.U32, no operand
+// re-packing, then the two folds on 32-bit limbs with carry chains.
 __device__ __forceinline__ u64 h61_step64(u64 y, u64 x, u64 a) {
-    const u32 y0 = lo32(y), y1 = hi32(y), x0 = lo32(x), x1 = hi32(x);
-    const u64 A = mulw(y0, x0);
-    const u64 B = mulw(y0, x1) + (A >> 32);
-    const u64 Cc = mulw(y1, x0) + (u64)lo32(B);
-    const u64 D = mulw(y1, x1) + (B >> 32) + (Cc >> 32);  // y x >> 64
-    const u64 tlo = (Cc << 32) | lo32(A);                  // y x mod 2^64
-    const u64 s = (tlo & kP61) + ((D << 3) | (tlo >> 61)) + a;
-    return (s & kP61) + (s >> 61);
+    u64 r;
+    asm("{\n\t"
+        ".reg .u32 y0, y1, x0, x1, a0, a1, t0, t1, t2, t3, m0, m1, p0, p1, h0, h1, s0, s1, q;\n\t"
+        ".reg .u64 P00, M, P11;\n\t"
+        "mov.b64 {y0, y1}, %1;\n\t"
+        "mov.b64 {x0, x1}, %2;\n\t"
+        "mov.b64 {a0, a1}, %3;\n\t"
+        "mul.wide.u32 P00, y0, x0;\n\t"
+        "mul.wide.u32 M, y0, x1;\n\t"
+        "mad.wide.u32 M, y1, x0, M;\n\t"
+        "mul.wide.u32 P11, y1, x1;\n\t"
+        "mov.b64 {t0, p0}, P00;\n\t"
+        "mov.b64 {m0, m1}, M;\n\t"
+        "mov.b64 {p1, t3}, P11;\n\t"
+        "add.cc.u32 t1, p0, m0;\n\t"       // t = (t0, t1, t2, t3)
+        "addc.cc.u32 t2, p1, m1;\n\t"
+        "addc.u32 t3, t3, 0;\n\t"
+        "shf.r.clamp.b32 h0, t1, t2, 29;\n\t"  // t >> 61
+        "shf.r.clamp.b32 h1, t2, t3, 29;\n\t"
+        "and.b32 t1, t1, 0x1FFFFFFF;\n\t"      // t & p
+        "add.cc.u32 s0, t0, h0;\n\t"
+        "addc.u32 s1, t1, h1;\n\t"
+        "add.cc.u32 s0, s0, a0;\n\t"
+        "addc.u32 s1, s1, a1;\n\t"
+        "shr.u32 q, s1, 29;\n\t"                // second fold: (s & p) + (s >> 61)
+        "and.b32 s1, s1, 0x1FFFFFFF;\n\t"
+        "add.cc.u32 s0, s0, q;\n\t"
+        "addc.u32 s1, s1, 0;\n\t"
+        "mov.b64 %0, {s0, s1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(y), "l"(x), "l"(a));
+    return r;
 }
 
 // ---------------------------------------------------------------------------

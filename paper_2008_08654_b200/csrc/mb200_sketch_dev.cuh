@@ -178,6 +178,54 @@ __device__ __forceinline__ void process_item(const SketchParams& sp, u64 x, i64 
     }
 }
 
+// U independent items at once: for each family the U Horner chains are issued
+// back to back (instruction-level parallelism across items), then split and
+// scattered.  Same arithmetic and update order per item as process_item.
+template <int MODE, int K, int STRAT, int U, typename KeyT>
+__device__ __forceinline__ void process_items(const SketchParams& sp, const KeyT (&x)[U], const i64 (&delta)[U],
+                                              unsigned valid, void* smem, i64* table) {
+    if (MODE == M89) {
+        const uint32_t subs = sp.splitter == SPLIT_TWO_FOR_ONE ? 2 : 1;
+#pragma unroll 1
+        for (uint32_t f = 0; f < sp.families; ++f) {
+            u64 hlo[U], hhi[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) hash89<K>(sp, f, (u64)x[u], hlo[u], hhi[u]);
+            for (uint32_t s = 0; s < subs; ++s) {
+                const uint32_t row = subs * f + s;
+                if (row >= sp.rows) break;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (!((valid >> u) & 1)) continue;
+                    bool neg;
+                    const u64 idx = split89(sp, hlo[u], hhi[u], s, neg);
+                    const u64 d = (u64)delta[u];
+                    table_add<STRAT>(smem, table, (u64)row * sp.width + idx, neg ? (0ull - d) : d);
+                }
+            }
+        }
+    } else {
+        const uint32_t subs = sp.splitter == SPLIT_TWO_FOR_ONE ? 2 : 1;
+#pragma unroll 1
+        for (uint32_t f = 0; f < sp.families; ++f) {
+            u64 h[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) h[u] = hash_small<MODE, K>(sp, f, (u64)x[u]);
+            for (uint32_t s = 0; s < subs; ++s) {
+                const uint32_t row = subs * f + s;
+                if (row >= sp.rows) break;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (!((valid >> u) & 1)) continue;
+                    bool neg;
+                    const u64 idx = split_small(sp, h[u], s, neg);
+                    const u64 d = (u64)delta[u];
+                    table_add<STRAT>(smem, table, (u64)row * sp.width + idx, neg ? (0ull - d) : d);
+                }
+            }
+        }
+    }
+}
 
 }  // namespace sk
 }  // namespace mb200

@@ -1,0 +1,192 @@
+// C++ host-API tests: the reference's own unit-test cases (tests/unit/
+// test_{field,polyhash,sketch}.cpp under /root/reference/proj), re-run against
+// mersenne::b200 (include/mersenne_b200/mersenne_b200.hpp) on the GPU, plus
+// batch parity against the C oracle (oracle/liboracle.so, test infrastructure).
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mersenne_b200/mersenne_b200.hpp"
+#include "../../oracle/oracle.h"
+
+using namespace mersenne::b200;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                            \
+    do {                                                                       \
+        if (cond) {                                                            \
+            ++g_pass;                                                          \
+        } else {                                                               \
+            ++g_fail;                                                          \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+        }                                                                      \
+    } while (0)
+#define CHECK_THROWS_AS(expr, ex)                                                          \
+    do {                                                                                   \
+        bool thrown = false;                                                               \
+        try {                                                                              \
+            (void)(expr);                                                                  \
+        } catch (const ex&) {                                                              \
+            thrown = true;                                                                 \
+        } catch (...) {                                                                    \
+        }                                                                                  \
+        if (thrown) {                                                                      \
+            ++g_pass;                                                                      \
+        } else {                                                                           \
+            ++g_fail;                                                                      \
+            std::fprintf(stderr, "FAIL %s:%d: %s does not throw %s\n", __FILE__, __LINE__, #expr, #ex); \
+        }                                                                                  \
+    } while (0)
+
+static void test_field() {  // test_field.cpp:56-158
+    CHECK(MersenneModulus(3).p() == 7);
+    CHECK_THROWS_AS(MersenneModulus(1), std::invalid_argument);
+    CHECK_THROWS_AS(MersenneModulus(128), std::invalid_argument);
+    CHECK_THROWS_AS(MersenneModulus(11, true), std::invalid_argument);
+    MersenneModulus m13(13, true);
+    CHECK(m13.prime_exponent());
+    CHECK_THROWS_AS(PseudoMersenneModulus(4, 8), std::invalid_argument);
+    CHECK_THROWS_AS(PseudoMersenneModulus(4, 0), std::invalid_argument);
+    PseudoMersenneModulus m(4, 3, 2);
+    CHECK(m.p() == 13 && m.iterations() == 2 && m.max_input()[0] == 69);
+    u64 v[4] = {27, 0, 69, 0}, q[2], r[2];
+    m.divmod(v, 2, q, r);
+    CHECK(q[0] == 2 && r[0] == 1 && q[1] == 5 && r[1] == 4);
+    u64 bad[2] = {70, 0};
+    CHECK_THROWS_AS(m.divmod(bad, 1, q, r), std::domain_error);
+    CHECK(PseudoMersenneModulus(64, 59).iterations() == 3);
+    CHECK(PseudoMersenneModulus(61, 1).iterations() == 2);
+}
+
+static void test_polyhash() {  // test_polyhash.cpp:57-88
+    MersenneModulus m7(3, true);
+    PolyHashFamily f(m7, std::vector<u128>{3, 5}, 4);
+    CHECK(f(2) == 6 && f(0) == 3 && f(1) == 1 && f(3) == 4);
+    CHECK_THROWS_AS(f(4), std::domain_error);
+    MersenneModulus m31(5, true);
+    PolyHashFamily ident(m31, std::vector<u128>{0, 1, 0, 0}, 16);
+    PolyHashFamily constant(m31, std::vector<u128>{23, 0, 0, 0}, 16);
+    bool ok = true;
+    for (u128 x = 0; x < 16; ++x) ok &= ident(x) == x && constant(x) == 23;
+    CHECK(ok);
+    CHECK_THROWS_AS(PolyHashFamily(m31, 4, 32, 1), std::invalid_argument);
+    CHECK_THROWS_AS(PolyHashFamily(m31, 0, 16, 1), std::invalid_argument);
+    CHECK_THROWS_AS(PolyHashFamily(m31, std::vector<u128>{31}, 16), std::invalid_argument);
+    // seeded draws and a 61-bit batch vs the oracle
+    MersenneModulus m61(61, true);
+    PolyHashFamily g(m61, 4, u128(1) << 32, 0xABCDEF);
+    std::vector<u64> lo(4), hi(4);
+    orc_draw_coeffs(61, 4, 0xABCDEF, lo.data(), hi.data());
+    for (unsigned i = 0; i < 4; ++i) CHECK(g.coefficients()[i] == lo[i]);
+    std::vector<u64> keys(10000);
+    orc_gen_u64_keys(7, 0, keys.size(), keys.data());
+    for (auto& k : keys) k &= 0xFFFFFFFFull;
+    auto h = g.hash(keys);
+    std::vector<u64> out(keys.size());
+    CHECK(orc_hash_batch(61, lo.data(), hi.data(), 4, 32, keys.data(), keys.size(), out.data(), nullptr) == 0);
+    bool same = true;
+    for (size_t i = 0; i < keys.size(); ++i) same &= h[i] == out[i];
+    CHECK(same);
+    // 89-bit family
+    MersenneModulus m89(89, true);
+    PolyHashFamily g89(m89, 4, u128(1) << 64, 3);
+    orc_draw_coeffs(89, 4, 3, lo.data(), hi.data());
+    orc_gen_u64_keys(8, 0, keys.size(), keys.data());
+    auto h89 = g89.hash(keys);
+    std::vector<u64> oh(keys.size());
+    orc_hash_batch(89, lo.data(), hi.data(), 4, 64, keys.data(), keys.size(), out.data(), oh.data());
+    same = true;
+    for (size_t i = 0; i < keys.size(); ++i) same &= h89[i] == ((u128(oh[i]) << 64) | out[i]);
+    CHECK(same);
+}
+
+static void test_sketch() {  // test_sketch.cpp
+    CHECK((split_pow2(0b110, 3, 2) == SignIndexPair{2, -1}));
+    CHECK((split_pow2(0, 3, 2) == SignIndexPair{0, +1}));
+    CHECK((split_pow2(0b011, 3, 2) == SignIndexPair{3, +1}));
+    MersenneModulus m61(61, true);
+    {
+        CountSketch sk(3, 8, m61, u128(1) << 32, Splitter::Pow2, 0xF00D);
+        CHECK(sk.second_moment().value == 0);
+        sk.process(123, -7);
+        for (unsigned r = 0; r < 3; ++r) CHECK(sk.row_second_moment(r).value == 49);
+        CHECK(sk.second_moment(true).value == 49);
+    }
+    {
+        CountSketch sk(3, 8, m61, u128(1) << 32, Splitter::MersenneArb, 0xCAFE);
+        sk.process(17, 5);
+        sk.process(17, -5);
+        bool zero = true;
+        for (i64 c : sk.counters()) zero &= c == 0;
+        CHECK(zero);
+    }
+    {
+        CountSketch sk(5, 16, m61, u128(1) << 32, Splitter::MersenneArb, 0xBEEF);
+        CHECK(sk.point_query(42) == 0);
+        sk.process(42, 1234);
+        CHECK(sk.point_query(42) == 1234);
+        sk.process(42, -234);
+        CHECK(sk.point_query(42) == 1000);
+    }
+    {  // merge equals the concatenated stream (test_sketch.cpp:239-261)
+        auto fresh = [&] { return CountSketch(3, 32, m61, u128(1) << 32, Splitter::MersenneArb, 0x5EED); };
+        CountSketch a = fresh(), b = fresh(), both = fresh();
+        std::vector<u64> k(600);
+        std::vector<i64> d(600);
+        for (size_t i = 0; i < k.size(); ++i) {
+            k[i] = orc_splitmix_at(0xAB, 2 * i) & 0xFFFF;
+            d[i] = i64(orc_splitmix_at(0xAB, 2 * i + 1) % 200) - 100;
+        }
+        a.process_batch(k.data(), 64, d.data(), MB200_W_I64, 300);
+        b.process_batch(k.data() + 300, 64, d.data() + 300, MB200_W_I64, 300);
+        both.process_batch(k.data(), 64, d.data(), MB200_W_I64, 600);
+        a.merge(b);
+        CHECK(a.counters() == both.counters());
+        CHECK_THROWS_AS(a.merge(CountSketch(3, 32, m61, u128(1) << 32, Splitter::MersenneArb, 1)),
+                        std::invalid_argument);
+    }
+    // construction validation (test_sketch.cpp:278-298)
+    MersenneModulus m31(5, true);
+    CHECK_THROWS_AS(CountSketch(1, 1, m61, 16, Splitter::MersenneArb, 1), std::invalid_argument);
+    CHECK_THROWS_AS(CountSketch(0, 8, m61, 16, Splitter::Pow2, 1), std::invalid_argument);
+    CHECK_THROWS_AS(CountSketch(1, 24, m61, 16, Splitter::Pow2, 1), std::invalid_argument);
+    CHECK_THROWS_AS(CountSketch(1, 32, m31, 16, Splitter::Pow2, 1), std::invalid_argument);
+    CHECK_THROWS_AS(CountSketch(1, 17, m31, 16, Splitter::MersenneArb, 1), std::invalid_argument);
+    CHECK_THROWS_AS(CountSketch(1, 4, m31, 32, Splitter::Pow2, 1), std::invalid_argument);
+    {
+        CountSketch sk(1, 4, m31, 16, Splitter::Pow2, 1);
+        CHECK_THROWS_AS(sk.process(16, 1), std::domain_error);
+        CHECK_THROWS_AS(sk.point_query(16), std::domain_error);
+    }
+    {  // config-1 slice through the host-buffer batch API vs the oracle
+        CountSketch sk(1, 1024, m61, u128(1) << 32, Splitter::Pow2, 1);
+        std::vector<uint32_t> keys(1 << 20);
+        orc_gen_u32_keys(1 ^ 0x7b5bad595e238e31ull, 0, keys.size(), keys.data());
+        sk.process_batch(keys.data(), 32, nullptr, MB200_W_NONE, keys.size());
+        std::vector<u64> lo(4), hi(4);
+        orc_draw_coeffs(61, 4, sk.seeds()[0], lo.data(), hi.data());
+        std::vector<int64_t> exp(1024, 0);
+        orc_cs_process(1, 1024, 61, 4, lo.data(), hi.data(), 32, 0, nullptr, keys.data(), nullptr, nullptr,
+                       keys.size(), exp.data());
+        CHECK(sk.counters() == exp);
+        u64 vlo, vhi;
+        int sat;
+        orc_cs_row_moment(exp.data(), 1024, &vlo, &vhi, &sat);
+        CHECK(sk.second_moment().value == ((u128(vhi) << 64) | vlo));
+    }
+}
+
+int main() {
+    try {
+        test_field();
+        test_polyhash();
+        test_sketch();
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "unexpected exception: %s\n", e.what());
+        return 2;
+    }
+    std::printf("%d checks passed, %d failed\n", g_pass, g_fail);
+    return g_fail ? 1 : 0;
+}

@@ -171,6 +171,8 @@ int mb200_hash61(const void* d_keys, int key_width, uint64_t n, unsigned b, cons
     if (!coeffs) return fail(MB200_INVALID_ARGUMENT, "null coefficients");
     HashParams hp;
     std::memset(&hp, 0, sizeof(hp));
+    hp.c31 = 0x80000000u;
+    hp.c2 = 2;
     hp.b = b;
     hp.k = k;
     hp.p = (1ull << b) - 1;

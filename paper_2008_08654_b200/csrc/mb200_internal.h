@@ -17,6 +17,7 @@ enum SplitKind { SPLIT_POW2 = 0, SPLIT_UNIFORM_ARB = 1, SPLIT_MERSENNE_ARB = 2, 
 
 struct HashParams {
     uint32_t b, k;
+    uint32_t c31 = 0x80000000u, c2 = 2;  // opaque multipliers (see h61_step_l31)
     uint64_t p;
     uint64_t lo[kMaxK];
     uint64_t hi[kMaxK];

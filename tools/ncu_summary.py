@@ -50,7 +50,11 @@ def main(rep, top=12):
     iI = hdr.index("Instructions Executed")
     iS = hdr.index("Warp Stall Sampling (All Samples)")
     lines = [x for x in r if len(x) > iI and x[0].isdigit()]
-    f = lambda s: float(s) if s not in ("", "-") else 0.0  # noqa: E731
+    def f(s):
+        try:
+            return float(s)
+        except ValueError:
+            return 0.0
     ti = sum(f(x[iI]) for x in lines) or 1
     ts = sum(f(x[iS]) for x in lines) or 1
     print(f"  top source lines (of {ti:.3g} warp instructions):")

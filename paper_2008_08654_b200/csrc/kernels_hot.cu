@@ -14,17 +14,15 @@
 //                  from the count histogram so that at most H qualify) form the
 //                  hot list, with their sample counts;
 //   3. cs_hot    : one 1024-thread CTA per SM keeps the hot keys in a shared-
-//                  memory table (hottest keys inserted first, so they sit in
-//                  their home slots) with an exact 64-bit accumulator per key
-//                  (two u32 words: a 2^31-biased low word plus a wrap counter).
-//                  A hit costs one shared atomic and no hashing.  Misses are
+//                  memory table with an exact 64-bit accumulator per key.  A hit
+//                  costs one shared reduction and no hashing.  Misses are
 //                  compacted per warp into full-warp batches that run the fused
 //                  hash -> split -> red.global path.  Warps pull 128-item tiles
 //                  of their CTA's contiguous range from a shared counter, so
 //                  they finish together.  Finally each CTA applies every hot key
 //                  once (hash -> split -> red).
-// The table is bit-identical to the per-item path for ANY hot list (integer
-// addition commutes); the hot list only decides how much L2 traffic is saved.
+// The table is bit-identical to the per-item path for ANY hot set (integer
+// addition commutes); the hot set only decides how much L2 traffic is saved.
 #include <type_traits>
 
 #include "mb200_sketch_dev.cuh"
@@ -40,7 +38,7 @@ constexpr int kHotWarps = kHotThreads / 32;
 constexpr uint32_t kHotSample = 1u << 18;
 constexpr uint32_t kCountLog2 = 20;
 constexpr uint32_t kCountSlots = 1u << kCountLog2;
-constexpr int kQueue = 64;  // < 32 queued + one slot of 32 misses
+constexpr int kQueue = 64;     // < 32 queued + one slot of 32 misses
 constexpr int kTileSlots = 4;  // items per lane per tile
 constexpr uint64_t kTile = 32ull * kTileSlots;
 
@@ -48,29 +46,42 @@ template <typename KeyT>
 struct HotGeom;
 template <>
 struct HotGeom<u32> {
-    static constexpr uint32_t kLog2 = 14;  // 16384 slots x 12 B = 192 KiB
+    static constexpr uint32_t kLog2 = 14;  // 16384 slots x (4 B key + 8 B sum) = 192 KiB
     static constexpr uint32_t kCap = 8192;
     static constexpr u32 kEmpty = 0xffffffffu;
-    static constexpr uint32_t kWays = 4;  // keys per 16-byte bucket
     using Cas = unsigned;
 };
 template <>
 struct HotGeom<u64> {
-    static constexpr uint32_t kLog2 = 13;  // 8192 slots x 16 B = 128 KiB
+    static constexpr uint32_t kLog2 = 13;  // 8192 slots x (8 B key + 8 B sum) = 128 KiB
     static constexpr uint32_t kCap = 4096;
     static constexpr u64 kEmpty = ~0ull;
-    static constexpr uint32_t kWays = 2;
     using Cas = unsigned long long;
 };
 
-// home slot from the HIGH bits of a multiplicative / splitmix hash
+__device__ __forceinline__ u32 fmix32(u32 h) {
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    return h ^ (h >> 16);
+}
+// two independent slot choices from the HIGH bits of multiplicative / mixing hashes
 template <uint32_t LOG2>
-__device__ __forceinline__ u32 home(u32 key) {
+__device__ __forceinline__ u32 slot1(u32 key) {
     return (key * 0x9E3779B1u) >> (32 - LOG2);
 }
 template <uint32_t LOG2>
-__device__ __forceinline__ u32 home(u64 key) {
+__device__ __forceinline__ u32 slot2(u32 key) {
+    return fmix32(key) >> (32 - LOG2);
+}
+template <uint32_t LOG2>
+__device__ __forceinline__ u32 slot1(u64 key) {
     return (u32)(mix64(key) >> (64 - LOG2));
+}
+template <uint32_t LOG2>
+__device__ __forceinline__ u32 slot2(u64 key) {
+    return (u32)(mix64(key) >> 20) & ((1u << LOG2) - 1);
 }
 
 template <typename KeyT>
@@ -81,7 +92,7 @@ __global__ void hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT*
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const KeyT key = ld_nc(keys + i);
         if (key == G::kEmpty) continue;
-        u32 h = home<kCountLog2>(key);
+        u32 h = slot1<kCountLog2>(key);
         for (;;) {
             KeyT cur = tk[h];
             if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(tk + h), (C)G::kEmpty, (C)key);
@@ -133,48 +144,11 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
     }
 }
 
-// bucket choices of the shared hot table (4096 buckets of 16 bytes)
-constexpr uint32_t kBucketLog2 = 12;
-__device__ __forceinline__ u32 fmix32(u32 h) {
-    h ^= h >> 16;
-    h *= 0x85ebca6bu;
-    h ^= h >> 13;
-    h *= 0xc2b2ae35u;
-    return h ^ (h >> 16);
-}
-__device__ __forceinline__ u32 bucket1(u32 key) { return (key * 0x9E3779B1u) >> (32 - kBucketLog2); }
-__device__ __forceinline__ u32 bucket2(u32 key) { return fmix32(key) >> (32 - kBucketLog2); }
-__device__ __forceinline__ u32 bucket1(u64 key) { return (u32)(mix64(key) >> (64 - kBucketLog2)); }
-__device__ __forceinline__ u32 bucket2(u64 key) { return (u32)(mix64(key) >> 20) & ((1u << kBucketLog2) - 1); }
-
-// slot of `key` in the bucketed table, or -1
-__device__ __forceinline__ int find_slot(const u32* hk, u32 key) {
-    const u32 b1 = bucket1(key);
-    const uint4 v = *reinterpret_cast<const uint4*>(hk + 4 * b1);
-    int s = v.x == key ? 0 : v.y == key ? 1 : v.z == key ? 2 : v.w == key ? 3 : -1;
-    if (s >= 0) return (int)(4 * b1) + s;
-    const bool full = (v.x != 0xffffffffu) & (v.y != 0xffffffffu) & (v.z != 0xffffffffu) & (v.w != 0xffffffffu);
-    if (!full) return -1;
-    const u32 b2 = bucket2(key);
-    const uint4 q = *reinterpret_cast<const uint4*>(hk + 4 * b2);
-    s = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
-    return s >= 0 ? (int)(4 * b2) + s : -1;
-}
-__device__ __forceinline__ int find_slot(const u64* hk, u64 key) {
-    const u32 b1 = bucket1(key);
-    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(hk + 2 * b1);
-    if (v.x == key) return (int)(2 * b1);
-    if (v.y == key) return (int)(2 * b1) + 1;
-    if (v.x == ~0ull || v.y == ~0ull) return -1;
-    const u32 b2 = bucket2(key);
-    const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(hk + 2 * b2);
-    if (q.x == key) return (int)(2 * b2);
-    if (q.y == key) return (int)(2 * b2) + 1;
-    return -1;
-}
-
-// exact 64-bit accumulation in two u32 words (|d| <= 2^31): the low word carries
-// a 2^31 bias so a sum hovering around zero never wraps; the high word counts wraps
+// Exact 64-bit accumulation in two u32 words (|d| <= 2^31).  sm_100 has no
+// native 64-bit shared-memory add (atomicAdd on u64 in shared memory compiles
+// to an ATOMS.CAST.SPIN.64 loop, which serialises on hot keys: 101 ms instead
+// of 13 ms on config 5), so: the low word carries a 2^31 bias, so a sum hovering
+// around zero never wraps, and the high word counts the wraps.
 __device__ __forceinline__ void hot_accumulate(u32* lo, u32* hi, u32 h, i32 d) {
     const u32 dd = (u32)d;
     const u32 old = atomicAdd(lo + h, dd);
@@ -215,14 +189,11 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     }
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
+    // Two-choice table, one key per slot: a key goes to slot1 if free, else to
+    // slot2 if free, else it stays cold (exactness never depends on the hot set).
+    // Slots are never freed, so a lookup whose slot1 is empty is a miss without
+    // touching slot2.  Hottest keys are placed first so they own their slot1.
     const u32 nhot = min(*hot_count, G::kCap);
-    // Two-choice bucketed table: a key lives in one of the 16-byte buckets b1/b2
-    // (4 u32 or 2 u64 keys each), so a lookup is at most two vector loads and
-    // never a divergent probe loop.  Hottest keys first, into b1 while it has
-    // room; a key reaches b2 only once b1 is full, so a lookup whose b1 still
-    // has an empty slot is a miss without reading b2.  Keys that find both
-    // buckets full stay cold (exactness does not depend on the hot set).
-    // hi[] doubles as the per-bucket fill counter during the build.
     const u32 bands[3] = {64u, 8u, 0u};
     u32 upper = 0xffffffffu;
     for (int r = 0; r < 3; ++r) {
@@ -230,19 +201,12 @@ __global__ void __launch_bounds__(kHotThreads, 1)
             const u32 c = hot_cnt[j];
             if (c < bands[r] || c >= upper) continue;
             const KeyT key = hot[j];
-            const u32 b1 = bucket1(key), b2 = bucket2(key);
-            u32 pos = atomicAdd(hi + b1, 1u);
-            if (pos < G::kWays) {
-                hk[b1 * G::kWays + pos] = key;
-            } else if ((pos = atomicAdd(hi + b2, 1u)) < G::kWays) {
-                hk[b2 * G::kWays + pos] = key;
-            }
+            if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + slot1<G::kLog2>(key)), (C)G::kEmpty, (C)key) != G::kEmpty)
+                atomicCAS(reinterpret_cast<C*>(hk + slot2<G::kLog2>(key)), (C)G::kEmpty, (C)key);
         }
         upper = bands[r];
         __syncthreads();
     }
-    for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) hi[s] = 0;
-    __syncthreads();
 
     const uint64_t lo_item = n * blockIdx.x / gridDim.x, hi_item = n * (blockIdx.x + 1) / gridDim.x;
     const uint64_t ntiles = (hi_item - lo_item + kTile - 1) / kTile;
@@ -259,23 +223,26 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         for (int u = 0; u < kTileSlots; ++u) {
             const uint64_t i = base + u * 32 + lane;
             const bool v = i < hi_item;
-            kx[u] = v ? ld_nc(keys + i) : KeyT(0);
+            kx[u] = v ? ld_nc(keys + i) : G::kEmpty;
             dx[u] = v ? load_w32<WK>(w, i) : 0;
         }
 #pragma unroll
         for (int u = 0; u < kTileSlots; ++u) {
             const bool valid = base + u * 32 + lane < hi_item;
-            bool hit = false;
-            if (valid && kx[u] != G::kEmpty) {
-                const int h = find_slot(hk, kx[u]);
-                hit = h >= 0;
-                if (hit) hot_accumulate(lo, hi, (u32)h, dx[u]);
+            const KeyT key = kx[u];
+            u32 h = slot1<G::kLog2>(key);
+            KeyT cur = hk[h];
+            if (cur != key && cur != G::kEmpty) {
+                h = slot2<G::kLog2>(key);
+                cur = hk[h];
             }
+            const bool hit = cur == key && key != G::kEmpty;
+            if (hit) hot_accumulate(lo, hi, h, dx[u]);
             const bool miss = valid && !hit;
             const unsigned m = __ballot_sync(kFull, miss);
             if (miss) {
                 const int pos = qn + __popc(m & ((1u << lane) - 1));
-                wqk[pos] = kx[u];
+                wqk[pos] = key;
                 wqd[pos] = dx[u];
             }
             qn += __popc(m);

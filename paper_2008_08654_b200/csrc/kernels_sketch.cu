@@ -38,7 +38,7 @@ using namespace sk;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-template <int MODE, int K, typename KeyT, int WK, int STRAT>
+template <int MODE, int K, typename KeyT, int WK, int STRAT, int FAM>
 __global__ void __launch_bounds__(kThreads) cs_update_kernel(const SketchParams sp,
                                                              const KeyT* __restrict__ keys,
                                                              const void* __restrict__ w, uint64_t n,
@@ -47,7 +47,11 @@ __global__ void __launch_bounds__(kThreads) cs_update_kernel(const SketchParams 
     __shared__ i64 scratch[kWarps][32];
     void* smem = smem_raw;
     const uint64_t cells = (uint64_t)sp.rows * sp.width;
-    if (STRAT != GLOBAL) {
+    if (STRAT == SMEM_LOHI) {  // 2^31-biased low words + wrap counters (see table_add)
+        for (uint64_t i = threadIdx.x; i < 2 * kLohiCells; i += kThreads)
+            reinterpret_cast<u32*>(smem)[i] = i < kLohiCells ? 0x80000000u : 0u;
+        __syncthreads();
+    } else if (STRAT != GLOBAL) {
         const uint64_t words = STRAT == SMEM32 ? cells : 2 * cells;
         for (uint64_t i = threadIdx.x; i < words; i += kThreads) reinterpret_cast<u32*>(smem)[i] = 0;
         __syncthreads();
@@ -56,6 +60,39 @@ __global__ void __launch_bounds__(kThreads) cs_update_kernel(const SketchParams 
     const uint64_t warps_total = (uint64_t)gridDim.x * kWarps;
     const uint64_t gw = (uint64_t)blockIdx.x * kWarps + warp;
     const uint64_t tile = 32ull * kSlots;
+    if (STRAT != GLOBAL || !aggregate) {
+        // independent items: the slots' Horner chains interleave, and the next
+        // tile's loads are in flight while this one is hashed
+        KeyT kx[kSlots];
+        i64 dx[kSlots];
+        uint64_t base = gw * tile;
+#pragma unroll
+        for (int u = 0; u < kSlots; ++u) {
+            const uint64_t i = base + u * 32 + lane;
+            kx[u] = i < n ? ld_nc(keys + i) : KeyT(0);
+            dx[u] = i < n ? load_weight<WK>(w, i) : 0;
+        }
+        for (; base < n; base += warps_total * tile) {
+            const uint64_t nb = base + warps_total * tile;
+            KeyT kn[kSlots];
+            i64 dn[kSlots];
+#pragma unroll
+            for (int u = 0; u < kSlots; ++u) {
+                const uint64_t i = nb + u * 32 + lane;
+                kn[u] = i < n ? ld_nc(keys + i) : KeyT(0);
+                dn[u] = i < n ? load_weight<WK>(w, i) : 0;
+            }
+            unsigned valid = 0;
+#pragma unroll
+            for (int u = 0; u < kSlots; ++u) valid |= (base + u * 32 + lane < n ? 1u : 0u) << u;
+            process_items<MODE, K, STRAT, kSlots, FAM>(sp, kx, dx, valid, smem, table);
+#pragma unroll
+            for (int u = 0; u < kSlots; ++u) {
+                kx[u] = kn[u];
+                dx[u] = dn[u];
+            }
+        }
+    } else {
     for (uint64_t base = gw * tile; base < n; base += warps_total * tile) {
         KeyT kx[kSlots];
         i64 dx[kSlots];
@@ -64,14 +101,6 @@ __global__ void __launch_bounds__(kThreads) cs_update_kernel(const SketchParams 
             const uint64_t i = base + u * 32 + lane;
             kx[u] = i < n ? ld_nc(keys + i) : KeyT(0);
             dx[u] = i < n ? load_weight<WK>(w, i) : 0;
-        }
-        if (STRAT != GLOBAL || !aggregate) {
-            // independent items: the slots' Horner chains interleave
-            unsigned valid = 0;
-#pragma unroll
-            for (int u = 0; u < kSlots; ++u) valid |= (base + u * 32 + lane < n ? 1u : 0u) << u;
-            process_items<MODE, K, STRAT, kSlots>(sp, kx, dx, valid, smem, table);
-            continue;
         }
 #pragma unroll 1
         for (int u = 0; u < kSlots; ++u) {
@@ -100,11 +129,15 @@ __global__ void __launch_bounds__(kThreads) cs_update_kernel(const SketchParams 
             }
         }
     }
+    }
     if (STRAT != GLOBAL) {
         __syncthreads();
         for (uint64_t c = threadIdx.x; c < cells; c += kThreads) {
             u64 v;
             if (STRAT == SMEM32) v = (u64)(i64)(i32)reinterpret_cast<u32*>(smem)[c];
+            else if (STRAT == SMEM_LOHI)
+                v = (((u64)reinterpret_cast<u32*>(smem)[kLohiCells + c] << 32) | reinterpret_cast<u32*>(smem)[c]) -
+                    0x80000000ull;
             else v = reinterpret_cast<u64*>(smem)[c];
             if (v) red_add_u64(reinterpret_cast<uint64_t*>(table) + c, v);
         }
@@ -204,12 +237,17 @@ int blocks_per_sm_cache(const void* fn, size_t smem) {
     return v > 0 ? v : 1;
 }
 
-template <int MODE, int K, typename KeyT, int WK, int STRAT>
+template <int MODE, int K, typename KeyT, int WK, int STRAT, int FAM = 0>
 cudaError_t launch_strat(const SketchParams& sp, const void* keys, const void* w, uint64_t n, int64_t* table,
                          cudaStream_t s, bool aggregate) {
-    auto fn = cs_update_kernel<MODE, K, KeyT, WK, STRAT>;
+    // one family with the Pow2 splitter (config 1's shape) gets a loop-free body
+    if (FAM == 0 && STRAT != GLOBAL && sp.families == 1 && sp.rows == 1 && sp.splitter == SPLIT_POW2)
+        return launch_strat<MODE, K, KeyT, WK, STRAT, 1>(sp, keys, w, n, table, s, aggregate);
+    auto fn = cs_update_kernel<MODE, K, KeyT, WK, STRAT, FAM>;
     const uint64_t cells = (uint64_t)sp.rows * sp.width;
-    const size_t smem = STRAT == GLOBAL ? 0 : (size_t)cells * (STRAT == SMEM32 ? 4 : 8);
+    const size_t smem = STRAT == GLOBAL      ? 0
+                        : STRAT == SMEM_LOHI ? (size_t)kLohiCells * 8
+                                             : (size_t)cells * (STRAT == SMEM32 ? 4 : 8);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -232,6 +270,10 @@ cudaError_t launch_w(const SketchParams& sp, const void* keys, const void* w, ui
     // sees fewer than 2^31 items; 64-bit otherwise.
     if (WK == W_NONE && cells * 4 <= 64 * 1024 && n < (1ull << 31))
         return launch_strat<MODE, K, KeyT, WK, SMEM32>(sp, keys, w, n, table, s, false);
+    // |delta| <= 2^31: exact two-word shared counters on native 32-bit atomics
+    if (WK != W_I64 && cells <= kLohiCells)
+        return launch_strat<MODE, K, KeyT, WK, SMEM_LOHI>(sp, keys, w, n, table, s, false);
+    // 64-bit shared atomics are CAS loops on sm_100: only for int64 weights
     if (cells * 8 <= 64 * 1024) return launch_strat<MODE, K, KeyT, WK, SMEM64>(sp, keys, w, n, table, s, false);
     // large batches: heavy-hitter accumulation in shared memory (|delta| < 2^31 for the
     // exact two-word accumulator), everything else straight to L2

@@ -17,7 +17,8 @@ constexpr int kSlots = 4;  // items per lane per warp-iteration (loads in flight
 constexpr unsigned kFull = 0xffffffffu;
 
 enum Mode { M61_K32 = 0, M61_K64 = 1, M89 = 2, MGEN = 3 };
-enum Strat { SMEM32 = 0, SMEM64 = 1, GLOBAL = 2 };
+enum Strat { SMEM32 = 0, SMEM64 = 1, GLOBAL = 2, SMEM_LOHI = 3 };
+constexpr uint32_t kLohiCells = 8192;  // SMEM_LOHI table capacity (2 x 32 KiB)
 
 template <typename T>
 __device__ __forceinline__ T ld_nc(const T* p) {
@@ -126,6 +127,15 @@ template <int STRAT>
 __device__ __forceinline__ void table_add(void* smem, i64* table, u64 cell, u64 sd) {
     if (STRAT == SMEM32) {
         atomicAdd(reinterpret_cast<unsigned*>(smem) + cell, (unsigned)sd);
+    } else if (STRAT == SMEM_LOHI) {
+        // exact 64-bit counter as a 2^31-biased low word + wrap counter, on native
+        // 32-bit shared atomics (|sd| <= 2^31; sm_100 has no 64-bit shared add)
+        u32* lo = reinterpret_cast<u32*>(smem);
+        const u32 dd = (u32)sd;
+        const u32 old = atomicAdd(lo + cell, dd);
+        const u32 nw = old + dd;
+        const int carry = (i64)sd >= 0 ? (int)(nw < old) : -(int)(nw > old);
+        if (carry) atomicAdd(lo + kLohiCells + cell, (u32)carry);
     } else if (STRAT == SMEM64) {
         red_add_shared_u64(reinterpret_cast<uint64_t*>(smem) + cell, sd);
     } else {
@@ -181,9 +191,24 @@ __device__ __forceinline__ void process_item(const SketchParams& sp, u64 x, i64 
 // U independent items at once: for each family the U Horner chains are issued
 // back to back (instruction-level parallelism across items), then split and
 // scattered.  Same arithmetic and update order per item as process_item.
-template <int MODE, int K, int STRAT, int U, typename KeyT>
+template <int MODE, int K, int STRAT, int U, int FAM = 0, typename KeyT>
 __device__ __forceinline__ void process_items(const SketchParams& sp, const KeyT (&x)[U], const i64 (&delta)[U],
                                               unsigned valid, void* smem, i64* table) {
+    if (FAM == 1 && MODE != M89) {
+        // one family, Pow2 splitter (the caller checked): no loops, no splitter switch
+        u64 h[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) h[u] = hash_small<MODE, K>(sp, 0, (u64)x[u]);
+        const u32 top = sp.b - 1;
+        const u64 mask = sp.width - 1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!((valid >> u) & 1)) continue;
+            const u64 d = (u64)delta[u];
+            table_add<STRAT>(smem, table, h[u] & mask, ((h[u] >> top) & 1) ? (0ull - d) : d);
+        }
+        return;
+    }
     if (MODE == M89) {
         const uint32_t subs = sp.splitter == SPLIT_TWO_FOR_ONE ? 2 : 1;
 #pragma unroll 1

@@ -266,13 +266,42 @@ def main():
         e1.synchronize()
         best = min(best, e0.elapsed_time(e1) / 1e3)
     imad_peak = blocks * threads * 8 * iters / best  # IMAD.WIDE.U32 per second
+    # L2 reduction peak: red.global.add.u64 on random cells of a config-5-sized table
+    red_buf = torch.zeros(C5_ROWS * C5_WIDTH, dtype=torch.int64, device=dev)
+    rblocks, rthreads, riters = mb_sm_count(torch) * 8, 256, 256
+    best = 1e9
+    for rep in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        mb.probe_atomics(2, rblocks, rthreads, riters, red_buf, C5_ROWS * C5_WIDTH)
+        e1.record()
+        e1.synchronize()
+        if rep:
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+    red_peak = rblocks * rthreads * riters / best
+    del red_buf
 
-    def roofline(cfg, units, kernel_s, kname):
+    def roofline(cfg, units, kernel_s, kname, l2_reds=None):
         bpu, lpu = WORK[cfg]
         hbm = units * bpu / kernel_s / 1e9
         ints = units * lpu / kernel_s
         frac_h, frac_i = hbm / hbm_peak, ints / imad_peak
-        tr = traffic.get(kname)
+        tr = (traffic.get(kname) or {}).get("dram_bytes_per_launch")
+        if l2_reds is not None:
+            red_rate = l2_reds / kernel_s
+            views = {"hbm": {"achieved": hbm, "peak": hbm_peak, "unit": "GB/s", "frac": frac_h,
+                             "peak_kind": peak_kind, "frac_of_8TBs": hbm / 8000.0},
+                     "int": {"achieved": ints / 1e12, "peak": imad_peak / 1e12, "unit": "T IMAD.WIDE/s",
+                             "frac": frac_i, "peak_kind": "measured (probe_imad, this run)",
+                             "note": "algorithmic limb products (SURVEY 8d) / measured IMAD.WIDE.U32 peak"},
+                     "l2_red": {"achieved": red_rate / 1e9, "peak": red_peak / 1e9, "unit": "G red/s",
+                                "frac": red_rate / red_peak, "reds_per_launch": l2_reds,
+                                "peak_kind": "measured (probe_atomics random red.global.add.u64, this run)"}}
+            bound = max(views, key=lambda k: views[k]["frac"])
+            out = {"bound": bound, **{k: views[bound][k] for k in ("achieved", "peak", "unit", "frac")},
+                   "traffic": tr, "peak_kind": views[bound]["peak_kind"]}
+            out.update({k: v for k, v in views.items() if k != bound})
+            return out
         if frac_h >= frac_i:
             return {"bound": "hbm", "achieved": hbm, "peak": hbm_peak, "unit": "GB/s", "frac": frac_h,
                     "traffic": tr, "peak_kind": peak_kind,
@@ -310,6 +339,7 @@ def main():
 
     for _ in range(max(3, args.warmup)):
         c5_step()
+    mb.hot_stats(reset=True)  # synchronizes; outside the timed region
     barrier_sync()
     t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -320,6 +350,9 @@ def main():
         barrier_sync()
     elapsed = max_over_ranks(t_start.elapsed_time(t_stop) / 1e3)
     kern = max_over_ranks(sum(a.elapsed_time(b) for a, b in k_ev) / 1e3 / args.steps)
+    hs = mb.hot_stats(reset=True)
+    # L2 reductions per launch: every miss and every applied hot key touches the 5 rows
+    c5_reds = C5_ROWS * (hs["misses"] + hs["hot_applied"]) / args.steps
     moments = mb.moments_to_python(mom)
     f2 = mb.lower_median(moments)
     value = n_total * args.steps / elapsed
@@ -336,11 +369,16 @@ def main():
                    "l2": "inputs 16 GiB >> 126 MB L2 (no flush needed)"},
         "hashes_per_s": value * C5_ROWS,
         "f2_median": str(f2[0]),
-        "roofline": roofline("c5", n_local, kern, "cs_update_kernel"),
+        "roofline": roofline("c5", n_local, kern, "c5", l2_reds=c5_reds),
         "kernel_ms": kern * 1e3,
-        "gpu_launches": 2 * args.steps,
+        "hot_path": {"miss_fraction": hs["misses"] / max(1, hs["items"]),
+                     "hot_keys_per_cta": hs["hot_keys"] / max(1, args.steps * mb_sm_count(torch)),
+                     "l2_reds_per_item": c5_reds / max(1, n_local)},
+        # per step: hh_count, hh_hist, hh_select, cs_hot, cs_moments (the table zeroing is a torch fill)
+        "gpu_launches": 5 * args.steps,
         "clocks": clocks,
-        "peaks": {"imad_wide_per_s": imad_peak, "hbm_gbs": hbm_peak, "hbm_kind": peak_kind},
+        "peaks": {"imad_wide_per_s": imad_peak, "l2_red_per_s": red_peak, "hbm_gbs": hbm_peak,
+                  "hbm_kind": peak_kind},
     }
     del keys, wts
 
@@ -440,7 +478,7 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
     tk = max_over_ranks(timed_steps(torch, steps, args.warmup, lambda: mb.cs_update(spec, keys, table), flush))
     out["c1"] = {"value": C1_ITEMS / t, "unit": "updates/s", "ms_per_step": t * 1e3,
                  "workload": "CountSketch(1,1024), 2^24 u32 keys, delta +1", "l2": "flushed between steps",
-                 "roofline": roofline("c1", hi - lo, tk, "cs_update_kernel")}
+                 "roofline": roofline("c1", hi - lo, tk, "c1")}
     del keys
 
     # config 2: raw hashing, 2^28 u64 keys uniform in [0, p), k = 4 and 8
@@ -455,7 +493,7 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
         out[f"c2_k{k}"] = {"value": C2_KEYS / t, "unit": "hashes/s", "ms_per_step": t * 1e3,
                            "workload": f"degree-{k-1} mod 2^61-1, 2^28 u64 keys in [0,p)",
                            "l2": "inputs 2 GiB > L2",
-                           "roofline": roofline(f"c2_k{k}", hi - lo, t, "hash61_key64_kernel")}
+                           "roofline": roofline(f"c2_k{k}", hi - lo, t, f"c2k{k}")}
     del keys, outb
 
     # config 3: div/mod by 2^64 - 59 of 2^28 u128 inputs in [0, p^2)
@@ -469,7 +507,7 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
     assert int(ovf.item()) == 0
     out["c3"] = {"value": C3_UNITS / t, "unit": "divmod/s", "ms_per_step": t * 1e3,
                  "workload": "Alg 4+5 by 2^64-59 (m=3), 2^28 u128 inputs in [0,p^2)", "l2": "inputs 4 GiB > L2",
-                 "roofline": roofline("c3", hi - lo, t, "pm_divmod_kernel")}
+                 "roofline": roofline("c3", hi - lo, t, "c3")}
     del v, q, r
 
     # config 4: 89-bit two-for-one, 2^26 u64 keys -> two rows of 2^16 counters
@@ -487,10 +525,13 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
         mb.cs_moments(table, 2, 1 << 16, mom)
 
     t = max_over_ranks(timed_steps(torch, steps, args.warmup, c4))
+    mb.hot_stats(reset=True)
     tk = max_over_ranks(timed_steps(torch, steps, args.warmup, lambda: mb.cs_update(spec, keys, table)))
+    hs = mb.hot_stats(reset=True)
+    c4_reds = 2 * (hs["misses"] + hs["hot_applied"]) / (steps + max(3, args.warmup))
     out["c4"] = {"value": C4_KEYS / t, "unit": "keys/s", "row_updates_per_s": 2 * C4_KEYS / t,
                  "ms_per_step": t * 1e3, "workload": "2^89-1 two-for-one, 2^26 u64 keys, 2 x 2^16 counters",
-                 "l2": "inputs 512 MiB > L2", "roofline": roofline("c4", hi - lo, tk, "cs_update_kernel")}
+                 "l2": "inputs 512 MiB > L2", "roofline": roofline("c4", hi - lo, tk, "c4", l2_reds=c4_reds)}
     del keys, flushbuf
     return out
 

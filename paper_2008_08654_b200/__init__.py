@@ -286,6 +286,13 @@ def probe_dsmem(cluster: int, mode: int, blocks: int, threads: int, iters: int, 
     check(lib.mb200_probe_dsmem(cluster, mode, blocks, threads, iters, words, _dptr(out), _stream(stream)))
 
 
+def hot_stats(reset: bool = False) -> dict:
+    """Counters of the heavy-hitter Count Sketch kernel since the last reset."""
+    out = np.zeros(4, np.uint64)
+    check(lib.mb200_hot_stats(_p(out), int(reset)))
+    return {"items": int(out[0]), "misses": int(out[1]), "hot_applied": int(out[2]), "hot_keys": int(out[3])}
+
+
 # ------------------------------------------------------------------ host object
 class CountSketch:
     """mersenne::CountSketch (sketch.hpp:40-92) with counters in HBM; host-buffer API."""

@@ -109,6 +109,7 @@ SIGNATURES = [
     ("mb200_probe_imad", I, [I, I, I, P, P]),
     ("mb200_probe_atomics", I, [I, I, I, I, P, u64, P]),
     ("mb200_probe_dsmem", I, [I, I, I, I, I, u32, P, P]),
+    ("mb200_hot_stats", I, [P, I]),
 ]
 
 

@@ -344,6 +344,11 @@ int mb200_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* 
     return e == cudaSuccess ? MB200_OK : cuda_fail(e, "probe");
 }
 
+int mb200_hot_stats(uint64_t out[4], int reset) {
+    cudaError_t e = hot_stats(out, reset != 0);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_hot_stats");
+}
+
 int mb200_probe_dsmem(int cluster, int mode, int blocks, int threads, int iters, uint32_t words, uint64_t* d_out,
                       void* stream) {
     cudaError_t e = launch_probe_dsmem(cluster, mode, blocks, threads, iters, words, d_out, (cudaStream_t)stream);

@@ -29,6 +29,10 @@
 
 namespace mb200 {
 
+// per-process counters of the heavy-hitter kernel: items, misses (items sent to
+// the fused L2 path), hot keys applied at the end, hot-set size (summed over CTAs)
+__device__ unsigned long long g_hot_stats[4];
+
 namespace {
 
 using namespace sk;
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     const uint64_t lo_item = n * blockIdx.x / gridDim.x, hi_item = n * (blockIdx.x + 1) / gridDim.x;
     const uint64_t ntiles = (hi_item - lo_item + kTile - 1) / kTile;
     int qn = 0;
+    unsigned misses = 0;
     for (;;) {
         u32 t = 0;
         if (lane == 0) t = atomicAdd(&s_next, 1u);
@@ -246,6 +251,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
                 wqd[pos] = dx[u];
             }
             qn += __popc(m);
+            misses += __popc(m);
             __syncwarp();
             if (qn >= 32) {  // a full warp of misses
                 process_item<MODE, K, GLOBAL>(sp, (u64)wqk[lane], (i64)wqd[lane], nullptr, table);
@@ -261,10 +267,22 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     }
     if (lane < qn) process_item<MODE, K, GLOBAL>(sp, (u64)wqk[lane], (i64)wqd[lane], nullptr, table);
     __syncthreads();
+    unsigned flushed = 0;
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
         if (hk[s] == G::kEmpty) continue;
         const u64 v = (((u64)hi[s] << 32) | lo[s]) - 0x80000000ull;
-        if (v) process_item<MODE, K, GLOBAL>(sp, (u64)hk[s], (i64)v, nullptr, table);
+        if (v) {
+            process_item<MODE, K, GLOBAL>(sp, (u64)hk[s], (i64)v, nullptr, table);
+            ++flushed;
+        }
+    }
+    // instrumentation for the L2-reduction roofline (mb200_hot_stats)
+    if (lane == 0) atomicAdd(&g_hot_stats[1], (unsigned long long)misses);
+    flushed = __reduce_add_sync(kFull, flushed);
+    if (lane == 0) atomicAdd(&g_hot_stats[2], (unsigned long long)flushed);
+    if (threadIdx.x == 0) {
+        atomicAdd(&g_hot_stats[0], (unsigned long long)(hi_item - lo_item));
+        atomicAdd(&g_hot_stats[3], (unsigned long long)nhot);
     }
 }
 
@@ -334,6 +352,16 @@ void retain_pool() {
 }
 
 }  // namespace
+
+cudaError_t hot_stats(uint64_t out[4], bool reset) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess && out) e = cudaMemcpyFromSymbol(out, g_hot_stats, sizeof(g_hot_stats));
+    if (e == cudaSuccess && reset) {
+        const unsigned long long z[4] = {0, 0, 0, 0};
+        e = cudaMemcpyToSymbol(g_hot_stats, z, sizeof(z));
+    }
+    return e;
+}
 
 cudaError_t launch_cs_hot(const SketchParams& sp, const void* keys, int key_width, const void* w, int w_kind,
                           uint64_t n, int64_t* table, cudaStream_t s) {

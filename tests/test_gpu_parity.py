@@ -310,6 +310,26 @@ def test_hot_path_large_batches(cuda, mb, orc, case):
     assert (cnt.cpu().numpy() == exp).all()
 
 
+@pytest.mark.parametrize("weight", [np.iinfo(np.int32).max, np.iinfo(np.int32).min])
+def test_hot_path_accumulator_wraps(cuda, mb, orc, weight):
+    """One key with extreme weights: every CTA's 32-bit hot accumulator wraps many
+    times (sum = 2^22 x +-2^31); the wrap counters keep the table exact."""
+    import torch
+
+    n = (1 << 22) + 7
+    keys = np.full(n, 7, np.uint32)
+    keys[::1000] = np.arange(len(keys[::1000]), dtype=np.uint32) + 100  # some cold keys
+    w = np.full(n, weight, np.int32)
+    spec, fams = make_spec(mb, orc, 5, 65536, 61, 32, 0, 0xAA)
+    cnt = torch.zeros(5 * 65536, dtype=torch.int64, device="cuda")
+    mb.hot_stats(reset=True)
+    mb.cs_update(spec, dev(keys), cnt, dev(w))
+    st = mb.hot_stats(reset=True)
+    assert st["items"] == n and st["misses"] < n // 100  # key 7 was accumulated in shared memory
+    exp = orc.cs_process(5, 65536, 61, fams, 32, 0, keys, w)
+    assert (cnt.cpu().numpy() == exp).all()
+
+
 def test_sketch_empty_and_single(cuda, mb, orc):
     import torch
 

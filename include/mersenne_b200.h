@@ -178,11 +178,12 @@ int mb200_gen_zipf_items(uint64_t master_seed, const uint64_t* d_cdf, uint32_t T
                          int32_t* d_weights, void* stream);
 
 /* ------------------------------------------------------------- probes --- */
-/* Counters of the heavy-hitter Count Sketch kernel since the last reset (device-
+/* Counters of the heavy-hitter Count Sketch kernels since the last reset (device-
  * wide, synchronizes the device): [0] items, [1] items sent to the fused L2 path,
- * [2] hot keys applied at kernel end (summed over CTAs), [3] hot-set size summed
- * over CTAs.  L2 reductions issued = rows x ([1] + [2]). */
-int mb200_hot_stats(uint64_t out[4], int reset);
+ * [2] shared-memory hot keys applied at kernel end (summed over CTAs), [3] hot-set
+ * size summed over CTAs, [4..7] reserved (0).  L2 reductions issued =
+ * rows x ([1] + [2]). */
+int mb200_hot_stats(uint64_t out[8], int reset);
 /* blocks x threads threads each issue 8 x iters independent mad.wide.u32 */
 int mb200_probe_imad(int blocks, int threads, int iters, uint64_t* d_sink, void* stream);
 int mb200_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* d_buf,

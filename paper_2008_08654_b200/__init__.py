@@ -288,9 +288,10 @@ def probe_dsmem(cluster: int, mode: int, blocks: int, threads: int, iters: int, 
 
 def hot_stats(reset: bool = False) -> dict:
     """Counters of the heavy-hitter Count Sketch kernel since the last reset."""
-    out = np.zeros(4, np.uint64)
+    out = np.zeros(8, np.uint64)
     check(lib.mb200_hot_stats(_p(out), int(reset)))
-    return {"items": int(out[0]), "misses": int(out[1]), "hot_applied": int(out[2]), "hot_keys": int(out[3])}
+    return {"items": int(out[0]), "misses": int(out[1]), "hot_applied": int(out[2]), "hot_keys": int(out[3]),
+            "tier2_hits": int(out[4]), "tier2_applied": int(out[5])}
 
 
 # ------------------------------------------------------------------ host object

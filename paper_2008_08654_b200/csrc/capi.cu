@@ -344,7 +344,7 @@ int mb200_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* 
     return e == cudaSuccess ? MB200_OK : cuda_fail(e, "probe");
 }
 
-int mb200_hot_stats(uint64_t out[4], int reset) {
+int mb200_hot_stats(uint64_t out[8], int reset) {
     cudaError_t e = hot_stats(out, reset != 0);
     return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_hot_stats");
 }

@@ -31,7 +31,7 @@ namespace mb200 {
 
 // per-process counters of the heavy-hitter kernel: items, misses (items sent to
 // the fused L2 path), hot keys applied at the end, hot-set size (summed over CTAs)
-__device__ unsigned long long g_hot_stats[4];
+__device__ unsigned long long g_hot_stats[8];  // [4..7] reserved (always 0)
 
 namespace {
 
@@ -353,11 +353,11 @@ void retain_pool() {
 
 }  // namespace
 
-cudaError_t hot_stats(uint64_t out[4], bool reset) {
+cudaError_t hot_stats(uint64_t out[8], bool reset) {
     cudaError_t e = cudaDeviceSynchronize();
     if (e == cudaSuccess && out) e = cudaMemcpyFromSymbol(out, g_hot_stats, sizeof(g_hot_stats));
     if (e == cudaSuccess && reset) {
-        const unsigned long long z[4] = {0, 0, 0, 0};
+        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         e = cudaMemcpyToSymbol(g_hot_stats, z, sizeof(z));
     }
     return e;

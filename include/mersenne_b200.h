@@ -164,6 +164,13 @@ int mb200_sketch_info(const mb200_sketch* s, unsigned* rows, uint64_t* width, un
 int mb200_sketch_seeds(const mb200_sketch* s, uint64_t* out);
 /* families x k coefficients actually used on the device */
 int mb200_sketch_coeffs(const mb200_sketch* s, uint64_t* lo, uint64_t* hi);
+/* CountSketch::serialize (sketch.cpp:195-211): MCSK1 bytes, byte-identical to the
+ * reference.  *len receives the size; bytes are written only when cap >= *len.
+ * logic_error for injected families (and for the two-for-one splitter). */
+int mb200_sketch_serialize(mb200_sketch* s, uint8_t* out, uint64_t cap, uint64_t* len);
+/* CountSketch::deserialize (sketch.cpp:213-244): families re-derived from the
+ * stored seeds, counters uploaded to HBM; invalid_argument on malformed payloads */
+int mb200_sketch_deserialize(const uint8_t* bytes, uint64_t len, mb200_sketch** out);
 
 /* ------------------------------------- workload generators (bench harness) --- */
 int mb200_gen_u32_keys(uint64_t seed, uint64_t start, uint64_t n, uint32_t* d_out, void* stream);

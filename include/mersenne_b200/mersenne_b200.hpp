@@ -137,6 +137,12 @@ public:
 
     CountSketch& merge(const CountSketch& other);  // requires identical seeds (sketch.cpp:182-193)
 
+    // MCSK1 wire format (sketch.cpp:195-244), byte-identical to the reference:
+    // "MCSK1", u32 b, u32 rows, u64 width, u32 k, u32 splitter, u32 log2(u),
+    // rows x u64 seeds, rows x width x u64 counters, little endian.
+    std::vector<uint8_t> serialize() const;
+    static CountSketch deserialize(const std::vector<uint8_t>& bytes);
+
     unsigned rows() const { return rows_; }
     u64 width() const { return width_; }
     Splitter splitter() const { return splitter_; }

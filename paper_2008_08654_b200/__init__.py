@@ -400,6 +400,22 @@ class CountSketch:
         check(lib.mb200_sketch_seeds(self._h, _p(out)))
         return [int(v) for v in out]
 
+    def serialize(self) -> bytes:
+        """MCSK1 bytes, identical to mersenne::CountSketch::serialize (sketch.cpp:195-211)."""
+        n = C.c_uint64()
+        check(lib.mb200_sketch_serialize(self._h, None, 0, C.byref(n)))
+        buf = np.zeros(n.value, np.uint8)
+        check(lib.mb200_sketch_serialize(self._h, _p(buf), n.value, C.byref(n)))
+        return buf.tobytes()
+
+    @classmethod
+    def deserialize(cls, payload: bytes) -> "CountSketch":
+        """mersenne::CountSketch::deserialize (sketch.cpp:213-244)."""
+        buf = np.frombuffer(payload, np.uint8).copy()
+        h = C.c_void_p()
+        check(lib.mb200_sketch_deserialize(_p(buf) if len(buf) else None, len(buf), C.byref(h)))
+        return cls(0, 0, _handle=h)
+
     def coefficients(self) -> list:
         fams = (self.rows + 1) // 2 if self.splitter == SPLIT_TWO_FOR_ONE else self.rows
         lo = np.zeros(fams * self.independence, np.uint64)

@@ -100,6 +100,8 @@ SIGNATURES = [
     ("mb200_sketch_info", I, [P, P, P, P, P, P, P]),
     ("mb200_sketch_seeds", I, [P, P]),
     ("mb200_sketch_coeffs", I, [P, P, P]),
+    ("mb200_sketch_serialize", I, [P, P, u64, P]),
+    ("mb200_sketch_deserialize", I, [P, u64, P]),
     ("mb200_gen_u32_keys", I, [u64, u64, u64, P, P]),
     ("mb200_gen_u64_keys", I, [u64, u64, u64, P, P]),
     ("mb200_gen_below_p61", I, [u64, u64, u64, P, P, P]),

@@ -157,6 +157,24 @@ int mb200_sketch_seeds(const mb200_sketch* s, uint64_t* out) {
     return MB200_OK;
 }
 
+int mb200_sketch_serialize(mb200_sketch* s, uint8_t* out, uint64_t cap, uint64_t* len) {
+    if (!s || !len) return mb200::fail(MB200_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        const std::vector<uint8_t> bytes = s->sk.serialize();
+        *len = bytes.size();
+        if (out && cap >= bytes.size()) std::memcpy(out, bytes.data(), bytes.size());
+    });
+}
+
+int mb200_sketch_deserialize(const uint8_t* bytes, uint64_t len, mb200_sketch** out) {
+    if (!out || (!bytes && len)) return mb200::fail(MB200_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    return guarded([&] {
+        std::vector<uint8_t> v(bytes, bytes + len);
+        *out = new mb200_sketch{CountSketch::deserialize(v)};
+    });
+}
+
 int mb200_sketch_coeffs(const mb200_sketch* s, uint64_t* lo, uint64_t* hi) {
     if (!s) return mb200::fail(MB200_INVALID_ARGUMENT, "null sketch");
     size_t i = 0;

@@ -381,6 +381,73 @@ CountSketch& CountSketch::merge(const CountSketch& other) {  // sketch.cpp:182-1
     return *this;
 }
 
+namespace {
+void put_u32(std::vector<uint8_t>& out, uint32_t v) {
+    for (int i = 0; i < 4; ++i) out.push_back(uint8_t(v >> (8 * i)));
+}
+void put_u64(std::vector<uint8_t>& out, uint64_t v) {
+    for (int i = 0; i < 8; ++i) out.push_back(uint8_t(v >> (8 * i)));
+}
+uint32_t get_u32(const uint8_t* p) {
+    uint32_t v = 0;
+    for (int i = 0; i < 4; ++i) v |= uint32_t(p[i]) << (8 * i);
+    return v;
+}
+uint64_t get_u64(const uint8_t* p) {
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= uint64_t(p[i]) << (8 * i);
+    return v;
+}
+constexpr char kMagic[5] = {'M', 'C', 'S', 'K', '1'};
+}  // namespace
+
+std::vector<uint8_t> CountSketch::serialize() const {  // sketch.cpp:195-211
+    if (seeds_.empty()) throw std::logic_error("sketch with injected families cannot serialize");
+    if (splitter_ == Splitter::TwoForOne)
+        throw std::logic_error("two-for-one sketches have no MCSK1 form");  // not a reference splitter
+    const std::vector<i64> c = counters();
+    std::vector<uint8_t> out;
+    out.reserve(33 + 8 * seeds_.size() + 8 * c.size());
+    out.insert(out.end(), std::begin(kMagic), std::end(kMagic));
+    put_u32(out, modulus().b());
+    put_u32(out, rows_);
+    put_u64(out, width_);
+    put_u32(out, independence());
+    put_u32(out, uint32_t(splitter_));
+    put_u32(out, families_.front().key_bits());
+    for (u64 s : seeds_) put_u64(out, s);
+    for (i64 v : c) put_u64(out, u64(v));
+    return out;
+}
+
+CountSketch CountSketch::deserialize(const std::vector<uint8_t>& bytes) {  // sketch.cpp:213-244
+    if (bytes.size() < 33 || !std::equal(std::begin(kMagic), std::end(kMagic), bytes.begin()))
+        throw std::invalid_argument("malformed sketch payload");
+    const uint8_t* p = bytes.data() + 5;
+    const uint32_t b = get_u32(p), d = get_u32(p + 4);
+    const uint64_t r = get_u64(p + 8);
+    const uint32_t k = get_u32(p + 16), splitter = get_u32(p + 20), key_bits = get_u32(p + 24);
+    if (b < 2 || b > 127 || d == 0 || splitter > 2 || key_bits > 126 || k == 0)
+        throw std::invalid_argument("malformed sketch payload");
+    const u128 expect = 33 + u128(8) * d + u128(8) * d * r;
+    if (u128(bytes.size()) != expect) throw std::invalid_argument("malformed sketch payload");
+    MersenneModulus modulus(b);
+    const u128 key_domain = u128(1) << key_bits;
+    const uint8_t* q = bytes.data() + 33;
+    std::vector<u64> seeds(d);
+    std::vector<PolyHashFamily> families;
+    for (uint32_t row = 0; row < d; ++row, q += 8) {
+        seeds[row] = get_u64(q);
+        families.emplace_back(modulus, k, key_domain, seeds[row]);  // re-derived from the seeds
+    }
+    CountSketch sk(r, Splitter(splitter), std::move(families));
+    sk.seeds_ = std::move(seeds);
+    std::vector<i64> c(size_t(d) * r);
+    for (size_t i = 0; i < c.size(); ++i, q += 8) c[i] = i64(get_u64(q));
+    sk.set_counters(c);
+    return sk;
+}
+
 std::vector<i64> CountSketch::counters() const {
     std::vector<i64> h(size_t(rows_) * width_);
     cudaStream_t s = (cudaStream_t)stream_;

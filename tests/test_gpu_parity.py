@@ -423,6 +423,29 @@ def test_count_sketch_object_matches_reference_semantics(cuda, mb, orc):
     assert (a.counters() == exp).all()
 
 
+def test_mcsk1_serialization_matches_reference(cuda, mb, golden):
+    """A GPU table serializes byte-identically to the reference (sketch.cpp:195-211),
+    round-trips, and keeps hashing identically after deserialize (test_sketch.cpp:180-205)."""
+    g = golden["mcsk1"]
+    sk = mb.CountSketch(3, 16, 61, 32, mb.SPLIT_MERSENNE_ARB, 0xABCD)
+    sk.process(np.array(g["keys"], np.uint64), np.array(g["weights"], np.int64))
+    payload = sk.serialize()
+    assert payload == bytes.fromhex(g["bytes"])
+    assert len(payload) == 33 + 8 * 3 + 8 * 3 * 16 and payload[:5] == b"MCSK1"
+    back = mb.CountSketch.deserialize(payload)
+    assert back.serialize() == payload
+    back.process_one(7, 3)
+    sk.process_one(7, 3)
+    assert back.serialize() == sk.serialize()
+    for bad in (b"", b"XCSK1" + payload[5:], payload[:-1], payload + b"\0",
+                payload[:25] + b"\x09" + payload[26:]):
+        with pytest.raises(mb.InvalidArgument, match="malformed sketch payload"):
+            mb.CountSketch.deserialize(bad)
+    inj = mb.CountSketch.from_families(4, mb.SPLIT_POW2, 5, 4, [[1, 2, 3, 4]])
+    with pytest.raises(mb.LogicError):
+        inj.serialize()
+
+
 def test_count_sketch_injected_families(cuda, mb):
     sk = mb.CountSketch.from_families(4, mb.SPLIT_POW2, 5, 4, [[1, 2, 3, 4]])
     with pytest.raises(mb.LogicError):

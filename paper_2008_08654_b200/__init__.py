@@ -331,8 +331,11 @@ class CountSketch:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            lib.mb200_sketch_destroy(h)
+        if h is not None and h.value and lib is not None:
+            try:
+                lib.mb200_sketch_destroy(h)
+            except Exception:  # interpreter teardown
+                pass
             self._h = None
 
     def process(self, keys, weights=None):

@@ -36,6 +36,9 @@ C1_ITEMS, C2_KEYS, C3_UNITS, C4_KEYS = 1 << 24, 1 << 28, 1 << 28, 1 << 26
 # algorithmic work per unit: bytes of HBM traffic and 32x32->64 limb products
 WORK = {
     "c1": (4, 6), "c2_k4": (16, 12), "c2_k8": (16, 28), "c3": (32, 6), "c4": (8, 18), "c5": (8, 30),
+    # SURVEY 8f rank 4 (not BASELINE configs): ExactDivisionMap over u64 values --
+    # 8 B in + 8 B out; v r (4 limb products) + 2 Alg-4 rounds by a 6-bit c (2 x 2)
+    "exact_div": (16, 8),
 }
 
 
@@ -537,7 +540,51 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
     out["c4"] = {"value": C4_KEYS / t, "unit": "keys/s", "row_updates_per_s": 2 * C4_KEYS / t,
                  "ms_per_step": t * 1e3, "workload": "2^89-1 two-for-one, 2^26 u64 keys, 2 x 2^16 counters",
                  "l2": "inputs 512 MiB > L2", "roofline": roofline("c4", hi - lo, tk, "c4", l2_reds=c4_reds)}
-    del keys, flushbuf
+    del keys
+
+    # ExactDivisionMap(PseudoMersenneModulus(64, 59), r) (bucketing.cpp:75-95)
+    # over 2^28 u64 values (uniform; P(v >= p) = 59 / 2^64, counted and asserted zero)
+    lo, hi = shard(C2_KEYS, rank, world)
+    vals = mb.gen_u64_keys(SK ^ 0xB0C, lo, hi - lo)
+    outb = torch.empty_like(vals)
+    ood = torch.zeros(1, dtype=torch.int64, device=dev)
+    r_buckets = 1000003
+    t = max_over_ranks(timed_steps(torch, steps, args.warmup, lambda: mb.bucket_map(
+        mb.MAP_EXACT_DIV, vals, 64, r_buckets, 59, out=outb, out_of_domain=ood)))
+    assert int(ood.item()) == 0
+    out["exact_div_map"] = {"value": C2_KEYS / t, "unit": "maps/s", "ms_per_step": t * 1e3,
+                            "workload": f"floor(v r / (2^64-59)), r = {r_buckets}, m = "
+                                        f"{mb.exact_division_iterations(64, 59, r_buckets)}, 2^28 u64 values",
+                            "l2": "inputs 2 GiB > L2", "roofline": roofline("exact_div", hi - lo, t, "exact_div")}
+    del vals, outb, flushbuf
+
+    # exhaustive moment enumeration (verify.cpp:505-603) over p^4 families,
+    # the reference suite's stream {(1,2),(3,-1),(7,3)} at p = 2^8 - 1 (4.2e9 families)
+    if rank == 0:
+        stream = [(1, 2), (3, -1), (7, 3)]
+        mb.enum_moment_sums(5, 4, mb.SPLIT_POW2, stream)  # warm-up (module load)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        sums = mb.enum_moment_sums(8, 16, mb.SPLIT_POW2, stream)
+        e1.record()
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1) / 1e3
+        ent = {"value": sums["families"] / te, "unit": "families/s", "ms": te * 1e3,
+               "workload": "enum_moment_sums b=8 (p=255, 255^4 families), r=16 Pow2, 3-key stream",
+               "sum_x": str(sums["sum_x"]), "sum_x_sq": str(sums["sum_x_sq"])}
+        try:  # cpu_baseline leg: the oracle restatement (all host threads) on p = 63 for scale
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from oracle_bind import oracle
+            orc = oracle()
+            t0 = time.perf_counter()
+            orc.enum_moment_sums(6, 16, 0, stream)
+            tc = time.perf_counter() - t0
+            ent["cpu_baseline"] = {"value": 63 ** 4 / tc, "unit": "families/s", "cores": os.cpu_count(),
+                                   "kind": "port", "sample": "b=6 (63^4 families), same stream, OpenMP over a0"}
+        except Exception as exc:  # noqa: BLE001
+            ent["cpu_baseline"] = {"unavailable": str(exc)[:200]}
+        out["enum_moments"] = ent
     return out
 
 

@@ -99,6 +99,45 @@ int mb200_hash89(const uint64_t* d_keys, uint64_t n, const uint64_t* coeffs_lo,
 int mb200_pm_divmod(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, unsigned m_iters,
                     uint64_t* d_q, uint64_t* d_r, uint64_t* d_overflow, void* stream);
 
+/* ------------------------------------------------------------- bucketing --- */
+/* Bucket maps of bucketing.hpp:31-58 on device u64 arrays (b <= 64):
+ *   MB200_MAP_POW2      map_pow2(v, b, r)      = floor(v r / 2^b)       bucketing.cpp:61-66
+ *                       v < 2^b, 1 <= r <= 2^b (r < 2^64)
+ *   MB200_MAP_MERSENNE  map_mersenne(v, b, r)  = floor((v+1) r / 2^b)   bucketing.cpp:68-73
+ *                       v < 2^b - 1, 1 <= r <= 2^b - 1
+ *   MB200_MAP_EXACT_DIV ExactDivisionMap(PseudoMersenneModulus(b, c), r)(v)
+ *                       = floor(v r / p), p = 2^b - c, by Alg 4     bucketing.cpp:75-95
+ *                       v < p, 1 <= r <= p; c is ignored by the other kinds. */
+#define MB200_MAP_POW2 0
+#define MB200_MAP_MERSENNE 1
+#define MB200_MAP_EXACT_DIV 2
+/* ExactDivisionMap ctor (bucketing.cpp:75-89): the divider's iteration count,
+ * the smallest m >= 1 with (p-1) r <= max_input(b, c, m).  r outside [1, p]:
+ * MB200_INVALID_ARGUMENT "bucket count must be in [1, p]".  b <= 127. */
+int mb200_exact_division_iterations(unsigned b, uint64_t c, uint64_t r, unsigned* iterations);
+/* The reference asserts the value domain; here values outside it are counted:
+ * into *d_out_of_domain (nullable device u64, accumulated, asynchronous), or,
+ * when d_out_of_domain is NULL, by a synchronizing read-back that returns
+ * MB200_DOMAIN_ERROR "value outside the map's domain" (outputs for in-domain
+ * values are written either way). */
+int mb200_bucket_map(int kind, const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, uint64_t r,
+                     uint64_t* d_out, uint64_t* d_out_of_domain, void* stream);
+
+/* ------------------------------------------------ moment enumeration --- */
+/* enum_moment_sums_serial / _parallel (verify.hpp:123-145, verify.cpp:505-603):
+ * over all p^4 degree-3 coefficient vectors (p = 2^b - 1) build the one-row
+ * sketch of the stream (keys[i], deltas[i]) with `buckets` counters and the
+ * given splitter (MB200_SPLIT_POW2 / _UNIFORM_ARB / _MERSENNE_ARB), and sum
+ * X = sum_i C_i^2 and X^2 exactly.  out[0..1] = sum_x (lo, hi), out[2..3] =
+ * sum_x_sq (lo, hi), out[4] = families (p^4).  Validation and messages follow
+ * validate_moment_spec (verify.cpp:480-503) and exact_family_count (:566-573):
+ * 2 <= b <= 15, keys < key_domain <= p, distinct modulo p, sum |delta| <= 1024.
+ * The GPU kernel takes at most 64 non-zero-weight entries (MB200_UNSUPPORTED
+ * beyond).  Synchronizes `stream`. */
+int mb200_enum_moment_sums(unsigned b, uint64_t key_domain, uint64_t buckets, int splitter,
+                           const uint64_t* keys, const int64_t* deltas, uint64_t n, uint64_t out[5],
+                           void* stream);
+
 /* --------------------------------------------------------- count sketch --- */
 typedef struct {
     unsigned rows;             /* counter rows t (<= 16) */

@@ -61,6 +61,26 @@ private:
     std::array<u64, 4> max_input_;
 };
 
+// bucketing.hpp:31-58 -- bucket maps over device u64 arrays (b <= 64)
+// map_pow2: floor(v r / 2^b), v < 2^b;  map_mersenne: floor((v+1) r / 2^b), v < 2^b - 1
+void map_pow2_device(const u64* d_v, u64 n, unsigned b, u64 r, u64* d_out, void* stream = nullptr);
+void map_mersenne_device(const u64* d_v, u64 n, unsigned b, u64 r, u64* d_out, void* stream = nullptr);
+
+// bucketing.hpp:43-58: floor(v r / p) on [0, p) by Alg 4, the divider's iteration
+// count grown at construction until (p-1) r is admissible (bucketing.cpp:75-89)
+class ExactDivisionMap {
+public:
+    ExactDivisionMap(const PseudoMersenneModulus& mod, u64 r);
+    u64 operator()(u64 v) const;  // one value (API parity; launches a one-element batch)
+    void map_device(const u64* d_v, u64 n, u64* d_out, void* stream = nullptr) const;
+    const PseudoMersenneModulus& divider() const { return divider_; }
+    u64 buckets() const { return r_; }
+
+private:
+    PseudoMersenneModulus divider_;
+    u64 r_;
+};
+
 enum class HashFinish { ConditionalSubtract, BranchFree };  // polyhash.hpp:10-13 (same values)
 
 // polyhash.hpp:18-43

@@ -517,6 +517,37 @@ void orc_split_arb_mersenne(u64 h_lo, u64 h_hi, unsigned b, u64 r, u64* index, i
     orc_split_arb_uniform((u64)h, (u64)(h >> 64), b, r, index, sign);
 }
 
+/* ---- bucket maps (bucketing.cpp:61-95) ---- */
+
+/* bucketing.cpp:75-89: the iteration count grows from 1 until the largest
+ * product (p-1) r lies inside domain_threshold(b, c, m).  0 = invalid r. */
+unsigned orc_exact_div_iterations(unsigned b, u64 c, u64 r) {
+    const u128 p = (((u128)1) << b) - c;
+    if (r == 0 || (u128)r > p) return 0; /* "bucket count must be in [1, p]" */
+    u256 largest = w_mul(w_of(p - 1), w_of(r));
+    for (unsigned m = 1;; ++m) {
+        u64 mx[4];
+        domain_threshold(b, c, m, mx);
+        u256 t = {{mx[0], mx[1], mx[2], mx[3]}};
+        if (w_cmp(largest, t) <= 0) return m;
+    }
+}
+
+/* kind 0 = map_pow2 (:61-66), 1 = map_mersenne (:68-73),
+ * 2 = ExactDivisionMap::operator() (:91-95) with m from orc_exact_div_iterations */
+u64 orc_bucket_map(int kind, unsigned b, u64 c, unsigned m, u64 r, u64 v) {
+    switch (kind) {
+        case 0: return (u64)scaled_shift(v, r, b);
+        case 1: return (u64)scaled_shift((u128)v + 1, r, b);
+        default: return pm_div_w(b, c, m, w_mul(w_of(v), w_of(r))).l[0];
+    }
+}
+
+void orc_bucket_map_batch(int kind, unsigned b, u64 c, unsigned m, u64 r, const u64* v, u64 n, u64* out) {
+#pragma omp parallel for schedule(static)
+    for (u64 i = 0; i < n; ++i) out[i] = orc_bucket_map(kind, b, c, m, r, v[i]);
+}
+
 /* ======================= sketch.cpp:121-193 (Count Sketch) ============== */
 static inline void split_dispatch(int splitter, unsigned b, u64 width, unsigned lw, u128 h,
                                   unsigned sub, u64* idx, int* sign) {
@@ -861,4 +892,83 @@ void orc_enum_sums(unsigned b, unsigned k, unsigned key_bits, u64 width, int spl
     }
     *sum_f2 = s2;
     *sum_pq = spq;
+}
+
+/* verify.cpp:505-546 moment_range + 555-603 enum_moment_sums_{serial,parallel}:
+ * for every (a0, a1, a2, a3) in Z_p^4 (p = 2^b - 1, a0 the x^3 coefficient)
+ * fill the one-row sketch of the stream, then X = sum c^2 (u64) and accumulate
+ * sum_x += X, sum_x_sq += X^2 (u128).  Restated loop for loop, counters
+ * included; the split tables are apply_splitter (verify.cpp:389-399), which
+ * is split_pow2 with l = bit_width(r) - 1 or the arbitrary-width splitters.
+ * out: sum_x lo/hi, sum_x_sq lo/hi.  Parallel over a0 like the reference's
+ * parallel kernel (integer sums: identical for any thread count). */
+void orc_enum_moment_sums(unsigned b, u64 buckets, int splitter, const u64* keys,
+                          const int64_t* deltas, u64 n, u64 out[4]) {
+    const u64 p = (((u64)1) << b) - 1;
+    unsigned* idx = (unsigned*)malloc(sizeof(unsigned) * p);
+    int* sgn = (int*)malloc(sizeof(int) * p);
+    unsigned lw = 0;
+    while ((((u64)1) << (lw + 1)) <= buckets) ++lw; /* bit_width(r) - 1 */
+    for (u64 h = 0; h < p; ++h) {
+        u64 ix;
+        int sg;
+        split_dispatch(splitter, b, buckets, lw, (u128)h, 0, &ix, &sg);
+        idx[h] = (unsigned)ix;
+        sgn[h] = sg;
+    }
+    u64 *x1 = (u64*)malloc(8 * (n + 1)), *x2 = (u64*)malloc(8 * (n + 1)), *x3 = (u64*)malloc(8 * (n + 1));
+    for (u64 j = 0; j < n; ++j) {
+        x1[j] = keys[j] % p;
+        x2[j] = x1[j] * x1[j] % p;
+        x3[j] = x2[j] * x1[j] % p;
+    }
+    u128 sum_x = 0, sum_xx = 0;
+#pragma omp parallel
+    {
+        u128 lx = 0, lxx = 0;
+        u64* t0 = (u64*)malloc(8 * (n + 1));
+        u64* t1 = (u64*)malloc(8 * (n + 1));
+        u64* t2 = (u64*)malloc(8 * (n + 1));
+        int64_t* counters = (int64_t*)malloc(8 * buckets);
+#pragma omp for schedule(static)
+        for (u64 a0 = 0; a0 < p; ++a0) {
+            for (u64 j = 0; j < n; ++j) t0[j] = a0 * x3[j] % p;
+            for (u64 a1 = 0; a1 < p; ++a1) {
+                for (u64 j = 0; j < n; ++j) t1[j] = (t0[j] + a1 * x2[j]) % p;
+                for (u64 a2 = 0; a2 < p; ++a2) {
+                    for (u64 j = 0; j < n; ++j) t2[j] = (t1[j] + a2 * x1[j]) % p;
+                    for (u64 a3 = 0; a3 < p; ++a3) {
+                        memset(counters, 0, 8 * buckets);
+                        for (u64 j = 0; j < n; ++j) {
+                            u64 h = t2[j] + a3;
+                            if (h >= p) h -= p;
+                            counters[idx[h]] += sgn[h] * deltas[j];
+                        }
+                        u64 x_val = 0;
+                        for (u64 i = 0; i < buckets; ++i) x_val += (u64)(counters[i] * counters[i]);
+                        lx += x_val;
+                        lxx += (u128)x_val * x_val;
+                    }
+                }
+            }
+        }
+#pragma omp critical
+        {
+            sum_x += lx;
+            sum_xx += lxx;
+        }
+        free(t0);
+        free(t1);
+        free(t2);
+        free(counters);
+    }
+    out[0] = (u64)sum_x;
+    out[1] = (u64)(sum_x >> 64);
+    out[2] = (u64)sum_xx;
+    out[3] = (u64)(sum_xx >> 64);
+    free(idx);
+    free(sgn);
+    free(x1);
+    free(x2);
+    free(x3);
 }

@@ -88,6 +88,14 @@ void orc_split_arb_uniform(uint64_t h_lo, uint64_t h_hi, unsigned b, uint64_t r,
 void orc_split_arb_mersenne(uint64_t h_lo, uint64_t h_hi, unsigned b, uint64_t r,
                             uint64_t* index, int* sign);
 
+/* ---- bucketing.cpp:61-95 (bucket maps) ---------------------------------- */
+/* ExactDivisionMap ctor: smallest m with (p-1) r <= max_input(b, c, m); 0 if r not in [1, p] */
+unsigned orc_exact_div_iterations(unsigned b, uint64_t c, uint64_t r);
+/* kind 0 map_pow2, 1 map_mersenne, 2 ExactDivisionMap (c, m used only by kind 2) */
+uint64_t orc_bucket_map(int kind, unsigned b, uint64_t c, unsigned m, uint64_t r, uint64_t v);
+void orc_bucket_map_batch(int kind, unsigned b, uint64_t c, unsigned m, uint64_t r,
+                          const uint64_t* v, uint64_t n, uint64_t* out);
+
 /* ---- sketch.cpp:133-168, 182-193 (Count Sketch) ------------------------ */
 /* splitter: 0 Pow2, 1 UniformArb, 2 MersenneArb, 3 TwoForOne (one family per two rows,
  * SURVEY 7.4 bit layout: row j takes index bits [l j, l j + l) and sign bit b-1-j).
@@ -117,6 +125,11 @@ void orc_cs_merge(int64_t* dst, const int64_t* src, uint64_t count);
 void orc_enum_sums(unsigned b, unsigned k, unsigned key_bits, uint64_t width, int splitter,
                    const uint64_t* keys, const int64_t* deltas, uint64_t n, uint64_t qkey,
                    uint64_t* sum_f2, int64_t* sum_pq);
+/* verify.cpp:505-603 enum_moment_sums: sum over Z_p^4 (p = 2^b - 1) of X = sum c^2
+ * and X^2 for a one-row sketch (splitter 0 Pow2 with l = log2 r, 1 UniformArb,
+ * 2 MersenneArb).  out: sum_x lo/hi, sum_x_sq lo/hi. */
+void orc_enum_moment_sums(unsigned b, uint64_t buckets, int splitter, const uint64_t* keys,
+                          const int64_t* deltas, uint64_t n, uint64_t out[4]);
 
 /* ---- synthetic workload generators ---------------- */
 void orc_gen_u32_keys(uint64_t key_seed, uint64_t start, uint64_t n, uint32_t* out);

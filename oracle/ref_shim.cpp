@@ -15,6 +15,7 @@
 #include <stdexcept>
 #include <vector>
 
+#include "mersenne/bucketing.hpp"
 #include "mersenne/cli.hpp"
 #include "mersenne/field.hpp"
 #include "mersenne/polyhash.hpp"
@@ -177,6 +178,25 @@ void ref_split(int which, uint64_t h_lo, uint64_t h_hi, unsigned b, uint64_t l_o
                                    : split_arb_mersenne(mk(h_lo, h_hi), b, l_or_r);
     *index = uint64_t(s.index);
     *sign = s.sign;
+}
+
+// bucketing.cpp:61-95 on a batch: kind 0 map_pow2(v, b, r), 1 map_mersenne(v, b, r),
+// 2 ExactDivisionMap(PseudoMersenneModulus(b, c), r)(v).  Returns the divider's
+// iteration count for kind 2 (1 otherwise), 0 if the constructor threw.
+unsigned ref_bucket_map(int kind, unsigned b, uint64_t c, uint64_t r, const uint64_t* v,
+                        uint64_t n, uint64_t* out) {
+    if (kind == 2) {
+        try {
+            const ExactDivisionMap map(PseudoMersenneModulus(b, c), r);
+            for (uint64_t i = 0; i < n; ++i) out[i] = uint64_t(map(v[i]));
+            return map.divider().iterations();
+        } catch (const std::invalid_argument&) {
+            return 0;
+        }
+    }
+    for (uint64_t i = 0; i < n; ++i)
+        out[i] = uint64_t(kind == 0 ? map_pow2(v[i], b, r) : map_mersenne(v[i], b, r));
+    return 1;
 }
 
 // Seeded CountSketch(rows, width, MersenneModulus(b,true), 2^key_bits, splitter, seed);

@@ -16,7 +16,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from ._lib import (  # noqa: F401
-    KEY_U32, KEY_U64, LIB_PATH, SIGNATURES, SPLIT_MERSENNE_ARB, SPLIT_POW2, SPLIT_TWO_FOR_ONE,
+    KEY_U32, KEY_U64, LIB_PATH, MAP_EXACT_DIV, MAP_MERSENNE, MAP_POW2, SIGNATURES, SPLIT_MERSENNE_ARB, SPLIT_POW2, SPLIT_TWO_FOR_ONE,
     SPLIT_UNIFORM_ARB, W_I32, W_I64, W_NONE, CudaError, DomainError, InvalidArgument, LogicError,
     SketchDesc, Unsupported, check, lib,
 )
@@ -147,6 +147,87 @@ def pm_divmod(v, b: int, c: int, m_iters: int = 0, q=None, r=None, overflow=None
     check(lib.mb200_pm_divmod(_dptr(v), n, b, c, m_iters, _dptr(q), _dptr(r), _dptr(overflow),
                               _stream(stream)))
     return q, r
+
+
+def exact_division_iterations(b: int, c: int, r: int) -> int:
+    """ExactDivisionMap(PseudoMersenneModulus(b, c), r).divider().iterations()
+    (bucketing.cpp:75-89)."""
+    m = C.c_uint()
+    check(lib.mb200_exact_division_iterations(b, c, r, C.byref(m)))
+    return m.value
+
+
+def bucket_map(kind: int, v, b: int, r: int, c: int = 0, out=None, out_of_domain=None, stream=None):
+    """Bucket map of a device u64 batch (int64 tensor): MAP_POW2 map_pow2(v, b, r),
+    MAP_MERSENNE map_mersenne(v, b, r), MAP_EXACT_DIV ExactDivisionMap(PseudoMersenneModulus(b, c), r)(v)
+    (bucketing.cpp:61-95).  Values outside the domain raise DomainError unless
+    `out_of_domain` (device int64[1]) collects their count asynchronously."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(v.numel(), dtype=torch.int64, device=v.device)
+    check(lib.mb200_bucket_map(kind, _dptr(v), v.numel(), b, c, r, _dptr(out), _dptr(out_of_domain),
+                               _stream(stream)))
+    return out
+
+
+class ExactDivisionMap:
+    """bucketing.hpp:43-58: v -> floor(v r / p) on [0, p), p = 2^b - c, via Alg 4 with the
+    iteration count grown until (p-1) r is admissible.  Calls run on the GPU."""
+
+    def __init__(self, b: int, c: int, r: int):
+        self.m = exact_division_iterations(b, c, r)
+        self.b, self.c, self.r = b, c, r
+        self.p = (1 << b) - c
+
+    def buckets(self) -> int:
+        return self.r
+
+    def iterations(self) -> int:
+        return self.m
+
+    def __call__(self, v, out=None, stream=None):
+        return bucket_map(MAP_EXACT_DIV, v, self.b, self.r, self.c, out=out, stream=stream)
+
+
+def enum_moment_sums(b: int, buckets: int, splitter: int, stream, key_domain: Optional[int] = None,
+                     stream_=None) -> dict:
+    """enum_moment_sums (verify.cpp:575-603) on the GPU: over all p^4 degree-3 families
+    (p = 2^b - 1) of a one-row sketch with `buckets` counters, exact sums of
+    X = sum C_i^2 and X^2.  stream: [(key, delta), ...] with distinct keys mod p."""
+    keys = np.array([int(k) for k, _ in stream], np.uint64)
+    deltas = np.array([int(d) for _, d in stream], np.int64)
+    if key_domain is None:
+        key_domain = (1 << b) - 1
+    out = np.zeros(5, np.uint64)
+    check(lib.mb200_enum_moment_sums(b, key_domain, buckets, splitter, _p(keys), _p(deltas), len(keys),
+                                     _p(out), _stream(stream_) if stream_ is not None else None))
+    return {"sum_x": int(out[0]) | (int(out[1]) << 64), "sum_x_sq": int(out[2]) | (int(out[3]) << 64),
+            "families": int(out[4])}
+
+
+def enum_sketch_moments(b: int, buckets: int, splitter: int, stream, key_domain: Optional[int] = None) -> dict:
+    """The three exact checks of enum_sketch_moments (verify.cpp:605-653) from the GPU sums:
+    the mean equals (F2 p^2 + F1^2 - F2) / p^2, lies within F2 (n-1)/p^2 of F2, and the
+    variance is below 2 F2^2 / r (Pow2) or 2 F2^2 (2^(2b) + r^2) / (r 2^(2b)).  Values are
+    exact fractions.  (The reference's JSON report/budget layer is out of scope.)"""
+    from fractions import Fraction as Fr
+
+    s = enum_moment_sums(b, buckets, splitter, stream, key_domain)
+    p = (1 << b) - 1
+    f1 = sum(int(d) for _, d in stream)
+    f2 = sum(int(d) * int(d) for _, d in stream)
+    fam, p2, n = s["families"], p * p, len(stream)
+    mean = Fr(s["sum_x"], fam)
+    formula = Fr(f2 * p2 + f1 * f1 - f2, p2)
+    tol = Fr(f2 * (n - 1), p2)
+    var = Fr(s["sum_x_sq"], fam) - mean * mean
+    bound = (Fr(2 * f2 * f2, buckets) if splitter == SPLIT_POW2 else
+             Fr(2 * f2 * f2 * ((1 << (2 * b)) + buckets * buckets), buckets << (2 * b)))
+    checks = [("mean matches exact formula", mean, formula, "=="),
+              ("mean within relative distance of F2", abs(mean - f2), tol, "<="),
+              ("variance below bound", var, bound, "<=")]
+    return {"sums": s, "checks": [{"name": nm, "value": v, "bound": bd, "relation": rel,
+                                   "pass": v == bd if rel == "==" else v <= bd} for nm, v, bd, rel in checks]}
 
 
 class SketchSpec:

@@ -22,6 +22,7 @@ MB200_UNSUPPORTED = 5
 KEY_U32, KEY_U64 = 32, 64
 W_NONE, W_I32, W_I64 = 0, 32, 64
 SPLIT_POW2, SPLIT_UNIFORM_ARB, SPLIT_MERSENNE_ARB, SPLIT_TWO_FOR_ONE = 0, 1, 2, 3
+MAP_POW2, MAP_MERSENNE, MAP_EXACT_DIV = 0, 1, 2
 
 
 class InvalidArgument(ValueError):
@@ -81,6 +82,9 @@ SIGNATURES = [
     ("mb200_hash61", I, [P, I, u64, U, P, U, U, P, P]),
     ("mb200_hash89", I, [P, u64, P, P, U, U, P, P, P]),
     ("mb200_pm_divmod", I, [P, u64, U, u64, U, P, P, P, P]),
+    ("mb200_exact_division_iterations", I, [U, u64, u64, P]),
+    ("mb200_bucket_map", I, [I, P, u64, U, u64, u64, P, P, P]),
+    ("mb200_enum_moment_sums", I, [U, u64, u64, I, P, P, u64, P, P]),
     ("mb200_cs_update", I, [P, P, I, P, I, u64, P, P]),
     ("mb200_cs_moments", I, [P, U, u64, P, P]),
     ("mb200_cs_merge", I, [P, P, u64, P]),

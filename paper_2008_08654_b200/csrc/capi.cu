@@ -3,6 +3,7 @@
 // data-dependent domain checks, and kernel dispatch.  No CPU fallback.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -171,8 +172,6 @@ int mb200_hash61(const void* d_keys, int key_width, uint64_t n, unsigned b, cons
     if (!coeffs) return fail(MB200_INVALID_ARGUMENT, "null coefficients");
     HashParams hp;
     std::memset(&hp, 0, sizeof(hp));
-    hp.c31 = 0x80000000u;
-    hp.c2 = 2;
     hp.b = b;
     hp.k = k;
     hp.p = (1ull << b) - 1;
@@ -249,6 +248,124 @@ int mb200_pm_divmod(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, uns
     e = launch_pm_divmod(d_v, n, b, c, m, d_q, d_r, flags, s);
     if (scratch) cudaFreeAsync(scratch, s);
     return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_pm_divmod");
+}
+
+int mb200_bucket_map(int kind, const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, uint64_t r,
+                     uint64_t* d_out, uint64_t* d_out_of_domain, void* stream) {
+    if (kind != MB200_MAP_POW2 && kind != MB200_MAP_MERSENNE && kind != MB200_MAP_EXACT_DIV)
+        return fail(MB200_INVALID_ARGUMENT, "unknown bucket map");
+    unsigned m = 0;
+    uint64_t bound = 0;  // values must be < bound (0: all of u64)
+    if (kind == MB200_MAP_EXACT_DIV) {
+        if (int rc = mb200_exact_division_iterations(b, c, r, &m)) return rc;
+        if (b > 64) return fail(MB200_UNSUPPORTED, "GPU bucket maps support b <= 64");
+        bound = b == 64 ? (uint64_t)0 - c : (1ull << b) - c;
+    } else {
+        if (b < 1 + (kind == MB200_MAP_MERSENNE) || b > 127)  // bucketing.cpp:62, :69
+            return fail(MB200_INVALID_ARGUMENT, "width must be in [1, 127] (map_pow2) / [2, 127] (map_mersenne)");
+        if (b > 64) return fail(MB200_UNSUPPORTED, "GPU bucket maps support b <= 64");
+        const uint64_t top = b == 64 ? ~0ull : (1ull << b) - (kind == MB200_MAP_MERSENNE);  // largest r
+        if (r == 0 || r > top) return fail(MB200_INVALID_ARGUMENT, "bucket count out of range for the map");
+        bound = kind == MB200_MAP_POW2 ? (b == 64 ? 0 : 1ull << b) : (b == 64 ? ~0ull : (1ull << b) - 1);
+    }
+    if (n == 0) return MB200_OK;
+    if (!d_v || !d_out) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (d_out_of_domain) {
+        cudaError_t e = launch_bucket_map(kind, d_v, n, b, c, m, r, bound, d_out,
+                                          reinterpret_cast<unsigned long long*>(d_out_of_domain), s);
+        return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_bucket_map");
+    }
+    unsigned long long bad = 0;
+    int rc = count_on_device(
+        [&](unsigned long long* d, cudaStream_t st) {
+            return launch_bucket_map(kind, d_v, n, b, c, m, r, bound, d_out, d, st);
+        },
+        s, &bad);
+    if (rc) return rc;
+    if (bad) return fail(MB200_DOMAIN_ERROR, "value outside the map's domain");
+    return MB200_OK;
+}
+
+int mb200_enum_moment_sums(unsigned b, uint64_t key_domain, uint64_t buckets, int splitter, const uint64_t* keys,
+                           const int64_t* deltas, uint64_t n, uint64_t out[5], void* stream) {
+    // validate_moment_spec (verify.cpp:480-503)
+    if (b < 2 || b > 31) return fail(MB200_INVALID_ARGUMENT, "width must be in [2, 31]");
+    if (splitter != MB200_SPLIT_POW2 && splitter != MB200_SPLIT_UNIFORM_ARB && splitter != MB200_SPLIT_MERSENNE_ARB)
+        return fail(MB200_INVALID_ARGUMENT, "unknown splitter");
+    // validate_splitter_width (verify.cpp:401-409)
+    if (buckets < 1) return fail(MB200_INVALID_ARGUMENT, "bucket count must be at least 1");
+    if (splitter == MB200_SPLIT_POW2 && (buckets & (buckets - 1)) != 0)
+        return fail(MB200_INVALID_ARGUMENT, "bucket count must be a power of two for this splitter");
+    if (buckets > (1ull << (b - 1))) return fail(MB200_INVALID_ARGUMENT, "bucket count exceeds half the hash range");
+    const uint64_t p = (1ull << b) - 1;
+    if (key_domain < 1 || key_domain > p) return fail(MB200_INVALID_ARGUMENT, "modulus too small for key domain");
+    if (n == 0) return fail(MB200_INVALID_ARGUMENT, "stream must not be empty");
+    if (!keys || !deltas || !out) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    uint64_t weight = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (keys[i] >= key_domain) return fail(MB200_INVALID_ARGUMENT, "key outside domain");
+        weight += deltas[i] < 0 ? 0ull - (uint64_t)deltas[i] : (uint64_t)deltas[i];
+        if (weight > 1024) return fail(MB200_INVALID_ARGUMENT, "stream weights too large for exact enumeration");
+    }
+    {
+        std::vector<uint64_t> res(n);
+        for (uint64_t i = 0; i < n; ++i) res[i] = keys[i] % p;
+        std::sort(res.begin(), res.end());
+        if (std::adjacent_find(res.begin(), res.end()) != res.end())
+            return fail(MB200_INVALID_ARGUMENT, "stream keys must be distinct modulo the modulus");
+    }
+    // exact_family_count (verify.cpp:566-573)
+    if (b > 15) return fail(MB200_INVALID_ARGUMENT, "width must be in [2, 15] to enumerate exactly");
+    // entries with delta = 0 never move a counter
+    std::vector<uint32_t> xs;
+    std::vector<int32_t> ws;
+    uint32_t w2 = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (deltas[i] == 0) continue;
+        ws.push_back((int32_t)deltas[i]);
+        w2 += (uint32_t)(deltas[i] * deltas[i]);
+    }
+    const uint32_t m = (uint32_t)ws.size();
+    if (m > 64) return fail(MB200_UNSUPPORTED, "GPU enumeration supports at most 64 non-zero stream entries");
+    xs.resize(3 * (size_t)m);
+    for (uint64_t i = 0, j = 0; i < n; ++i) {
+        if (deltas[i] == 0) continue;
+        const uint64_t x = keys[i] % p, x2 = x * x % p;
+        xs[j] = (uint32_t)x;
+        xs[m + j] = (uint32_t)x2;
+        xs[2 * m + j] = (uint32_t)(x2 * x % p);
+        ++j;
+    }
+    SketchParams sp;
+    std::memset(&sp, 0, sizeof(sp));
+    sp.rows = sp.families = 1;
+    sp.b = b;
+    sp.p = p;
+    sp.splitter = (uint32_t)splitter;
+    sp.width = buckets;
+    sp.lw = (unsigned)__builtin_ctzll(buckets);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t xs_bytes = 3 * (size_t)m * 4 + 16, ws_bytes = (size_t)m * 4 + 16, tab_bytes = (size_t)p * 2 + 16;
+    unsigned char* ws_dev = nullptr;
+    cudaError_t e = cudaMallocAsync(&ws_dev, 32 + xs_bytes + ws_bytes + tab_bytes, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    unsigned long long* d_out = reinterpret_cast<unsigned long long*>(ws_dev);
+    uint32_t* d_xs = reinterpret_cast<uint32_t*>(ws_dev + 32);
+    int32_t* d_ws = reinterpret_cast<int32_t*>(ws_dev + 32 + xs_bytes);
+    uint16_t* d_tab = reinterpret_cast<uint16_t*>(ws_dev + 32 + xs_bytes + ws_bytes);
+    uint64_t host[4] = {0, 0, 0, 0};
+    e = cudaMemsetAsync(d_out, 0, 32, s);
+    if (e == cudaSuccess && m) e = cudaMemcpyAsync(d_xs, xs.data(), 3 * (size_t)m * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && m) e = cudaMemcpyAsync(d_ws, ws.data(), (size_t)m * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = launch_enum_moments(sp, m, w2, d_xs, d_ws, d_tab, d_out, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host, d_out, 32, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(ws_dev, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "mb200_enum_moment_sums");
+    for (int i = 0; i < 4; ++i) out[i] = host[i];
+    out[4] = p * p * p * p;
+    return MB200_OK;
 }
 
 int mb200_cs_update(const mb200_sketch_desc* desc, const void* d_keys, int key_width, const void* d_weights,

@@ -146,6 +146,71 @@ __global__ void count_above_kernel(const u64* __restrict__ v, uint64_t n, u64 ma
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(count, bad);
 }
 
+// Bucket maps (bucketing.cpp:61-95) on u64 values, b <= 64:
+//   KIND 0 map_pow2      (v r) >> b
+//   KIND 1 map_mersenne  ((v + 1) r) >> b
+//   KIND 2 ExactDivisionMap  floor(v r / p) by Alg 4 with the constructor's m
+// The product is formed in registers (u128), so one launch reads 8 B and
+// writes 8 B per value (HBM-bound, like K6).  Values >= `bound` (the map's
+// domain; 0 = every u64 is in the domain) are counted into flags[0].
+template <int KIND, int B, int M>
+__device__ __forceinline__ u64 bucket_one(u64 v, u32 b_rt, u64 c, u32 m_rt, u64 r, u64 bound, unsigned& bad) {
+    bad += bound != 0 && v >= bound;
+    if (KIND == 2) {
+        u64 q, rem;
+        unsigned overflow = 0;  // impossible inside the domain ((p-1) r <= max_input by construction)
+        divmod_one<B, M>(v * r, __umul64hi(v, r), b_rt, c, m_rt, q, rem, overflow);
+        return q;
+    }
+    const u64 x = KIND == 1 ? v + 1 : v;  // v < 2^b - 1, so no wrap for b = 64
+    const u64 lo = x * r, hi = __umul64hi(x, r);
+    const u32 b = B ? (u32)B : b_rt;
+    return b == 64 ? hi : (lo >> b) | (hi << (64 - b));
+}
+
+template <int KIND, int B, int M>
+__global__ void __launch_bounds__(kThreads) bucket_map_kernel(const u64* __restrict__ v, uint64_t n, u32 b, u64 c,
+                                                              u32 m, u64 r, u64 bound, u64* __restrict__ out,
+                                                              unsigned long long* flags) {
+    const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(v);
+    ulonglong2* o2 = reinterpret_cast<ulonglong2*>(out);
+    const uint64_t npairs = n >> 1;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    unsigned bad = 0;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (kUnroll - 1) * stride < npairs; i += kUnroll * stride) {
+        ulonglong2 a[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) a[u] = ld_stream(v2 + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            st_stream(o2 + i + u * stride,
+                      make_ulonglong2(bucket_one<KIND, B, M>(a[u].x, b, c, m, r, bound, bad),
+                                      bucket_one<KIND, B, M>(a[u].y, b, c, m, r, bound, bad)));
+    }
+    for (; i < npairs; i += stride) {
+        const ulonglong2 a = ld_stream(v2 + i);
+        st_stream(o2 + i, make_ulonglong2(bucket_one<KIND, B, M>(a.x, b, c, m, r, bound, bad),
+                                          bucket_one<KIND, B, M>(a.y, b, c, m, r, bound, bad)));
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+        out[n - 1] = bucket_one<KIND, B, M>(v[n - 1], b, c, m, r, bound, bad);
+    bad = __reduce_add_sync(0xffffffffu, bad);
+    if (bad && (threadIdx.x & 31) == 0) atomicAdd(flags, (unsigned long long)bad);
+}
+
+template <int KIND, int B, int M>
+__global__ void __launch_bounds__(kThreads) bucket_map_scalar(const u64* __restrict__ v, uint64_t n, u32 b, u64 c,
+                                                              u32 m, u64 r, u64 bound, u64* __restrict__ out,
+                                                              unsigned long long* flags) {
+    unsigned bad = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = bucket_one<KIND, B, M>(v[i], b, c, m, r, bound, bad);
+    bad = __reduce_add_sync(0xffffffffu, bad);
+    if (bad && (threadIdx.x & 31) == 0) atomicAdd(flags, (unsigned long long)bad);
+}
+
 int grid_for(uint64_t items, int per_sm) {
     const uint64_t need = (items + kThreads - 1) / kThreads;
     const uint64_t cap = (uint64_t)sm_count() * per_sm;
@@ -169,6 +234,31 @@ cudaError_t launch_pm_divmod(const uint64_t* v, uint64_t n, uint32_t b, uint64_t
     else if (b == 64 && iters == 2) pm_divmod_kernel<64, 2><<<g, kThreads, 0, s>>>(v, n, b, c, iters, q, r, d_flags);
     else if (b == 64) pm_divmod_kernel<64, 0><<<g, kThreads, 0, s>>>(v, n, b, c, iters, q, r, d_flags);
     else pm_divmod_kernel<0, 0><<<g, kThreads, 0, s>>>(v, n, b, c, iters, q, r, d_flags);
+    return cudaGetLastError();
+}
+
+namespace {
+template <int KIND, int B, int M>
+void bucket_launch(bool vec, const uint64_t* v, uint64_t n, uint32_t b, uint64_t c, uint32_t m, uint64_t r,
+                   uint64_t bound, uint64_t* out, unsigned long long* flags, cudaStream_t s) {
+    if (vec)
+        bucket_map_kernel<KIND, B, M>
+            <<<grid_for((n / 2 + kUnroll - 1) / kUnroll, 8), kThreads, 0, s>>>(v, n, b, c, m, r, bound, out, flags);
+    else
+        bucket_map_scalar<KIND, B, M><<<grid_for(n, 8), kThreads, 0, s>>>(v, n, b, c, m, r, bound, out, flags);
+}
+}  // namespace
+
+cudaError_t launch_bucket_map(int kind, const uint64_t* v, uint64_t n, uint32_t b, uint64_t c, uint32_t m,
+                              uint64_t r, uint64_t bound, uint64_t* out, unsigned long long* d_flags, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const bool vec = (((uintptr_t)v | (uintptr_t)out) & 15) == 0;
+    if (kind == 0) bucket_launch<0, 0, 0>(vec, v, n, b, c, m, r, bound, out, d_flags, s);
+    else if (kind == 1) bucket_launch<1, 0, 0>(vec, v, n, b, c, m, r, bound, out, d_flags, s);
+    else if (b == 64 && m == 2) bucket_launch<2, 64, 2>(vec, v, n, b, c, m, r, bound, out, d_flags, s);
+    else if (b == 64 && m == 3) bucket_launch<2, 64, 3>(vec, v, n, b, c, m, r, bound, out, d_flags, s);
+    else if (b == 64) bucket_launch<2, 64, 0>(vec, v, n, b, c, m, r, bound, out, d_flags, s);
+    else bucket_launch<2, 0, 0>(vec, v, n, b, c, m, r, bound, out, d_flags, s);
     return cudaGetLastError();
 }
 

@@ -17,7 +17,6 @@ enum SplitKind { SPLIT_POW2 = 0, SPLIT_UNIFORM_ARB = 1, SPLIT_MERSENNE_ARB = 2, 
 
 struct HashParams {
     uint32_t b, k;
-    uint32_t c31 = 0x80000000u, c2 = 2;  // opaque multipliers (see h61_step_l31)
     uint64_t p;
     uint64_t lo[kMaxK];
     uint64_t hi[kMaxK];
@@ -68,6 +67,15 @@ cudaError_t launch_pm_divmod(const uint64_t* v, uint64_t n, uint32_t b, uint64_t
                              uint64_t* q, uint64_t* r, unsigned long long* d_flags, cudaStream_t s);
 cudaError_t launch_count_above(const uint64_t* v, uint64_t n, uint64_t max_lo, uint64_t max_hi,
                                unsigned long long* d_count, cudaStream_t s);
+// bucket maps: kind 0 map_pow2, 1 map_mersenne, 2 exact division (m iterations);
+// values >= bound (0 = no bound) are counted into *d_flags
+cudaError_t launch_bucket_map(int kind, const uint64_t* v, uint64_t n, uint32_t b, uint64_t c, uint32_t m,
+                              uint64_t r, uint64_t bound, uint64_t* out, unsigned long long* d_flags,
+                              cudaStream_t s);
+
+// exhaustive moment enumeration (kernels_enum.cu): sp carries b, p, splitter, width
+cudaError_t launch_enum_moments(const SketchParams& sp, uint32_t n, uint32_t w2, const uint32_t* xs,
+                                const int32_t* ws, uint16_t* tab, unsigned long long* out, cudaStream_t s);
 
 // workload generators (kernels_gen.cu)
 cudaError_t launch_gen_u32(uint64_t seed, uint64_t start, uint64_t n, uint32_t* out, cudaStream_t s);

@@ -159,6 +159,29 @@ int mb200_pm_modulus(unsigned b, uint64_t c, unsigned m_iters, unsigned* iterati
     return MB200_OK;
 }
 
+int mb200_exact_division_iterations(unsigned b, uint64_t c, uint64_t r, unsigned* iterations) {
+    using mb200::fail;
+    if (int rc = mb200_pm_modulus(b, c, 0, nullptr, nullptr)) return rc;  // PseudoMersenneModulus(b, c)
+    const u128 p = (u128(1) << b) - c;
+    if (r == 0 || u128(r) > p) return fail(MB200_INVALID_ARGUMENT, "bucket count must be in [1, p]");
+    // bucketing.cpp:80-88: grow m until the largest product (p-1) r is admissible
+    Big largest;
+    largest.w = {u64(p - 1), u64((p - 1) >> 64)};
+    largest.trim();
+    largest.mul(r);
+    for (unsigned m = 1;; ++m) {
+        u64 thr[4];
+        domain_threshold(b, c, m, thr);
+        Big t;
+        t.w.assign(thr, thr + 4);
+        t.trim();
+        if (cmp(largest, t) <= 0) {
+            if (iterations) *iterations = m;
+            return MB200_OK;
+        }
+    }
+}
+
 int mb200_draw_coeffs(unsigned b, unsigned k, uint64_t seed, uint64_t* lo, uint64_t* hi) {
     using mb200::fail;
     if (b < 2 || b > 127) return fail(MB200_INVALID_ARGUMENT, "exponent must be in [2, 127]");

@@ -77,6 +77,40 @@ void PseudoMersenneModulus::divmod(const u64* h_v, u64 n, u64* h_q, u64* h_r) co
     cuda_check(cudaMemcpy(h_r, r.p, n * sizeof(u64), cudaMemcpyDeviceToHost), "D2H");
 }
 
+// -------------------------------------------------------------- bucketing --
+void map_pow2_device(const u64* d_v, u64 n, unsigned b, u64 r, u64* d_out, void* stream) {
+    throw_status(mb200_bucket_map(MB200_MAP_POW2, d_v, n, b, 0, r, d_out, nullptr, stream));
+}
+
+void map_mersenne_device(const u64* d_v, u64 n, unsigned b, u64 r, u64* d_out, void* stream) {
+    throw_status(mb200_bucket_map(MB200_MAP_MERSENNE, d_v, n, b, 0, r, d_out, nullptr, stream));
+}
+
+namespace {
+PseudoMersenneModulus exact_divider(const PseudoMersenneModulus& mod, u64 r) {
+    unsigned m = 0;
+    throw_status(mb200_exact_division_iterations(mod.b(), mod.c(), r, &m));
+    return PseudoMersenneModulus(mod.b(), mod.c(), m);
+}
+}  // namespace
+
+ExactDivisionMap::ExactDivisionMap(const PseudoMersenneModulus& mod, u64 r)
+    : divider_(exact_divider(mod, r)), r_(r) {}
+
+void ExactDivisionMap::map_device(const u64* d_v, u64 n, u64* d_out, void* stream) const {
+    throw_status(mb200_bucket_map(MB200_MAP_EXACT_DIV, d_v, n, divider_.b(), divider_.c(), r_, d_out, nullptr,
+                                  stream));
+}
+
+u64 ExactDivisionMap::operator()(u64 v) const {
+    DevBuf<u64> d(2);
+    cuda_check(cudaMemcpy(d.p, &v, sizeof(u64), cudaMemcpyHostToDevice), "H2D");
+    map_device(d.p, 1, d.p + 1, nullptr);
+    u64 out = 0;
+    cuda_check(cudaMemcpy(&out, d.p + 1, sizeof(u64), cudaMemcpyDeviceToHost), "D2H");
+    return out;
+}
+
 // --------------------------------------------------------------- polyhash --
 PolyHashFamily::PolyHashFamily(const MersenneModulus& modulus, unsigned k, u128 key_domain, u64 seed,
                                HashFinish finish)

@@ -2,6 +2,8 @@
 // test_{field,polyhash,sketch}.cpp under /root/reference/proj), re-run against
 // mersenne::b200 (include/mersenne_b200/mersenne_b200.hpp) on the GPU, plus
 // batch parity against the C oracle (oracle/liboracle.so, test infrastructure).
+#include <cuda_runtime.h>
+
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
@@ -102,6 +104,46 @@ static void test_polyhash() {  // test_polyhash.cpp:57-88
     CHECK(same);
 }
 
+static void test_bucketing() {  // test_bucketing.cpp:101-127
+    PseudoMersenneModulus m13(4, 3);
+    ExactDivisionMap map4(m13, 4);
+    long counts[4] = {0, 0, 0, 0};
+    for (u64 v = 0; v < 13; ++v) ++counts[map4(v)];
+    CHECK(counts[0] == 4 && counts[1] == 3 && counts[2] == 3 && counts[3] == 3);
+    ExactDivisionMap ident(m13, 13);
+    bool id = true;
+    for (u64 v = 0; v < 13; ++v) id &= ident(v) == v;
+    CHECK(id);
+    CHECK(map4.buckets() == 4 && map4.divider().iterations() >= 1);
+    CHECK_THROWS_AS(ExactDivisionMap(m13, 0), std::invalid_argument);
+    CHECK_THROWS_AS(ExactDivisionMap(m13, 14), std::invalid_argument);
+    CHECK_THROWS_AS(map4(13), std::domain_error);
+    // batch vs oracle at b = 64
+    const PseudoMersenneModulus big(64, 59);
+    const ExactDivisionMap dmap(big, 1000003);
+    const u64 n = 4099;
+    std::vector<u64> v(n), got(n);
+    orc_gen_u64_keys(5, 0, n, v.data());
+    for (auto& x : v) x %= u64(big.p());
+    u64 *d_v = nullptr, *d_o = nullptr;
+    cudaMalloc(&d_v, n * 8);
+    cudaMalloc(&d_o, n * 8);
+    cudaMemcpy(d_v, v.data(), n * 8, cudaMemcpyHostToDevice);
+    dmap.map_device(d_v, n, d_o);
+    cudaMemcpy(got.data(), d_o, n * 8, cudaMemcpyDeviceToHost);
+    bool same = true;
+    const unsigned m = orc_exact_div_iterations(64, 59, 1000003);
+    for (u64 i = 0; i < n; ++i) same &= got[i] == orc_bucket_map(2, 64, 59, m, 1000003, v[i]);
+    CHECK(same && m == dmap.divider().iterations());
+    map_pow2_device(d_v, n, 64, 77, d_o);
+    cudaMemcpy(got.data(), d_o, n * 8, cudaMemcpyDeviceToHost);
+    same = true;
+    for (u64 i = 0; i < n; ++i) same &= got[i] == orc_bucket_map(0, 64, 0, 0, 77, v[i]);
+    CHECK(same);
+    cudaFree(d_v);
+    cudaFree(d_o);
+}
+
 static void test_sketch() {  // test_sketch.cpp
     CHECK((split_pow2(0b110, 3, 2) == SignIndexPair{2, -1}));
     CHECK((split_pow2(0, 3, 2) == SignIndexPair{0, +1}));
@@ -182,6 +224,7 @@ int main() {
     try {
         test_field();
         test_polyhash();
+        test_bucketing();
         test_sketch();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "unexpected exception: %s\n", e.what());

@@ -69,6 +69,10 @@ class Oracle:
         _sig(lib, "orc_split_pow2", None, [u64, u64, U, U, P, P])
         _sig(lib, "orc_split_arb_uniform", None, [u64, u64, U, u64, P, P])
         _sig(lib, "orc_split_arb_mersenne", None, [u64, u64, U, u64, P, P])
+        _sig(lib, "orc_exact_div_iterations", U, [U, u64, u64])
+        _sig(lib, "orc_enum_moment_sums", None, [U, u64, I, P, P, u64, P])
+        _sig(lib, "orc_bucket_map", u64, [I, U, u64, U, u64, u64])
+        _sig(lib, "orc_bucket_map_batch", None, [I, U, u64, U, u64, P, u64, P])
         _sig(lib, "orc_cs_process", u64,
              [U, u64, U, U, P, P, U, I, P, P, P, P, u64, P])
         _sig(lib, "orc_cs_row_moment", None, [P, u64, P, P, P])
@@ -183,6 +187,22 @@ class Oracle:
         fn(h & (2**64 - 1), h >> 64, b, l_or_r, C.byref(idx), C.byref(sign))
         return idx.value, sign.value
 
+
+    def enum_moment_sums(self, b, buckets, splitter, stream):
+        keys = np.array([k for k, _ in stream], np.uint64)
+        deltas = np.array([d for _, d in stream], np.int64)
+        out = np.zeros(4, np.uint64)
+        self.lib.orc_enum_moment_sums(b, buckets, splitter, ptr(keys), ptr(deltas), len(keys), ptr(out))
+        return int(out[0]) | (int(out[1]) << 64), int(out[2]) | (int(out[3]) << 64)
+
+    def bucket_map(self, kind, b, r, v, c=0):
+        """kind 0 map_pow2, 1 map_mersenne, 2 ExactDivisionMap; returns (m, out)."""
+        v = np.ascontiguousarray(v, np.uint64)
+        m = self.lib.orc_exact_div_iterations(b, c, r) if kind == 2 else 1
+        out = np.zeros(len(v), np.uint64)
+        if m:
+            self.lib.orc_bucket_map_batch(kind, b, c, m, r, ptr(v), len(v), ptr(out))
+        return m, out
     def cs_process(self, rows, width, b, coeff_rows, key_bits, splitter, keys, weights=None,
                    counters=None):
         """coeff_rows: list (families) of coefficient lists."""
@@ -290,6 +310,7 @@ class Ref:
         _sig(lib, "ref_pm_divmod", I, [U, u64, U, u64, u64, P, P, P, P])
         _sig(lib, "ref_cch_divmod", None, [U, u64, u64, u64, P, P, P, P])
         _sig(lib, "ref_split", None, [I, u64, u64, U, u64, P, P])
+        _sig(lib, "ref_bucket_map", U, [I, U, u64, u64, P, u64, P])
         _sig(lib, "ref_cs_run", I, [U, u64, U, U, I, u64, P, P, P, P, u64, I, P, P])
         _sig(lib, "ref_cs_run_families", I, [U, u64, U, U, I, U, P, P, P, P, u64, P, P])
         _sig(lib, "ref_cs_point_query", I, [U, u64, U, U, I, u64, P, P, u64, P, u64, P])
@@ -371,6 +392,12 @@ class Ref:
                            C.byref(sign))
         return idx.value, sign.value
 
+
+    def bucket_map(self, kind, b, r, v, c=0):
+        v = np.ascontiguousarray(v, np.uint64)
+        out = np.zeros(len(v), np.uint64)
+        m = self.lib.ref_bucket_map(kind, b, c, r, ptr(v), len(v), ptr(out))
+        return m, out
     def cs_run(self, rows, width, b, key_bits, splitter, seed, keys, weights=None, threads=1):
         k64 = k32 = w32 = w64 = None
         if keys.dtype == np.uint32:

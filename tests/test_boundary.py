@@ -57,6 +57,26 @@ def test_host_pm_modulus_matches_oracle(mb, orc):
     assert mb.pm_modulus(64, 59) == orc.pm_setup(64, 59)[:2]
 
 
+def test_host_exact_division_iterations(mb, orc, ref):
+    """ExactDivisionMap ctor (bucketing.cpp:75-89) on the host vs oracle and compiled reference."""
+    rng = np.random.default_rng(0xE)
+    cases = [(4, 3, 4), (4, 3, 13), (3, 1, 3), (64, 59, (1 << 64) - 59), (64, (1 << 62) + 1, 12345)]
+    for _ in range(150):
+        b = int(rng.integers(3, 65))
+        c = int(rng.integers(1, 2 ** min(b - 1, 63)))
+        p = (1 << b) - c
+        r = int(rng.integers(1, min(p, 2**63 - 1) + 1)) if rng.random() < 0.7 else p if p < 2**64 else 1
+        cases.append((b, c, r))
+    for b, c, r in cases:
+        m = mb.exact_division_iterations(b, c, r)
+        assert m == orc.lib.orc_exact_div_iterations(b, c, r)
+        assert m == ref.bucket_map(2, b, r, np.zeros(1, np.uint64), c=c)[0], (b, c, r)
+    with pytest.raises(mb.InvalidArgument, match=r"bucket count must be in \[1, p\]"):
+        mb.exact_division_iterations(4, 3, 14)
+    with pytest.raises(mb.InvalidArgument, match="offset"):
+        mb.exact_division_iterations(4, 8, 1)
+
+
 def test_validation_messages(mb):
     with pytest.raises(mb.InvalidArgument, match=r"offset must satisfy 1 <= c < 2\^\(b-1\)"):
         mb.pm_modulus(4, 8)
@@ -103,3 +123,28 @@ def test_no_cpu_fallback(mb):
 
     with pytest.raises(mb.InvalidArgument, match="CUDA tensors"):
         mb.hash61(torch.zeros(8, dtype=torch.int32), mb.draw_coeffs(61, 4, 1))
+
+
+def test_enum_moment_validation_without_gpu(mb):
+    """validate_moment_spec / exact_family_count messages (verify.cpp:480-503, 566-573):
+    all checked on the host before any device work."""
+    s = [(1, 2), (3, -1), (7, 3)]
+    bad = [
+        (dict(b=1, buckets=4, splitter=0, stream=s), "width must be in \\[2, 31\\]"),
+        (dict(b=5, buckets=0, splitter=0, stream=s), "bucket count must be at least 1"),
+        (dict(b=5, buckets=3, splitter=0, stream=s), "power of two for this splitter"),
+        (dict(b=5, buckets=17, splitter=2, stream=s), "exceeds half the hash range"),
+        (dict(b=5, buckets=4, splitter=0, stream=s, key_domain=32), "modulus too small for key domain"),
+        (dict(b=5, buckets=4, splitter=0, stream=[]), "stream must not be empty"),
+        (dict(b=5, buckets=4, splitter=0, stream=s, key_domain=5), "key outside domain"),
+        (dict(b=5, buckets=4, splitter=0, stream=[(1, 1000), (2, 25)]), "too large for exact enumeration"),
+        (dict(b=5, buckets=4, splitter=0, stream=[(1, 1), (1, 2)]), "distinct modulo the modulus"),
+        (dict(b=16, buckets=4, splitter=0, stream=s), "\\[2, 15\\] to enumerate exactly"),
+        (dict(b=5, buckets=4, splitter=3, stream=s), "unknown splitter"),
+    ]
+    for kw, msg in bad:
+        with pytest.raises(mb.InvalidArgument, match=msg):
+            mb.enum_moment_sums(**kw)
+    big = [(i, 1) for i in range(70)]
+    with pytest.raises(mb.Unsupported, match="64 non-zero"):
+        mb.enum_moment_sums(7, 4, 0, big)

@@ -173,6 +173,67 @@ def test_divmod_random(cuda, mb, orc, b, c):
     assert all(int(host_u64(q)[i]) == vals[i] // p for i in range(64))
 
 
+# ---------------------------------------------------------------- bucket maps
+def test_golden_bucket_maps(cuda, mb, golden):
+    for case in golden["bucket_maps"]:
+        b, c, r = case["b"], int(case["c"]), int(case["r"])
+        if case["kind"] == mb.MAP_EXACT_DIV:
+            assert mb.exact_division_iterations(b, c, r) == case["iterations"]
+        out = mb.bucket_map(case["kind"], dev(np.array(case["v"], np.uint64)), b, r, c)
+        assert [int(x) for x in host_u64(out)] == case["out"]
+
+
+def test_bucket_map_known_answers(cuda, mb):
+    # test_bucketing.cpp:101-127
+    m13 = mb.ExactDivisionMap(4, 3, 4)
+    out = host_u64(m13(dev(np.arange(13, dtype=np.uint64)))).astype(np.int64)
+    assert np.bincount(out, minlength=4).tolist() == [4, 3, 3, 3]
+    ident = mb.ExactDivisionMap(4, 3, 13)
+    assert host_u64(ident(dev(np.arange(13, dtype=np.uint64)))).tolist() == list(range(13))
+    for r in (0, 14):
+        with pytest.raises(mb.InvalidArgument, match=r"bucket count must be in \[1, p\]"):
+            mb.ExactDivisionMap(4, 3, r)
+    x = dev(np.arange(32, dtype=np.uint64))
+    assert host_u64(mb.bucket_map(mb.MAP_POW2, x, 5, 32)).tolist() == list(range(32))
+    assert host_u64(mb.bucket_map(mb.MAP_POW2, x, 5, 1)).tolist() == [0] * 32
+
+
+@pytest.mark.parametrize("kind,b,c,r", [(0, 64, 0, 1000003), (0, 61, 0, 1 << 61), (0, 17, 0, 5),
+                                         (1, 64, 0, (1 << 63) + 12345), (1, 40, 0, 77),
+                                         (2, 64, 59, (1 << 64) - 59), (2, 64, 59, 1000),
+                                         (2, 64, (1 << 62) + 1, 12345), (2, 33, 7, 1 << 32),
+                                         (2, 61, 1, (1 << 61) - 1), (2, 48, (1 << 40) + 3, 1 << 47)])
+def test_bucket_map_random(cuda, mb, orc, kind, b, c, r):
+    dom = (1 << b) - (c if kind == 2 else kind)
+    n = (1 << 20) + 3  # odd: exercises the vector body and the scalar tail
+    v = orc.gen_u64_keys(kind * 1000 + b, 0, n)
+    if dom < (1 << 64):
+        v = v % np.uint64(dom)
+    v[:3] = [0, 1, dom - 1]
+    got = host_u64(mb.bucket_map(kind, dev(v), b, r, c))
+    m, exp = orc.bucket_map(kind, b, r, v, c=c)
+    assert (got == exp).all()
+    # unaligned views take the scalar kernel
+    got1 = host_u64(mb.bucket_map(kind, dev(v)[1:], b, r, c))
+    assert (got1 == exp[1:]).all()
+
+
+def test_bucket_map_domain(cuda, mb):
+    import torch
+
+    v = dev(np.array([0, 5, 12, 13, 40], np.uint64))
+    with pytest.raises(mb.DomainError, match="outside the map's domain"):
+        mb.bucket_map(mb.MAP_EXACT_DIV, v, 4, 4, 3)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    mb.bucket_map(mb.MAP_EXACT_DIV, v, 4, 4, 3, out_of_domain=cnt)
+    assert int(cnt.item()) == 2
+    with pytest.raises(mb.DomainError):
+        mb.bucket_map(mb.MAP_MERSENNE, dev(np.array([7], np.uint64)), 3, 3)
+    assert mb.bucket_map(mb.MAP_POW2, dev(np.zeros(0, np.uint64)), 5, 3).numel() == 0
+    with pytest.raises(mb.Unsupported):
+        mb.bucket_map(mb.MAP_EXACT_DIV, v, 89, 4, 1)
+
+
 # ---------------------------------------------------------------- sketches
 def make_spec(mb, orc, rows, width, b, key_bits, splitter, seed):
     if splitter == mb.SPLIT_TWO_FOR_ONE:
@@ -544,3 +605,58 @@ def test_full_size_c1_and_c5(cuda, mb, orc):
     assert (cnt.cpu().numpy() == exp).all()
     m = mb.moments_to_python(mb.cs_moments(cnt, 5, 65536))
     assert mb.lower_median(m) == orc.second_moment(exp, 5, 65536, True)
+
+
+# ---------------------------------------------------------------- moment enumeration
+ENUM_STREAM = [(1, 2), (3, -1), (7, 3)]
+
+
+def test_enum_moment_sums_known_answers(cuda, mb):
+    # test_verify.cpp:205-265 frozen values (see tests/test_oracle.py for the derivation)
+    from fractions import Fraction
+
+    F = 31 ** 4
+    s = mb.enum_moment_sums(5, 4, mb.SPLIT_POW2, ENUM_STREAM, key_domain=16)
+    assert (s["sum_x"], s["sum_x_sq"], s["families"]) == (12931216, 226416064, F)
+    assert mb.enum_moment_sums(5, 4, mb.SPLIT_MERSENNE_ARB, ENUM_STREAM, 16)["sum_x"] == 12931216
+    assert mb.enum_moment_sums(5, 4, mb.SPLIT_POW2, [(5, 9)], 16)["sum_x_sq"] == 6561 * F
+    rep = mb.enum_sketch_moments(5, 4, mb.SPLIT_POW2, ENUM_STREAM, 16)
+    c = {x["name"]: x for x in rep["checks"]}
+    assert all(x["pass"] for x in rep["checks"])
+    assert c["mean matches exact formula"]["value"] == Fraction(13456, 961)
+    assert c["variance below bound"]["value"] == Fraction(45352128, 923521)
+    assert c["variance below bound"]["bound"] == Fraction(2 * 14 * 14, 4)
+    mrep = mb.enum_sketch_moments(5, 3, mb.SPLIT_MERSENNE_ARB, ENUM_STREAM, 16)
+    mv = [x for x in mrep["checks"] if x["name"] == "variance below bound"][0]
+    assert mv["value"] == Fraction(60396800, 923521)
+    assert mv["bound"] == Fraction(2 * 14 * 14 * (1024 + 9), 3 * 1024)
+    assert all(x["pass"] for x in mrep["checks"])
+
+
+@pytest.mark.parametrize("b,r,splitter,n", [(5, 4, 0, 3), (5, 3, 1, 5), (5, 16, 2, 9), (5, 1, 0, 17),
+                                             (4, 8, 0, 15), (6, 5, 2, 31), (6, 32, 0, 40), (3, 2, 1, 7)])
+def test_enum_moment_sums_vs_oracle(cuda, mb, orc, b, r, splitter, n):
+    p = (1 << b) - 1
+    rng = np.random.default_rng(b * 100 + n)
+    keys = rng.choice(p, size=n, replace=False)
+    budget = 1024 // n
+    deltas = rng.integers(-min(budget, 50), min(budget, 50) + 1, size=n)
+    deltas[0] = 0 if n > 3 else deltas[0]  # zero weights are skipped by the kernel
+    stream = [(int(k), int(d)) for k, d in zip(keys, deltas)]
+    got = mb.enum_moment_sums(b, r, splitter, stream)
+    exp = orc.enum_moment_sums(b, r, splitter, stream)
+    assert (got["sum_x"], got["sum_x_sq"]) == exp
+    assert got["families"] == p ** 4
+
+
+def test_enum_moment_mean_exact_b7(cuda, mb):
+    # p = 127 (2.6e8 families): the exact-mean identity holds on the GPU sums
+    from fractions import Fraction
+
+    stream = [(3, 5), (10, -7), (126, 2), (64, 1)]
+    for splitter, r in ((mb.SPLIT_POW2, 16), (mb.SPLIT_UNIFORM_ARB, 10), (mb.SPLIT_MERSENNE_ARB, 6)):
+        rep = mb.enum_sketch_moments(7, r, splitter, stream)
+        assert rep["sums"]["families"] == 127 ** 4
+        assert all(x["pass"] for x in rep["checks"]), rep["checks"]
+        f1, f2 = 1, 25 + 49 + 4 + 1
+        assert Fraction(rep["sums"]["sum_x"], 127 ** 4) == Fraction(f2 * 127 ** 2 + f1 * f1 - f2, 127 ** 2)

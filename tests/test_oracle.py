@@ -8,6 +8,7 @@
     against the reference itself.
 """
 import ctypes as C
+from fractions import Fraction
 
 import numpy as np
 import pytest
@@ -300,3 +301,100 @@ def test_sketch_matches_reference_all_splitters(orc, ref):
         r, moms, med = ref.cs_run(3, width, 31, 20, splitter, 0xC0FFEE, keys, w)
         assert (a == r).all()
         assert orc.second_moment(a, 3, width, True) == med
+
+
+# ------------------------------------------------------------------ bucket maps
+def _counts(vals, r):
+    return np.bincount(np.asarray(vals, np.int64), minlength=r).tolist()
+
+
+def test_bucket_map_known_answers(orc):
+    # test_bucketing.cpp:101-127 (ExactDivisionMap over p = 13 and p = 7)
+    m, out = orc.bucket_map(2, 4, 4, np.arange(13), c=3)
+    assert _counts(out, 4) == [4, 3, 3, 3]
+    _, ident = orc.bucket_map(2, 4, 13, np.arange(13), c=3)
+    assert ident.tolist() == list(range(13))
+    _, div3 = orc.bucket_map(2, 3, 3, np.arange(7), c=1)
+    _, mer3 = orc.bucket_map(1, 3, 3, np.arange(7))
+    assert sorted(_counts(div3, 3)) == sorted(_counts(mer3, 3))
+    assert _counts(div3, 3) != _counts(mer3, 3)
+    assert div3.tolist() != mer3.tolist()
+    assert orc.lib.orc_exact_div_iterations(4, 3, 0) == 0
+    assert orc.lib.orc_exact_div_iterations(4, 3, 14) == 0
+    assert orc.lib.orc_exact_div_iterations(4, 3, 13) > 0
+    # test_bucketing.cpp:83-98 (map_pow2 / map_mersenne)
+    _, pw = orc.bucket_map(0, 3, 3, np.arange(8))
+    assert sorted(_counts(pw, 3)) == [2, 3, 3]
+    assert orc.bucket_map(0, 5, 32, np.arange(32))[1].tolist() == list(range(32))
+    assert orc.bucket_map(0, 5, 1, np.arange(32))[1].tolist() == [0] * 32
+    assert orc.bucket_map(1, 3, 1, np.arange(7))[1].tolist() == [0] * 7
+    assert _counts(orc.bucket_map(1, 3, 7, np.arange(7))[1], 7) == [1] * 7
+
+
+def test_bucket_maps_most_uniform(orc):
+    # test_bucketing.cpp:129-150: every map keeps preimage sizes within one
+    for b in (4, 6, 9, 11):
+        q = 1 << b
+        for r in (1, 2, 3, 5, 8, 17, 33, 64):
+            if r > q - 1:
+                continue
+            for kind, dom, c in ((0, q, 0), (1, q - 1, 0), (2, q - 3, 3)):
+                _, out = orc.bucket_map(kind, b, r, np.arange(dom), c=c)
+                cnt = _counts(out, r)
+                assert max(cnt) - min(cnt) <= 1 and sum(cnt) == dom
+
+
+def test_bucket_maps_match_reference(orc, ref):
+    rng = np.random.default_rng(0xB0C)
+    cases = [(0, 64, 0, 1000003), (0, 17, 0, 5), (1, 64, 0, 2**63 + 12345), (1, 40, 0, 77),
+             (2, 64, 59, 2**64 - 59), (2, 64, 59, 1000), (2, 64, 2**62 + 1, 12345), (2, 33, 7, 2**32),
+             (2, 20, 1, 3), (2, 61, 1, 2**61 - 1), (2, 48, 2**40 + 3, 2**47)]
+    for kind, b, c, r in cases:
+        dom = (1 << b) - (c if kind == 2 else kind)
+        v = (rng.integers(0, 2**63, 4096, dtype=np.uint64) * np.uint64(3)) % np.uint64(dom) \
+            if dom < 2**64 else rng.integers(0, 2**63, 4096, dtype=np.uint64) * np.uint64(2)
+        v[:3] = [0, 1, dom - 1]
+        mo, out_o = orc.bucket_map(kind, b, r, v, c=c)
+        mr, out_r = ref.bucket_map(kind, b, r, v, c=c)
+        assert mo == mr, (kind, b, c, r)
+        assert (out_o == out_r).all(), (kind, b, c, r)
+    assert ref.bucket_map(2, 4, 14, np.arange(3), c=3)[0] == 0  # invalid_argument
+
+
+def test_golden_bucket_maps(orc, golden):
+    for case in golden["bucket_maps"]:
+        m, out = orc.bucket_map(case["kind"], case["b"], int(case["r"]), np.array(case["v"], np.uint64),
+                                c=int(case["c"]))
+        assert m == case["iterations"]
+        assert out.tolist() == case["out"]
+
+
+# ------------------------------------------------------------------ moment enumeration
+ENUM_STREAM = [(1, 2), (3, -1), (7, 3)]
+
+
+def test_enum_moment_sums_known_answers(orc):
+    # test_verify.cpp:205-216 (frozen values), :227-243 (variance 45352128/923521 for
+    # Pow2 r=4), :245-256 (variance 60396800/923521 for MersenneArb r=3): with
+    # F = 923521 families, sum_x_sq = F var + sum_x^2 / F.
+    F = 31 ** 4
+    sx, sxx = orc.enum_moment_sums(5, 4, 0, ENUM_STREAM)
+    assert (sx, sxx) == (12931216, 226416064)
+    assert F * Fraction(sxx, F) - Fraction(sx * sx, F) == 45352128
+    assert orc.enum_moment_sums(5, 4, 2, ENUM_STREAM)[0] == 12931216
+    sx3, sxx3 = orc.enum_moment_sums(5, 3, 2, ENUM_STREAM)
+    assert F * Fraction(sxx3, F) - Fraction(sx3 * sx3, F) == 60396800
+    # single key: X = 81 for every family, variance exactly zero (:258-265)
+    assert orc.enum_moment_sums(5, 4, 0, [(5, 9)]) == (81 * F, 6561 * F)
+
+
+@pytest.mark.parametrize("b,r,splitter", [(3, 2, 0), (3, 3, 1), (5, 3, 1), (5, 5, 2), (5, 8, 0)])
+def test_enum_moment_mean_is_exact(orc, b, r, splitter):
+    # size-independent property (verify.cpp:621-625, p prime): E[X] = (F2 p^2 + F1^2 - F2) / p^2
+    p = (1 << b) - 1
+    stream = [(0, 3), (2, -2), (5, 1), (p - 1, 4)][: 3 if b == 3 else 4]
+    sx, sxx = orc.enum_moment_sums(b, r, splitter, stream)
+    f1 = sum(d for _, d in stream)
+    f2 = sum(d * d for _, d in stream)
+    assert Fraction(sx, p ** 4) == Fraction(f2 * p * p + f1 * f1 - f2, p * p)
+    assert sxx >= sx * sx // p ** 4

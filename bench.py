@@ -354,8 +354,9 @@ def main():
     elapsed = max_over_ranks(t_start.elapsed_time(t_stop) / 1e3)
     kern = max_over_ranks(sum(a.elapsed_time(b) for a, b in k_ev) / 1e3 / args.steps)
     hs = mb.hot_stats(reset=True)
-    # L2 reductions per launch: every miss and every applied hot key touches the 5 rows
-    c5_reds = C5_ROWS * (hs["misses"] + hs["hot_applied"]) / args.steps
+    # L2 reductions per launch: every applied hot key touches the 5 rows, plus the
+    # bin-table merges and the row updates that took the direct path
+    c5_reds = (C5_ROWS * hs["hot_applied"] + hs["bin_merges"] + hs["direct"]) / args.steps
     moments = mb.moments_to_python(mom)
     f2 = mb.lower_median(moments)
     value = n_total * args.steps / elapsed
@@ -376,7 +377,10 @@ def main():
         "kernel_ms": kern * 1e3,
         "hot_path": {"miss_fraction": hs["misses"] / max(1, hs["items"]),
                      "hot_keys_per_cta": hs["hot_keys"] / max(1, args.steps * mb_sm_count(torch)),
-                     "l2_reds_per_item": c5_reds / max(1, n_local)},
+                     "l2_reds_per_item": c5_reds / max(1, n_local),
+                     "binned_entries_per_item": hs["binned"] / max(1, hs["items"]),
+                     "direct_row_updates": hs["direct"] / args.steps,
+                     "raw_batches": hs["raw_batches"]},
         # per step: hh_count, hh_hist, hh_select, cs_hot, cs_moments (the table zeroing is a torch fill)
         "gpu_launches": 5 * args.steps,
         "clocks": clocks,
@@ -536,7 +540,7 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
     mb.hot_stats(reset=True)
     tk = max_over_ranks(timed_steps(torch, steps, args.warmup, lambda: mb.cs_update(spec, keys, table)))
     hs = mb.hot_stats(reset=True)
-    c4_reds = 2 * (hs["misses"] + hs["hot_applied"]) / (steps + max(3, args.warmup))
+    c4_reds = (2 * hs["hot_applied"] + hs["bin_merges"] + hs["direct"]) / (steps + max(3, args.warmup))
     out["c4"] = {"value": C4_KEYS / t, "unit": "keys/s", "row_updates_per_s": 2 * C4_KEYS / t,
                  "ms_per_step": t * 1e3, "workload": "2^89-1 two-for-one, 2^26 u64 keys, 2 x 2^16 counters",
                  "l2": "inputs 512 MiB > L2", "roofline": roofline("c4", hi - lo, tk, "c4", l2_reds=c4_reds)}

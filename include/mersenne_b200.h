@@ -225,11 +225,21 @@ int mb200_gen_zipf_items(uint64_t master_seed, const uint64_t* d_cdf, uint32_t T
 
 /* ------------------------------------------------------------- probes --- */
 /* Counters of the heavy-hitter Count Sketch kernels since the last reset (device-
- * wide, synchronizes the device): [0] items, [1] items sent to the fused L2 path,
- * [2] shared-memory hot keys applied at kernel end (summed over CTAs), [3] hot-set
- * size summed over CTAs, [4..7] reserved (0).  L2 reductions issued =
- * rows x ([1] + [2]). */
+ * wide, synchronizes the device): [0] items, [1] items that missed the shared-
+ * memory hot set, [2] hot keys applied at kernel end (summed over CTAs), [3] hot-set
+ * size summed over CTAs, [4] row updates written to HBM bins, [5] row updates
+ * that took the direct red.global path, [6] red.global merges of bin tables,
+ * [7] batches binned from the raw stream (no hot pass).  L2 reductions issued =
+ * rows x [2] + [5] + [6]. */
 int mb200_hot_stats(uint64_t out[8], int reset);
+/* Strategy for Count Sketch tables larger than shared memory (both exact):
+ * MB200_LARGE_DIRECT (default) sends hot-set misses straight to L2 reductions;
+ * MB200_LARGE_BINNED routes them through HBM bins summed in shared memory.
+ * *previous (if not NULL) receives the strategy in force before the call.
+ * MB200_INVALID_ARGUMENT for an unknown strategy. */
+#define MB200_LARGE_DIRECT 0
+#define MB200_LARGE_BINNED 1
+int mb200_set_large_table_strategy(int strategy, int* previous);
 /* blocks x threads threads each issue 8 x iters independent mad.wide.u32 */
 int mb200_probe_imad(int blocks, int threads, int iters, uint64_t* d_sink, void* stream);
 int mb200_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* d_buf,

@@ -372,7 +372,18 @@ def hot_stats(reset: bool = False) -> dict:
     out = np.zeros(8, np.uint64)
     check(lib.mb200_hot_stats(_p(out), int(reset)))
     return {"items": int(out[0]), "misses": int(out[1]), "hot_applied": int(out[2]), "hot_keys": int(out[3]),
-            "tier2_hits": int(out[4]), "tier2_applied": int(out[5])}
+            "binned": int(out[4]), "direct": int(out[5]), "bin_merges": int(out[6]), "raw_batches": int(out[7])}
+
+
+LARGE_DIRECT, LARGE_BINNED = 0, 1
+
+
+def set_large_table_strategy(strategy: int) -> int:
+    """Route hot-set misses of large tables to L2 reductions (LARGE_DIRECT, default) or
+    through HBM bins (LARGE_BINNED); returns the previous strategy."""
+    prev = C.c_int(0)
+    check(lib.mb200_set_large_table_strategy(int(strategy), C.byref(prev)))
+    return prev.value
 
 
 # ------------------------------------------------------------------ host object

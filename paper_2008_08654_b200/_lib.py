@@ -116,6 +116,7 @@ SIGNATURES = [
     ("mb200_probe_atomics", I, [I, I, I, I, P, u64, P]),
     ("mb200_probe_dsmem", I, [I, I, I, I, I, u32, P, P]),
     ("mb200_hot_stats", I, [P, I]),
+    ("mb200_set_large_table_strategy", I, [I, P]),
 ]
 
 

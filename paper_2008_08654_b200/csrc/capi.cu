@@ -466,6 +466,13 @@ int mb200_hot_stats(uint64_t out[8], int reset) {
     return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_hot_stats");
 }
 
+int mb200_set_large_table_strategy(int strategy, int* previous) {
+    const int old = set_large_table_strategy(strategy);
+    if (old < 0) return fail(MB200_INVALID_ARGUMENT, "unknown large-table strategy");
+    if (previous) *previous = old;
+    return MB200_OK;
+}
+
 int mb200_probe_dsmem(int cluster, int mode, int blocks, int threads, int iters, uint32_t words, uint64_t* d_out,
                       void* stream) {
     cudaError_t e = launch_probe_dsmem(cluster, mode, blocks, threads, iters, words, d_out, (cudaStream_t)stream);

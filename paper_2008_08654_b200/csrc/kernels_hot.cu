@@ -16,11 +16,24 @@
 //   3. cs_hot    : one 1024-thread CTA per SM keeps the hot keys in a shared-
 //                  memory table with an exact 64-bit accumulator per key.  A hit
 //                  costs one shared reduction and no hashing.  Misses are
-//                  compacted per warp into full-warp batches that run the fused
-//                  hash -> split -> red.global path.  Warps pull 128-item tiles
-//                  of their CTA's contiguous range from a shared counter, so
-//                  they finish together.  Finally each CTA applies every hot key
-//                  once (hash -> split -> red).
+//                  compacted per warp into full-warp batches of 32 (key, delta)
+//                  pairs appended to a miss buffer in HBM.  Warps pull 128-item
+//                  tiles of their CTA's contiguous range from a shared counter,
+//                  so they finish together.  Finally each CTA applies every hot
+//                  key once (hash -> split -> red).
+//   4. cs_bin    : the misses (or, when the sample shows no heavy hitters, the
+//                  raw stream -- pass 3 is then skipped) are hashed, split and
+//                  turned into 4-byte entries (13-bit cell | 19-bit signed
+//                  delta) that are staged per (row, 8192-cell bin) in shared
+//                  memory and written to per-bin buffers in HBM in 16-byte
+//                  groups (one global atomic per bin per round).
+//   5. cs_accum  : one CTA per (bin, part) sums its bin's entries into an exact
+//                  shared-memory table of 8192 cells and merges it into the L2
+//                  table with one red.global per non-zero cell.
+// Passes 4-5 replace ~rows L2 reductions per missed item (the L2 atomic unit
+// runs at ~1.8e11/s, config 5's old bound) by 8 bytes of streaming HBM traffic
+// per row update.  Anything that does not fit a staging buffer, a bin, the
+// miss buffer or the 19-bit delta field takes the direct red.global path.
 // The table is bit-identical to the per-item path for ANY hot set (integer
 // addition commutes); the hot set only decides how much L2 traffic is saved.
 #include <type_traits>
@@ -29,9 +42,12 @@
 
 namespace mb200 {
 
-// per-process counters of the heavy-hitter kernel: items, misses (items sent to
-// the fused L2 path), hot keys applied at the end, hot-set size (summed over CTAs)
-__device__ unsigned long long g_hot_stats[8];  // [4..7] reserved (always 0)
+// per-process counters of the heavy-hitter pipeline: [0] items, [1] misses (items
+// not accumulated in a hot table), [2] hot keys applied at the end, [3] hot-set
+// size (summed over CTAs), [4] entries written to HBM bins, [5] row updates that
+// took the direct red.global path, [6] red.global merges of the bin tables,
+// [7] batches that ran in raw mode (no hot pass)
+__device__ unsigned long long g_hot_stats[8];
 
 namespace {
 
@@ -43,8 +59,7 @@ constexpr uint32_t kHotSample = 1u << 18;
 constexpr uint32_t kCountLog2 = 20;
 constexpr uint32_t kCountSlots = 1u << kCountLog2;
 constexpr int kQueue = 64;     // < 32 queued + one slot of 32 misses
-constexpr int kTileSlots = 4;  // items per lane per tile
-constexpr uint64_t kTile = 32ull * kTileSlots;
+constexpr uint32_t kMissChunk = 1024;  // miss-buffer slots a warp reserves at once
 
 template <typename KeyT>
 struct HotGeom;
@@ -63,13 +78,6 @@ struct HotGeom<u64> {
     using Cas = unsigned long long;
 };
 
-__device__ __forceinline__ u32 fmix32(u32 h) {
-    h ^= h >> 16;
-    h *= 0x85ebca6bu;
-    h ^= h >> 13;
-    h *= 0xc2b2ae35u;
-    return h ^ (h >> 16);
-}
 // two independent slot choices from the HIGH bits of multiplicative / mixing hashes
 template <uint32_t LOG2>
 __device__ __forceinline__ u32 slot1(u32 key) {
@@ -77,7 +85,7 @@ __device__ __forceinline__ u32 slot1(u32 key) {
 }
 template <uint32_t LOG2>
 __device__ __forceinline__ u32 slot2(u32 key) {
-    return fmix32(key) >> (32 - LOG2);
+    return ((key ^ (key >> 15)) * 0x2C1B3C6Du) >> (32 - LOG2);
 }
 template <uint32_t LOG2>
 __device__ __forceinline__ u32 slot1(u64 key) {
@@ -124,7 +132,7 @@ __global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist) {
 
 template <typename KeyT>
 __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restrict__ tc, const u32* __restrict__ hist,
-                                 u32 cap, KeyT* hot, u32* hot_cnt, u32* hot_count) {
+                                 u32 cap, KeyT* hot, u32* hot_cnt, u32* hot_count, u32* hot_sum) {
     __shared__ u32 thr;
     if (threadIdx.x == 0) {  // smallest threshold >= 2 whose tail fits the shared table
         u32 tail = 0, c = 255;
@@ -143,6 +151,7 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
             if (idx < cap) {
                 hot[idx] = tk[s];
                 hot_cnt[idx] = c;
+                atomicAdd(hot_sum, c);  // sampled items the hot set covers
             }
         }
     }
@@ -161,19 +170,86 @@ __device__ __forceinline__ void hot_accumulate(u32* lo, u32* hi, u32 h, i32 d) {
     if (carry) atomicAdd(hi + h, (u32)carry);
 }
 
+// Raw mode: the hot set covers under 30% of the sample, so the hot pass would
+// mostly copy the stream into the miss buffer; the binning pass then reads the
+// stream itself.  Every kernel of the pipeline evaluates this on the same inputs.
+__device__ __forceinline__ bool raw_mode(const u32* hot_sum, uint32_t sample) {
+    return (uint64_t)*hot_sum * 10 < (uint64_t)sample * 3;
+}
+
+// where a missed item goes: the HBM miss buffer (binned later) or, when the
+// buffer is full, the direct hash -> split -> red.global path
+template <typename KeyT>
+struct MissBuf {
+    KeyT* keys;
+    i32* deltas;
+    unsigned long long* count;  // items stored (multiple of 32; may exceed cap)
+    uint64_t cap;               // capacity, multiple of 32
+};
+
 template <int WK>
 __device__ __forceinline__ i32 load_w32(const void* w, uint64_t i) {
     if (WK == W_NONE) return 1;
     return ld_nc(reinterpret_cast<const i32*>(w) + i);
 }
 
+// a full warp of misses whose miss-buffer slots are gone: the direct path (rare)
+template <int MODE, int K, typename KeyT>
+__device__ __forceinline__ void misses_direct(const SketchParams& sp, KeyT key, i32 d, bool valid, i64* table) {
+    if (valid) process_item<MODE, K, GLOBAL>(sp, (u64)key, (i64)d, nullptr, table);
+}
+
+// 16-byte vector of keys / weights (4 u32 or 2 u64 keys per vector)
+template <typename KeyT>
+struct KeyVec;
+template <>
+struct KeyVec<u32> {
+    static constexpr int N = 4;
+    uint4 v;
+    __device__ __forceinline__ void load(const u32* p) { v = ld_stream(reinterpret_cast<const uint4*>(p)); }
+    __device__ __forceinline__ u32 operator[](int e) const { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
+};
+template <>
+struct KeyVec<u64> {
+    static constexpr int N = 2;
+    ulonglong2 v;
+    __device__ __forceinline__ void load(const u64* p) { v = ld_stream(reinterpret_cast<const ulonglong2*>(p)); }
+    __device__ __forceinline__ u64 operator[](int e) const { return e == 0 ? v.x : v.y; }
+};
+template <int N, int WK>
+struct WVec {
+    i32 d[N];
+    __device__ __forceinline__ void load(const void* w, uint64_t i) {
+        if (WK == W_NONE) {
+#pragma unroll
+            for (int e = 0; e < N; ++e) d[e] = 1;
+        } else if (N == 4) {
+            const int4 v = ld_stream(reinterpret_cast<const int4*>(reinterpret_cast<const i32*>(w) + i));
+            d[0] = v.x;
+            d[1] = v.y;
+            d[2] = v.z;
+            d[3] = v.w;
+        } else {
+            const long long v = __ldcs(reinterpret_cast<const long long*>(reinterpret_cast<const i32*>(w) + i));
+            d[0] = (i32)(u32)v;
+            d[1] = (i32)(u32)((u64)v >> 32);
+        }
+    }
+};
+
 template <int MODE, int K, typename KeyT, int WK>
 __global__ void __launch_bounds__(kHotThreads, 1)
     cs_hot_kernel(const SketchParams sp, const KeyT* __restrict__ keys, const void* __restrict__ w, uint64_t n,
                   i64* __restrict__ table, const KeyT* __restrict__ hot, const u32* __restrict__ hot_cnt,
-                  const u32* __restrict__ hot_count) {
+                  const u32* __restrict__ hot_count, const u32* __restrict__ hot_sum, uint32_t sample,
+                  const MissBuf<KeyT> mb, bool vec_ok) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
+    using KV = KeyVec<KeyT>;
+    constexpr int kV = KV::N;          // items per vector
+    constexpr int kVT = 8 / kV;        // vectors per lane per tile
+    constexpr int kIt = kV * kVT;      // items per lane per tile (8 u32 / 4 u64)
+    constexpr uint64_t kT = 32ull * kIt;
     constexpr uint32_t S = 1u << G::kLog2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
@@ -185,6 +261,22 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     KeyT* wqk = qk + warp * kQueue;
     i32* wqd = qd + warp * kQueue;
+    // CTAs own whole tiles (16-byte vector loads) and a share of the < kT tail
+    // items (scalar loads; everything, when the buffers are not 16-byte aligned)
+    const uint64_t ntiles_all = vec_ok ? n / kT : 0;
+    const uint64_t t_lo = ntiles_all * blockIdx.x / gridDim.x, t_hi = ntiles_all * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t rest = n - ntiles_all * kT;
+    const uint64_t tail_lo = ntiles_all * kT + rest * blockIdx.x / gridDim.x;
+    const uint64_t tail_hi = ntiles_all * kT + rest * (blockIdx.x + 1) / gridDim.x;
+    if (mb.cap != 0 && raw_mode(hot_sum, sample)) {  // the binning pass reads the stream itself
+        if (threadIdx.x == 0) {
+            const uint64_t cnt = (t_hi - t_lo) * kT + (tail_hi - tail_lo);
+            atomicAdd(&g_hot_stats[0], (unsigned long long)cnt);
+            atomicAdd(&g_hot_stats[1], (unsigned long long)cnt);
+            if (blockIdx.x == 0) atomicAdd(&g_hot_stats[7], 1ull);
+        }
+        return;
+    }
 
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
         hk[s] = G::kEmpty;
@@ -212,60 +304,124 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         __syncthreads();
     }
 
-    const uint64_t lo_item = n * blockIdx.x / gridDim.x, hi_item = n * (blockIdx.x + 1) / gridDim.x;
-    const uint64_t ntiles = (hi_item - lo_item + kTile - 1) / kTile;
     int qn = 0;
-    unsigned misses = 0;
-    for (;;) {
-        u32 t = 0;
-        if (lane == 0) t = atomicAdd(&s_next, 1u);
-        t = __shfl_sync(kFull, t, 0);
-        if (t >= ntiles) break;
-        const uint64_t base = lo_item + (uint64_t)t * kTile;
-        KeyT kx[kTileSlots];
-        i32 dx[kTileSlots];
-#pragma unroll
-        for (int u = 0; u < kTileSlots; ++u) {
-            const uint64_t i = base + u * 32 + lane;
-            const bool v = i < hi_item;
-            kx[u] = v ? ld_nc(keys + i) : G::kEmpty;
-            dx[u] = v ? load_w32<WK>(w, i) : 0;
+    unsigned misses = 0, direct = 0;
+    unsigned long long wbase = 0;  // this warp's reserved miss-buffer slots [wbase + wfill, wbase + kMissChunk)
+    uint32_t wfill = kMissChunk;
+    // one item: hot-table hit -> shared accumulation; miss -> the warp's queue,
+    // and a full queue of 32 -> the miss buffer (warp-uniform call)
+    auto item = [&](KeyT key, i32 d, bool valid) {
+        // both slots probed speculatively (no divergent second probe); a key never
+        // sits in its slot2 unless its slot1 was taken first, so this is exact
+        const u32 h1 = slot1<G::kLog2>(key), h2 = slot2<G::kLog2>(key);
+        const KeyT c1 = hk[h1], c2 = hk[h2];
+        const u32 h = c1 == key ? h1 : h2;
+        const bool hit = valid && (c1 == key || c2 == key) && key != G::kEmpty;
+        if (hit) hot_accumulate(lo, hi, h, d);
+        const bool miss = valid && !hit;
+        const unsigned m = __ballot_sync(kFull, miss);
+        if (miss) {
+            const int pos = qn + __popc(m & ((1u << lane) - 1));
+            wqk[pos] = key;
+            wqd[pos] = d;
         }
-#pragma unroll
-        for (int u = 0; u < kTileSlots; ++u) {
-            const bool valid = base + u * 32 + lane < hi_item;
-            const KeyT key = kx[u];
-            u32 h = slot1<G::kLog2>(key);
-            KeyT cur = hk[h];
-            if (cur != key && cur != G::kEmpty) {
-                h = slot2<G::kLog2>(key);
-                cur = hk[h];
-            }
-            const bool hit = cur == key && key != G::kEmpty;
-            if (hit) hot_accumulate(lo, hi, h, dx[u]);
-            const bool miss = valid && !hit;
-            const unsigned m = __ballot_sync(kFull, miss);
-            if (miss) {
-                const int pos = qn + __popc(m & ((1u << lane) - 1));
-                wqk[pos] = key;
-                wqd[pos] = dx[u];
-            }
-            qn += __popc(m);
-            misses += __popc(m);
+        qn += __popc(m);
+        misses += __popc(m);
+        if (qn >= 32 && mb.cap == 0) {  // a full warp of misses -> hash, split, red.global
             __syncwarp();
-            if (qn >= 32) {  // a full warp of misses
-                process_item<MODE, K, GLOBAL>(sp, (u64)wqk[lane], (i64)wqd[lane], nullptr, table);
-                __syncwarp();
-                if (lane < qn - 32) {
-                    wqk[lane] = wqk[32 + lane];
-                    wqd[lane] = wqd[32 + lane];
-                }
-                __syncwarp();
-                qn -= 32;
+            misses_direct<MODE, K, KeyT>(sp, wqk[lane], wqd[lane], true, table);
+            direct += sp.rows;
+            __syncwarp();
+            if (lane < qn - 32) {
+                wqk[lane] = wqk[32 + lane];
+                wqd[lane] = wqd[32 + lane];
             }
+            __syncwarp();
+            qn -= 32;
+        } else if (qn >= 32) {  // a full warp of misses -> 32 slots of the miss buffer
+            __syncwarp();
+            if (wfill == kMissChunk) {
+                if (lane == 0) wbase = atomicAdd(mb.count, (unsigned long long)kMissChunk);
+                wbase = __shfl_sync(kFull, wbase, 0);
+                wfill = 0;
+            }
+            const unsigned long long pos = wbase + wfill;
+            wfill += 32;
+            if (pos + 32 <= mb.cap) {
+                mb.keys[pos + lane] = wqk[lane];
+                mb.deltas[pos + lane] = wqd[lane];
+            } else {
+                misses_direct<MODE, K, KeyT>(sp, wqk[lane], wqd[lane], true, table);
+                direct += sp.rows;
+            }
+            __syncwarp();
+            if (lane < qn - 32) {
+                wqk[lane] = wqk[32 + lane];
+                wqd[lane] = wqd[32 + lane];
+            }
+            __syncwarp();
+            qn -= 32;
+        }
+    };
+
+    // full tiles, pulled dynamically from a shared counter; the next tile's
+    // vectors are in flight while the current one is processed
+    const uint64_t ntiles = t_hi - t_lo;
+    KV kv[kVT];
+    WVec<kV, WK> wv[kVT];
+    u32 t = 0;
+    if (lane == 0) t = atomicAdd(&s_next, 1u);
+    t = __shfl_sync(kFull, t, 0);
+    if (t < ntiles) {
+        const uint64_t b = (t_lo + t) * kT;
+#pragma unroll
+        for (int v = 0; v < kVT; ++v) {
+            const uint64_t i = b + (uint64_t)v * 32 * kV + lane * kV;
+            kv[v].load(keys + i);
+            wv[v].load(w, i);
         }
     }
-    if (lane < qn) process_item<MODE, K, GLOBAL>(sp, (u64)wqk[lane], (i64)wqd[lane], nullptr, table);
+    while (t < ntiles) {
+        u32 tn = 0;
+        if (lane == 0) tn = atomicAdd(&s_next, 1u);
+        tn = __shfl_sync(kFull, tn, 0);
+        KV kn[kVT];
+        WVec<kV, WK> wn[kVT];
+        if (tn < ntiles) {
+            const uint64_t b = (t_lo + tn) * kT;
+#pragma unroll
+            for (int v = 0; v < kVT; ++v) {
+                const uint64_t i = b + (uint64_t)v * 32 * kV + lane * kV;
+                kn[v].load(keys + i);
+                wn[v].load(w, i);
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < kVT; ++v)
+#pragma unroll
+            for (int e = 0; e < kV; ++e) item(kv[v][e], wv[v].d[e], true);
+#pragma unroll
+        for (int v = 0; v < kVT; ++v) {
+            kv[v] = kn[v];
+            wv[v] = wn[v];
+        }
+        t = tn;
+    }
+    // this CTA's tail share: scalar loads
+    for (uint64_t b = tail_lo + (uint64_t)warp * 32; b < tail_hi; b += (uint64_t)kHotWarps * 32) {
+        const uint64_t i = b + lane;
+        const bool v = i < tail_hi;
+        item(v ? ld_nc(keys + i) : G::kEmpty, v ? load_w32<WK>(w, i) : 0, v);
+    }
+    if (lane < qn) {
+        misses_direct<MODE, K, KeyT>(sp, wqk[lane], wqd[lane], true, table);
+        direct += sp.rows;
+    }
+    // unused reserved slots become no-op items (delta 0)
+    for (unsigned long long p = wbase + wfill + lane; p < wbase + kMissChunk && p < mb.cap; p += 32) {
+        mb.keys[p] = 0;
+        mb.deltas[p] = 0;
+    }
     __syncthreads();
     unsigned flushed = 0;
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
@@ -278,50 +434,446 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     }
     // instrumentation for the L2-reduction roofline (mb200_hot_stats)
     if (lane == 0) atomicAdd(&g_hot_stats[1], (unsigned long long)misses);
+    direct = __reduce_add_sync(kFull, direct);
+    if (lane == 0 && direct) atomicAdd(&g_hot_stats[5], (unsigned long long)direct);
     flushed = __reduce_add_sync(kFull, flushed);
     if (lane == 0) atomicAdd(&g_hot_stats[2], (unsigned long long)flushed);
     if (threadIdx.x == 0) {
-        atomicAdd(&g_hot_stats[0], (unsigned long long)(hi_item - lo_item));
+        atomicAdd(&g_hot_stats[0], (unsigned long long)((t_hi - t_lo) * kT + (tail_hi - tail_lo)));
         atomicAdd(&g_hot_stats[3], (unsigned long long)nhot);
     }
+}
+
+// ---- passes 4 and 5: binned row updates ------------------------------------
+// A bin is one row (or a 65536-cell slice of a wider row).  Entry = cell
+// (16 bits) | signed delta (16 bits) << 16; 0 is a no-op (padding).
+constexpr uint32_t kCellLog2 = 16;
+constexpr i32 kDeltaLim = 1 << 15;
+constexpr int kBinThreads = 1024;
+constexpr uint32_t kMaxBins = 64;
+constexpr size_t kStageBytes = 200 * 1024;
+constexpr uint64_t kMinBinChunk = 1ull << 26;  // items binned per (pass 4, pass 5) round trip
+constexpr uint32_t kMaxChunks = 8;
+constexpr int kAccThreads = 1024;
+enum SplitC { SPC_POW2 = 0, SPC_TFO = 1, SPC_ANY = 2 };  // compile-time splitter of the binned path
+
+struct BinGeom {
+    u32* bins;                 // [nb][cap] 4-byte entries
+    unsigned long long* gcnt;  // [chunks][nb] entries appended (may exceed cap)
+    uint64_t cap;              // entries per bin, multiple of 4
+    uint64_t width;
+    uint32_t nb, bpr;          // bins, bins per row
+    uint32_t cell_log2;        // log2 cells per bin (<= 16)
+    uint32_t cap_s;            // staged entries per bin per round, multiple of 4
+    uint32_t groups;           // 4-item groups per thread per round
+};
+
+__device__ __forceinline__ u32 make_entry(u32 cell, i32 d) { return cell | ((u32)d << kCellLog2); }
+__device__ __forceinline__ void apply_entry_direct(const BinGeom& g, i64* table, u32 bin, u32 e) {
+    if (!e) return;
+    const u32 row = bin / g.bpr;
+    const u64 idx = ((u64)(bin % g.bpr) << g.cell_log2) | (e & 0xffffu);
+    red_add_u64(reinterpret_cast<uint64_t*>(table) + (u64)row * g.width + idx, (u64)(i64)((i32)e >> kCellLog2));
+}
+
+// Appends one row update per lane (warp-uniform call).  Lanes that target the
+// same bin form one group (one ballot per bin-index bit; none when a row is
+// one bin, ONEBIN) and one lane reserves the group's staging slots with ONE
+// shared atomic -- per-lane atomics on a handful of counters serialise.
+template <bool ONEBIN>
+struct BinSink {
+    const BinGeom& g;
+    u32* stage;
+    u32* scnt;
+    i64* table;
+    unsigned& direct;
+    uint32_t sub_bits;  // ceil(log2(bins per row))
+    __device__ __forceinline__ void operator()(u32 row, u32 idx, bool neg, i32 d, bool active) {
+        active = active && d != 0;  // delta 0 adds nothing (sketch.cpp:136-138)
+        const bool fits = active && (u32)(d + (kDeltaLim - 1)) < (u32)(2 * kDeltaLim - 1);  // |d| < 2^15
+        const int lane = threadIdx.x & 31;
+        unsigned peers = __ballot_sync(kFull, fits);
+        u32 bin, base = 0;
+        if (ONEBIN) {
+            bin = row;
+            if (lane == 0 && peers) base = atomicAdd(scnt + bin, (u32)__popc(peers));
+            base = __shfl_sync(kFull, base, 0);
+        } else {
+            const u32 sub = idx >> g.cell_log2;
+            for (uint32_t bit = 0; bit < sub_bits; ++bit) {
+                const bool set = (sub >> bit) & 1;
+                const unsigned m = __ballot_sync(kFull, set);
+                peers &= set ? m : ~m;
+            }
+            bin = row * g.bpr + sub;
+            const int leader = __ffs(peers) - 1;
+            if (fits && lane == leader) base = atomicAdd(scnt + bin, (u32)__popc(peers));
+            base = __shfl_sync(kFull, base, fits ? leader : lane);
+        }
+        const u32 slot = base + __popc(peers & ((1u << lane) - 1));
+        if (fits && slot < g.cap_s) {
+            stage[bin * g.cap_s + slot] = make_entry(idx & ((1u << g.cell_log2) - 1), neg ? -d : d);
+        } else if (active) {
+            const u64 sd = (u64)(i64)d;
+            red_add_u64(reinterpret_cast<uint64_t*>(table) + (u64)row * g.width + idx, neg ? 0ull - sd : sd);
+            ++direct;
+        }
+    }
+};
+
+// bucket index (< 2^22 on the binned path) and sign of sub-row s, splitter known
+// at compile time where it is Pow2 / two-for-one (sketch.cpp:13-19)
+template <int MODE, int SPL>
+__device__ __forceinline__ u32 split_c(const SketchParams& sp, u64 hlo, u64 hhi, uint32_t s, bool& neg) {
+    if (MODE == M89) return (u32)split89(sp, hlo, hhi, s, neg);
+    if (MODE != MGEN && SPL == SPC_POW2) {  // b = 61: sign = bit 60, index = low bits
+        neg = (hi32(hlo) >> 28) & 1;
+        return lo32(hlo) & (u32)(sp.width - 1);
+    }
+    if (MODE != MGEN && SPL == SPC_TFO) {
+        neg = (hlo >> (60 - s)) & 1;
+        return (u32)(hlo >> (sp.lw * s)) & (u32)(sp.width - 1);
+    }
+    return (u32)split_small(sp, hlo, s, neg);
+}
+
+// U items: per family the U Horner chains are interleaved, then every sub-row
+// of every item goes to the sink (same arithmetic as process_item); warp-uniform.
+template <int MODE, int K, int SPL, int U, typename Sink>
+__device__ __forceinline__ void emit_items(const SketchParams& sp, const u64 (&x)[U], const i32 (&d)[U],
+                                           unsigned valid, Sink& sink) {
+    const uint32_t subs = (SPL == SPC_TFO || (SPL == SPC_ANY && sp.splitter == SPLIT_TWO_FOR_ONE)) ? 2 : 1;
+#pragma unroll 1
+    for (uint32_t f = 0; f < sp.families; ++f) {
+        u64 hlo[U], hhi[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (MODE == M89) hash89<K>(sp, f, x[u], hlo[u], hhi[u]);
+            else hlo[u] = hash_small<MODE, K>(sp, f, x[u]);
+        }
+        for (uint32_t s = 0; s < subs; ++s) {
+            const uint32_t row = subs * f + s;
+            if (row >= sp.rows) break;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                bool neg;
+                const u32 idx = split_c<MODE, SPL>(sp, hlo[u], hhi[u], s, neg);
+                sink(row, idx, neg, d[u], (valid >> u) & 1);
+            }
+        }
+    }
+}
+
+// Pass 4.  RAW: the batch itself (raw mode); else the miss buffer.  Chunk c
+// covers items [c * chunk_items, (c + 1) * chunk_items) of that source.
+template <int MODE, int K, int SPL, typename KeyT, int WK, bool RAW, bool ONEBIN>
+__global__ void __launch_bounds__(kBinThreads, 1)
+    cs_bin_kernel(const SketchParams sp, const BinGeom g, const KeyT* __restrict__ keys, const void* __restrict__ w,
+                  uint64_t n, const MissBuf<KeyT> mb, const u32* __restrict__ hot_sum, uint32_t sample,
+                  uint32_t chunk, uint64_t chunk_items, i64* __restrict__ table) {
+    if (raw_mode(hot_sum, sample) != RAW) return;
+    const uint64_t total = RAW ? n : min((uint64_t)*mb.count, mb.cap);
+    const uint64_t c0 = (uint64_t)chunk * chunk_items;
+    if (c0 >= total) return;
+    const uint64_t len = min(total - c0, chunk_items);
+    const uint64_t lo = c0 + len * blockIdx.x / gridDim.x, hi = c0 + len * (blockIdx.x + 1) / gridDim.x;
+    extern __shared__ __align__(16) u32 stage[];
+    __shared__ u32 scnt[kMaxBins], sc4[kMaxBins];
+    __shared__ unsigned long long spos[kMaxBins];
+    for (u32 b = threadIdx.x; b < g.nb; b += kBinThreads) scnt[b] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned direct = 0, written = 0;
+    uint32_t sub_bits = 0;
+    while ((1u << sub_bits) < g.bpr) ++sub_bits;
+    BinSink<ONEBIN> sink{g, stage, scnt, table, direct, sub_bits};
+    const uint64_t per_round = (uint64_t)kBinThreads * 4 * g.groups;
+    for (uint64_t base = lo; base < hi; base += per_round) {
+#pragma unroll 1
+        for (uint32_t gi = 0; gi < g.groups; ++gi) {
+            u64 kx[4];
+            i32 dx[4];
+            unsigned valid = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t i = base + (uint64_t)(gi * 4 + u) * kBinThreads + threadIdx.x;
+                const bool v = i < hi;
+                valid |= (v ? 1u : 0u) << u;
+                if (RAW) {
+                    kx[u] = v ? (u64)ld_nc(keys + i) : 0;
+                    dx[u] = v ? load_w32<WK>(w, i) : 0;
+                } else {
+                    kx[u] = v ? (u64)ld_nc(mb.keys + i) : 0;
+                    dx[u] = v ? ld_nc(mb.deltas + i) : 0;
+                }
+            }
+            emit_items<MODE, K, SPL, 4>(sp, kx, dx, valid, sink);
+        }
+        __syncthreads();
+        // flush: pad each bin to whole 16-byte groups, reserve its HBM range with
+        // one atomic, then all threads copy every bin in 16-byte groups
+        if ((u32)warp < g.nb) {
+            u32* st = stage + warp * g.cap_s;
+            const u32 c = min(scnt[warp], g.cap_s);
+            const u32 c4 = (c + 3) & ~3u;
+            if ((u32)lane < c4 - c) st[c + lane] = 0;
+            if (lane == 0) {
+                sc4[warp] = c4;
+                spos[warp] = c4 ? atomicAdd(g.gcnt + (uint64_t)chunk * g.nb + warp, (unsigned long long)c4) : 0;
+            }
+        }
+        __syncthreads();
+        for (u32 bin = 0; bin < g.nb; ++bin) {
+            const u32 c4 = sc4[bin];
+            const unsigned long long pos = spos[bin];
+            const u32* st = stage + bin * g.cap_s;
+            u32* dst = g.bins + (uint64_t)bin * g.cap;
+            for (u32 j = threadIdx.x * 4; j < c4; j += 4 * kBinThreads) {
+                const uint4 v = *reinterpret_cast<const uint4*>(st + j);
+                if (pos + j + 4 <= g.cap) {
+                    *reinterpret_cast<uint4*>(dst + pos + j) = v;
+                    written += 4;
+                } else {
+                    apply_entry_direct(g, table, bin, v.x);
+                    apply_entry_direct(g, table, bin, v.y);
+                    apply_entry_direct(g, table, bin, v.z);
+                    apply_entry_direct(g, table, bin, v.w);
+                    direct += 4;
+                }
+            }
+        }
+        __syncthreads();
+        for (u32 b = threadIdx.x; b < g.nb; b += kBinThreads) scnt[b] = 0;
+        __syncthreads();
+    }
+    direct = __reduce_add_sync(kFull, direct);
+    written = __reduce_add_sync(kFull, written);
+    if (lane == 0 && direct) atomicAdd(&g_hot_stats[5], (unsigned long long)direct);
+    if (lane == 0 && written) atomicAdd(&g_hot_stats[4], (unsigned long long)written);
+}
+
+// Exact accumulation into two 16-bit cells per 32-bit word (each 2^15-biased).
+// The 32-bit atomic returns the word before the add, so every add knows the
+// cell's 16-bit value before and after it: a value that leaves [0, 2^16) is
+// recorded as +-2^16 straight into the L2 table (rare for small signed
+// deltas).  A low-cell carry/borrow into the high cell is undone by a second
+// atomic whose own wrap is recorded the same way; per cell, displayed value +
+// 2^16 * (recorded wraps) = bias + sum of its deltas, exactly.
+__device__ __forceinline__ void wrap16(uint64_t* row, u32 cell, i32 nv) {
+    if (nv < 0 || nv > 0xffff) red_add_u64(row + cell, nv < 0 ? 0ull - 65536ull : 65536ull);
+}
+__device__ __forceinline__ void packed_add(u32* words, uint64_t* row, u32 cell, i32 d) {
+    u32* w = words + (cell >> 1);
+    if (cell & 1) {
+        const u32 old = atomicAdd(w, (u32)d << 16);
+        wrap16(row, cell, (i32)(old >> 16) + d);
+    } else {
+        const u32 old = atomicAdd(w, (u32)d);  // sign-extended: carries/borrows into the high cell
+        const i32 nl = (i32)(old & 0xffffu) + d;
+        if (nl < 0 || nl > 0xffff) {
+            const i32 c = nl < 0 ? -1 : 1;
+            red_add_u64(row + cell, (u64)(i64)(c * 65536));
+            wrap16(row, cell + 1, (i32)(old >> 16) + c);      // the carry's effect on the high cell
+            const u32 o2 = atomicAdd(w, (u32)(-c) << 16);     // ...undone
+            wrap16(row, cell + 1, (i32)(o2 >> 16) - c);
+        }
+    }
+}
+
+// Pass 5: CTA (bin, part) sums a slice of its bin's entries in the packed
+// shared table and merges the cells into the L2 table.
+__global__ void __launch_bounds__(kAccThreads)
+    cs_accum_kernel(const BinGeom g, uint32_t chunk, uint32_t parts, i64* __restrict__ table) {
+    const u32 bin = blockIdx.x / parts, part = blockIdx.x % parts;
+    const uint64_t cnt = min((uint64_t)g.gcnt[(uint64_t)chunk * g.nb + bin], g.cap);
+    const uint64_t q = cnt / 4, q0 = q * part / parts, q1 = q * (part + 1) / parts;
+    if (q0 == q1) return;
+    extern __shared__ __align__(16) u32 words[];
+    const u32 cells = 1u << g.cell_log2, nw = (cells + 1) / 2;
+    for (u32 c = threadIdx.x; c < nw; c += kAccThreads) words[c] = 0x80008000u;
+    __syncthreads();
+    const u32 row = bin / g.bpr;
+    const u64 col0 = (u64)(bin % g.bpr) << g.cell_log2;
+    uint64_t* dst = reinterpret_cast<uint64_t*>(table) + (u64)row * g.width + col0;
+    const uint4* src = reinterpret_cast<const uint4*>(g.bins + (uint64_t)bin * g.cap);
+    uint64_t i = q0 + threadIdx.x;
+    for (; i + 3 * kAccThreads < q1; i += 4 * kAccThreads) {  // four 16-byte loads in flight
+        uint4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = ld_stream(src + i + k * kAccThreads);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const u32 e[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (e[t]) packed_add(words, dst, e[t] & 0xffffu, (i32)e[t] >> kCellLog2);
+        }
+    }
+    for (; i < q1; i += kAccThreads) {
+        const uint4 v = ld_stream(src + i);
+        const u32 e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (e[t]) packed_add(words, dst, e[t] & 0xffffu, (i32)e[t] >> kCellLog2);
+    }
+    __syncthreads();
+    unsigned merged = 0;
+    for (u32 c = threadIdx.x; c < cells; c += kAccThreads) {
+        const i64 v = (i64)((words[c >> 1] >> ((c & 1) * 16)) & 0xffffu) - 0x8000;
+        if (v) {  // cells past the row end never receive entries
+            red_add_u64(dst + c, (u64)v);
+            ++merged;
+        }
+    }
+    merged = __reduce_add_sync(kFull, merged);
+    if ((threadIdx.x & 31) == 0 && merged) atomicAdd(&g_hot_stats[6], (unsigned long long)merged);
+}
+
+inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+// large-table strategy (mb200_set_large_table_strategy): misses either go
+// straight to L2 (fire-and-forget reductions, overlapped with the hot-key work;
+// measured fastest on configs 4 and 5) or through the binned passes 4-5
+int g_strategy = STRAT_DIRECT;
+
+// Buffers of one call, carved from one stream-ordered allocation (the pool keeps
+// its memory between calls, retain_pool).
+template <typename KeyT>
+struct HotPlan {
+    BinGeom g{};
+    uint32_t m = 0;            // sample size
+    uint32_t chunks = 0;       // (pass 4, pass 5) round trips
+    uint64_t chunk_items = 0;  // items per round trip
+    uint64_t cap_m = 0;        // miss-buffer capacity
+    size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, hot_bytes = 0, mk_bytes = 0, md_bytes = 0,
+           bin_bytes = 0;
+    size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes; }  // tc .. gcnt are contiguous
+    size_t total() const { return tk_bytes + zero_bytes() + hot_bytes + mk_bytes + md_bytes + bin_bytes; }
+};
+
+template <typename KeyT>
+HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
+    using G = HotGeom<KeyT>;
+    HotPlan<KeyT> P;
+    P.m = (uint32_t)(n < kHotSample ? n : kHotSample);
+    BinGeom& g = P.g;
+    // bin geometry: rows x ceil(width / 8192) bins of <= 8192 cells
+    g.width = sp.width;
+    uint32_t cl = 0;
+    while ((1ull << cl) < sp.width && cl < kCellLog2) ++cl;
+    g.cell_log2 = cl;
+    const uint64_t bpr = (sp.width + (1ull << cl) - 1) >> cl;
+    const bool binned = g_strategy == STRAT_BINNED && (uint64_t)sp.rows * bpr <= kMaxBins;
+    g.bpr = (uint32_t)bpr;
+    g.nb = binned ? sp.rows * g.bpr : 0;
+    if (binned) {
+        // miss buffer: half the batch (the rest, if ever, goes straight to L2)
+        P.cap_m = (n / 2 + 31) & ~31ull;
+        const uint64_t src_max = n > P.cap_m ? n : P.cap_m;
+        P.chunk_items = (src_max + kMaxChunks - 1) / kMaxChunks;
+        if (P.chunk_items < kMinBinChunk) P.chunk_items = kMinBinChunk;
+        P.chunks = (uint32_t)((src_max + P.chunk_items - 1) / P.chunk_items);
+        const uint64_t per_chunk = src_max < P.chunk_items ? src_max : P.chunk_items;
+        // a bin receives ~rows * per_chunk / nb entries per chunk (hash bits are
+        // uniform); 25% margin + round padding, overflow goes straight to L2
+        g.cap = (((uint64_t)sp.rows * per_chunk / g.nb) * 5 / 4 + 4 * (uint64_t)kBinThreads + 4096) & ~3ull;
+        g.cap_s = (uint32_t)(kStageBytes / 4 / g.nb) & ~3u;
+        // 4-item groups per round so that a bin's expected share (4096 rows / nb
+        // entries per group) stays under ~85% of its staging buffer
+        const uint64_t grp = (uint64_t)g.cap_s * 17 / 20 * g.nb / ((uint64_t)kBinThreads * 4 * sp.rows);
+        g.groups = (uint32_t)(grp < 1 ? 1 : grp > 16 ? 16 : grp);
+    }
+    P.tk_bytes = align256((size_t)kCountSlots * sizeof(KeyT));
+    P.tc_bytes = (size_t)kCountSlots * 4;
+    P.misc = 256 * 4 + 64;  // hist[256], hot_count, hot_sum, miss count (u64)
+    P.gcnt_bytes = align256((size_t)P.chunks * g.nb * 8 + 8);
+    P.hot_bytes = align256((size_t)G::kCap * (sizeof(KeyT) + 4));
+    P.mk_bytes = align256((size_t)P.cap_m * sizeof(KeyT));
+    P.md_bytes = align256((size_t)P.cap_m * 4);
+    P.bin_bytes = (size_t)g.nb * g.cap * 4;
+    return P;
+}
+
+template <int MODE, int K, int SPL, typename KeyT, int WK>
+cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uint64_t n, int64_t* table,
+                    cudaStream_t s, unsigned char* ws, HotPlan<KeyT> P) {
+    using G = HotGeom<KeyT>;
+    const int sms = sm_count();
+    BinGeom& g = P.g;
+    const bool binned = g.nb != 0;
+    KeyT* tk = reinterpret_cast<KeyT*>(ws);
+    u32* tc = reinterpret_cast<u32*>(ws + P.tk_bytes);
+    u32* hist = tc + kCountSlots;
+    u32* hot_count = hist + 256;
+    u32* hot_sum = hot_count + 1;
+    unsigned long long* mcount = reinterpret_cast<unsigned long long*>(hot_count + 2);
+    g.gcnt = reinterpret_cast<unsigned long long*>(ws + P.tk_bytes + P.tc_bytes + P.misc);
+    unsigned char* p = ws + P.tk_bytes + P.zero_bytes();
+    KeyT* hot = reinterpret_cast<KeyT*>(p);
+    u32* hot_cnt = reinterpret_cast<u32*>(hot + G::kCap);
+    p += P.hot_bytes;
+    const MissBuf<KeyT> mb{reinterpret_cast<KeyT*>(p), reinterpret_cast<i32*>(p + P.mk_bytes), mcount, P.cap_m};
+    p += P.mk_bytes + P.md_bytes;
+    g.bins = reinterpret_cast<u32*>(p);
+    cudaMemsetAsync(tk, 0xff, P.tk_bytes, s);
+    cudaMemsetAsync(tc, 0, P.zero_bytes(), s);
+    hh_count_kernel<KeyT><<<sms * 4, 256, 0, s>>>(keys, P.m, tk, tc);
+    hh_hist_kernel<<<sms, 256, 0, s>>>(tc, hist);
+    hh_select_kernel<KeyT><<<sms, 256, 0, s>>>(tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum);
+    auto fn = cs_hot_kernel<MODE, K, KeyT, WK>;
+    const size_t smem = ((size_t)sizeof(KeyT) + 8) << G::kLog2;
+    const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes));
+    if (e != cudaSuccess) return e;
+    uint64_t grid = (n + 256 * kHotWarps - 1) / (256 * kHotWarps);
+    if (grid > (uint64_t)sms) grid = sms;
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(keys) & 15) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
+    // without bins (cap 0) every miss takes the direct path and raw mode is off
+    fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, hot, hot_cnt, hot_count, hot_sum,
+                                                          binned ? P.m : 0, mb, vec_ok);
+    if ((e = cudaGetLastError()) != cudaSuccess || !binned) return e;
+    auto fb_raw = g.bpr == 1 ? cs_bin_kernel<MODE, K, SPL, KeyT, WK, true, true>
+                             : cs_bin_kernel<MODE, K, SPL, KeyT, WK, true, false>;
+    auto fb_miss = g.bpr == 1 ? cs_bin_kernel<MODE, K, SPL, KeyT, W_I32, false, true>
+                              : cs_bin_kernel<MODE, K, SPL, KeyT, W_I32, false, false>;
+    const size_t sbytes = (size_t)g.nb * g.cap_s * 4;
+    if ((e = cudaFuncSetAttribute(fb_raw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(fb_miss, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes)) != cudaSuccess)
+        return e;
+    const size_t abytes = (size_t)4 * (((1u << g.cell_log2) + 1) / 2);
+    if ((e = cudaFuncSetAttribute(cs_accum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 << kCellLog2)) !=
+        cudaSuccess)
+        return e;
+    // one wave: 1024-thread CTAs, up to 2 per SM when the cell table is small
+    const uint32_t per_sm = abytes <= 96 * 1024 ? 2 : 1;
+    const uint32_t parts = (uint32_t)(per_sm * sms / g.nb > 0 ? per_sm * sms / g.nb : 1);
+    for (uint32_t c = 0; c < P.chunks; ++c) {
+        if ((uint64_t)c * P.chunk_items < n)
+            fb_raw<<<sms, kBinThreads, sbytes, s>>>(sp, g, keys, w, n, mb, hot_sum, P.m, c, P.chunk_items, table);
+        if ((uint64_t)c * P.chunk_items < P.cap_m)
+            fb_miss<<<sms, kBinThreads, sbytes, s>>>(sp, g, keys, w, n, mb, hot_sum, P.m, c, P.chunk_items, table);
+        cs_accum_kernel<<<g.nb * parts, kAccThreads, abytes, s>>>(g, c, parts, table);
+    }
+    return cudaGetLastError();
 }
 
 template <int MODE, int K, typename KeyT, int WK>
 cudaError_t launch_hot(const SketchParams& sp, const void* keys, const void* w, uint64_t n, int64_t* table,
                        cudaStream_t s) {
-    using G = HotGeom<KeyT>;
-    const uint64_t m = n < kHotSample ? n : kHotSample;
-    const size_t tk_bytes = (size_t)kCountSlots * sizeof(KeyT), tc_bytes = (size_t)kCountSlots * 4;
-    const size_t misc = 256 * 4 + 16;
-    const size_t hot_bytes = (size_t)G::kCap * (sizeof(KeyT) + 4);
+    const HotPlan<KeyT> P = plan_hot<KeyT>(sp, n);
     unsigned char* ws = nullptr;
-    cudaError_t e = cudaMallocAsync(&ws, tk_bytes + tc_bytes + misc + hot_bytes, s);
+    cudaError_t e = cudaMallocAsync(&ws, P.total(), s);
     if (e != cudaSuccess) return e;
-    KeyT* tk = reinterpret_cast<KeyT*>(ws);
-    u32* tc = reinterpret_cast<u32*>(ws + tk_bytes);
-    u32* hist = tc + kCountSlots;
-    u32* hot_count = hist + 256;
-    KeyT* hot = reinterpret_cast<KeyT*>(ws + tk_bytes + tc_bytes + misc);
-    u32* hot_cnt = reinterpret_cast<u32*>(hot + G::kCap);
-    cudaMemsetAsync(tk, 0xff, tk_bytes, s);
-    cudaMemsetAsync(tc, 0, tc_bytes + misc, s);
-    const int sms = sm_count();
-    hh_count_kernel<KeyT><<<sms * 4, 256, 0, s>>>(reinterpret_cast<const KeyT*>(keys), m, tk, tc);
-    hh_hist_kernel<<<sms, 256, 0, s>>>(tc, hist);
-    hh_select_kernel<KeyT><<<sms, 256, 0, s>>>(tk, tc, hist, G::kCap, hot, hot_cnt, hot_count);
-    auto fn = cs_hot_kernel<MODE, K, KeyT, WK>;
-    const size_t smem = ((size_t)sizeof(KeyT) + 8) << G::kLog2;
-    const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes));
-    if (e == cudaSuccess) {
-        uint64_t grid = (n + kTile * kHotWarps - 1) / (kTile * kHotWarps);
-        if (grid > (uint64_t)sms) grid = sms;
-        fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, reinterpret_cast<const KeyT*>(keys), w, n, table,
-                                                              hot, hot_cnt, hot_count);
-        e = cudaGetLastError();
-    }
-    cudaFreeAsync(ws, s);
-    return e;
+    const KeyT* kk = reinterpret_cast<const KeyT*>(keys);
+    if (MODE != MGEN && sp.splitter == SPLIT_POW2)
+        e = run_hot<MODE, K, SPC_POW2, KeyT, WK>(sp, kk, w, n, table, s, ws, P);
+    else if (MODE != MGEN && sp.splitter == SPLIT_TWO_FOR_ONE)
+        e = run_hot<MODE, K, SPC_TFO, KeyT, WK>(sp, kk, w, n, table, s, ws, P);
+    else
+        e = run_hot<MODE, K, SPC_ANY, KeyT, WK>(sp, kk, w, n, table, s, ws, P);
+    const cudaError_t e2 = cudaFreeAsync(ws, s);
+    return e != cudaSuccess ? e : e2;
 }
 
 template <int MODE, typename KeyT>
@@ -352,6 +904,13 @@ void retain_pool() {
 }
 
 }  // namespace
+
+int set_large_table_strategy(int s) {
+    if (s != STRAT_DIRECT && s != STRAT_BINNED) return -1;
+    const int old = g_strategy;
+    g_strategy = s;
+    return old;
+}
 
 cudaError_t hot_stats(uint64_t out[8], bool reset) {
     cudaError_t e = cudaDeviceSynchronize();

@@ -31,13 +31,34 @@ __device__ __forceinline__ u32 hi32(u64 v) { return (u32)(v >> 32); }
 // One Horner step y <- y x + a, lazily reduced:
 //   in  y < 2^63, x < 2^32, a < p
 //   out (yx & p) + (yx >> 61) + a  <  2^61 + 2^34 + 2^61  <  2^63   (closed)
-// Two limb products (IMAD.WIDE.U32), ~5 ALU ops.
+// Two limb products (IMAD.WIDE.U32) A = y0 x, B = y1 x; y x = A + B 2^32 with
+// bits 32..63 = A1 + B0 (carry c) and bits 64..94 = B1 + c < 2^31; the fold
+// and the add of a are two 32-bit carry chains (no 64-bit operand re-packing).
 __device__ __forceinline__ u64 h61_step32(u64 y, u32 x, u64 a) {
-    const u64 p0 = mulw(lo32(y), x);                 // bits 0..63 of y0 x
-    const u64 p1 = mulw(hi32(y), x) + (p0 >> 32);    // y x >> 32, < 2^63 + 2^32
-    const u64 lo = (((p1 << 32) | lo32(p0))) & kP61; // (y x) & p
-    const u64 hi = p1 >> 29;                         // (y x) >> 61
-    return lo + hi + a;
+    u64 r;
+    asm("{\n\t"
+        ".reg .u32 y0, y1, a0, a1, A0, A1, B0, B1, m, t, s0, s1, r0, r1;\n\t"
+        ".reg .u64 A, B;\n\t"
+        "mov.b64 {y0, y1}, %1;\n\t"
+        "mov.b64 {a0, a1}, %3;\n\t"
+        "mul.wide.u32 A, y0, %2;\n\t"
+        "mul.wide.u32 B, y1, %2;\n\t"
+        "mov.b64 {A0, A1}, A;\n\t"
+        "mov.b64 {B0, B1}, B;\n\t"
+        "add.cc.u32 m, A1, B0;\n\t"          // bits 32..63 of y x
+        "addc.u32 t, B1, 0;\n\t"             // bits 64..94
+        "shf.r.clamp.b32 s0, m, t, 29;\n\t"  // (y x) >> 61
+        "shr.u32 s1, t, 29;\n\t"
+        "and.b32 m, m, 0x1FFFFFFF;\n\t"      // (y x) & p, high word
+        "add.cc.u32 r0, A0, s0;\n\t"
+        "addc.u32 r1, m, s1;\n\t"
+        "add.cc.u32 r0, r0, a0;\n\t"
+        "addc.u32 r1, r1, a1;\n\t"
+        "mov.b64 %0, {r0, r1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(y), "r"(x), "l"(a));
+    return r;
 }
 
 // Full reduction of a lazily reduced value y < 2^63 to [0, p): one fold to

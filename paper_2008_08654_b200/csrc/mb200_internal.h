@@ -56,6 +56,8 @@ cudaError_t launch_cs_update(const SketchParams& sp, const void* keys, int key_w
 cudaError_t launch_cs_hot(const SketchParams& sp, const void* keys, int key_width, const void* w, int w_kind,
                           uint64_t n, int64_t* table, cudaStream_t s);
 cudaError_t hot_stats(uint64_t out[8], bool reset);
+enum LargeTableStrategy { STRAT_DIRECT = 0, STRAT_BINNED = 1 };
+int set_large_table_strategy(int s);  // returns the previous strategy, -1 if invalid
 cudaError_t launch_cs_moments(const int64_t* table, uint32_t rows, uint64_t width, uint64_t* out,
                               cudaStream_t s);
 cudaError_t launch_cs_merge(int64_t* dst, const int64_t* src, uint64_t count, cudaStream_t s);

@@ -348,11 +348,15 @@ HOT_CASES = [
 ]
 
 
+@pytest.mark.parametrize("strategy", ["direct", "binned"])
 @pytest.mark.parametrize("case", HOT_CASES, ids=[f"r{c[0]}b{c[2]}{c[5]}" for c in HOT_CASES])
-def test_hot_path_large_batches(cuda, mb, orc, case):
+def test_hot_path_large_batches(cuda, mb, orc, case, strategy):
+    """Both large-table strategies (misses -> L2 reductions, misses -> HBM bins summed
+    in shared memory) give the oracle's table bit for bit."""
     import torch
 
     rows, width, b, kb, sp, kind, wdt = case
+    prev = mb.set_large_table_strategy(mb.LARGE_BINNED if strategy == "binned" else mb.LARGE_DIRECT)
     spec, fams = make_spec(mb, orc, rows, width, b, kb, sp, 0xB16 + rows)
     n = (1 << 22) + 12345
     zk, zw = orc.gen_zipf_items(7, 0, n)
@@ -366,9 +370,22 @@ def test_hot_path_large_batches(cuda, mb, orc, case):
     if w is not None:
         w[:4] = [np.iinfo(np.int32).min, np.iinfo(np.int32).max, -1, 1]
     cnt = torch.zeros(rows * width, dtype=torch.int64, device="cuda")
-    mb.cs_update(spec, dev(keys), cnt, None if w is None else dev(w))
+    mb.hot_stats(reset=True)
+    try:
+        mb.cs_update(spec, dev(keys), cnt, None if w is None else dev(w))
+    finally:
+        mb.set_large_table_strategy(prev)
+    st = mb.hot_stats(reset=True)
     exp = orc.cs_process(rows, width, b, fams, kb, sp, keys, w)
     assert (cnt.cpu().numpy() == exp).all()
+    assert st["items"] == n
+    if strategy == "binned" and rows * -(-width // 65536) <= 64:
+        assert st["binned"] > 0  # the binned passes really ran
+
+
+def test_large_table_strategy_rejects_unknown(cuda, mb):
+    with pytest.raises(mb.InvalidArgument):
+        mb.set_large_table_strategy(7)
 
 
 @pytest.mark.parametrize("weight", [np.iinfo(np.int32).max, np.iinfo(np.int32).min])

@@ -26,11 +26,7 @@ int grid_for(uint64_t work_items, int per_sm) {
 
 template <int K>
 __device__ __forceinline__ u64 eval61_key64(const u64 (&a)[K], u64 x) {
-    x = h61_key64(x);
-    u64 y = a[K - 1];
-#pragma unroll
-    for (int i = K - 2; i >= 0; --i) y = h61_step64(y, x, a[i]);
-    return h61_finish(y);
+    return h61_finish(h61_eval64<K>(a, h61_key64(x)));
 }
 
 template <int K>

@@ -32,17 +32,16 @@ __device__ __forceinline__ u32 hi32(u64 v) { return (u32)(v >> 32); }
 //   in  y < 2^63, x < 2^32, a < p
 //   out (yx & p) + (yx >> 61) + a  <  2^61 + 2^34 + 2^61  <  2^63   (closed)
 // Two limb products (IMAD.WIDE.U32) A = y0 x, B = y1 x; y x = A + B 2^32 with
-// bits 32..63 = A1 + B0 (carry c) and bits 64..94 = B1 + c < 2^31; the fold
-// and the add of a are two 32-bit carry chains (no 64-bit operand re-packing).
+// bits 32..63 = A1 + B0 (carry c) and bits 64..94 = B1 + c < 2^31; the fold is
+// one carry chain, the three-term sum one 3-input add pair (IADD3, IADD3.X).
 __device__ __forceinline__ u64 h61_step32(u64 y, u32 x, u64 a) {
-    u64 r;
+    u64 lo, hi;
     asm("{\n\t"
-        ".reg .u32 y0, y1, a0, a1, A0, A1, B0, B1, m, t, s0, s1, r0, r1;\n\t"
+        ".reg .u32 y0, y1, A0, A1, B0, B1, m, t, s0, s1;\n\t"
         ".reg .u64 A, B;\n\t"
-        "mov.b64 {y0, y1}, %1;\n\t"
-        "mov.b64 {a0, a1}, %3;\n\t"
-        "mul.wide.u32 A, y0, %2;\n\t"
-        "mul.wide.u32 B, y1, %2;\n\t"
+        "mov.b64 {y0, y1}, %2;\n\t"
+        "mul.wide.u32 A, y0, %3;\n\t"
+        "mul.wide.u32 B, y1, %3;\n\t"
         "mov.b64 {A0, A1}, A;\n\t"
         "mov.b64 {B0, B1}, B;\n\t"
         "add.cc.u32 m, A1, B0;\n\t"          // bits 32..63 of y x
@@ -50,22 +49,20 @@ __device__ __forceinline__ u64 h61_step32(u64 y, u32 x, u64 a) {
         "shf.r.clamp.b32 s0, m, t, 29;\n\t"  // (y x) >> 61
         "shr.u32 s1, t, 29;\n\t"
         "and.b32 m, m, 0x1FFFFFFF;\n\t"      // (y x) & p, high word
-        "add.cc.u32 r0, A0, s0;\n\t"
-        "addc.u32 r1, m, s1;\n\t"
-        "add.cc.u32 r0, r0, a0;\n\t"
-        "addc.u32 r1, r1, a1;\n\t"
-        "mov.b64 %0, {r0, r1};\n\t"
+        "mov.b64 %0, {A0, m};\n\t"
+        "mov.b64 %1, {s0, s1};\n\t"
         "}"
-        : "=l"(r)
-        : "l"(y), "r"(x), "l"(a));
-    return r;
+        : "=l"(lo), "=l"(hi)
+        : "l"(y), "r"(x));
+    return lo + hi + a;
 }
 
-// Full reduction of a lazily reduced value y < 2^63 to [0, p): one fold to
-// < 2^61 + 4 < 2p, then the reference's branch-free finish
+// Full reduction of a lazily reduced value y < 2^64 to [0, p): one fold to
+// < 2^61 + 8 < 2p, then the reference's branch-free finish
 // z = (y + 1) >> b; (y + z) & p   (polyhash.cpp:74-75).
+__device__ __forceinline__ u64 h61_fold(u64 y) { return (y & kP61) + (y >> 61); }
 __device__ __forceinline__ u64 h61_finish(u64 y) {
-    y = (y & kP61) + (y >> 61);
+    y = h61_fold(y);
     const u64 z = (y + 1) >> 61;
     return (y + z) & kP61;
 }
@@ -73,23 +70,23 @@ __device__ __forceinline__ u64 h61_finish(u64 y) {
 // ---------------------------------------------------------------------------
 // p = 2^61 - 1, any 64-bit key (config 2 draws keys from [0, p), beyond the
 // reference's u <= 2^60 domain; SURVEY 7.3 hard part 2).  Keys are folded once
-// to x < 2^61 + 8; the step keeps y < 2^62 with a second (3-bit) fold:
-//   in  y < 2^62, x < 2^61 + 8, a < p;  y x < 2^123.02
-//   s = (yx & p) + (yx >> 61) + a < 2^63.02;  out (s & p) + (s >> 61) < 2^61 + 8
-// Four limb products.
+// to x <= 2^61 + 6 (x1 = x >> 32 <= 2^29).  One step, bound B on the input y:
+//   t = y x = P00 + M 2^32 + P11 2^64 with M = y0 x1 + y1 x0 < 2^61 + B (one
+//   64-bit mad.wide chain, valid while B < 7 * 2^61), P11 = y1 x1 <= 2^61;
+//   out s = (t & p) + (t >> 61) + a < B + 2^62 + 43.
+// So from y < 2^61 + 8 up to THREE steps run without the second fold (bound
+// after j steps: (2j + 1) 2^61 + 43 j < 7 * 2^61); h61_eval64 folds y before
+// every fourth.  Four limb products per step.
 __device__ __forceinline__ u64 h61_key64(u64 x) { return (x & kP61) + (x >> 61); }
+constexpr int kLazySteps = 3;
 
-// y x = P00 + (y0 x1 + y1 x0) 2^32 + P11 2^64 where the middle sum M < 2^63 fits
-// one 64-bit mad.wide (y1 < 2^30, x1 <= 2^29): four IMAD.WIDE.U32, no operand
-// re-packing, then the two folds on 32-bit limbs with carry chains.
 __device__ __forceinline__ u64 h61_step64(u64 y, u64 x, u64 a) {
-    u64 r;
+    u64 lo, hi;
     asm("{\n\t"
-        ".reg .u32 y0, y1, x0, x1, a0, a1, t0, t1, t2, t3, m0, m1, p0, p1, h0, h1, s0, s1, q;\n\t"
+        ".reg .u32 y0, y1, x0, x1, t0, t1, t2, t3, m0, m1, p0, p1, h0, h1;\n\t"
         ".reg .u64 P00, M, P11;\n\t"
-        "mov.b64 {y0, y1}, %1;\n\t"
-        "mov.b64 {x0, x1}, %2;\n\t"
-        "mov.b64 {a0, a1}, %3;\n\t"
+        "mov.b64 {y0, y1}, %2;\n\t"
+        "mov.b64 {x0, x1}, %3;\n\t"
         "mul.wide.u32 P00, y0, x0;\n\t"
         "mul.wide.u32 M, y0, x1;\n\t"
         "mad.wide.u32 M, y1, x0, M;\n\t"
@@ -103,19 +100,40 @@ __device__ __forceinline__ u64 h61_step64(u64 y, u64 x, u64 a) {
         "shf.r.clamp.b32 h0, t1, t2, 29;\n\t"  // t >> 61
         "shf.r.clamp.b32 h1, t2, t3, 29;\n\t"
         "and.b32 t1, t1, 0x1FFFFFFF;\n\t"      // t & p
-        "add.cc.u32 s0, t0, h0;\n\t"
-        "addc.u32 s1, t1, h1;\n\t"
-        "add.cc.u32 s0, s0, a0;\n\t"
-        "addc.u32 s1, s1, a1;\n\t"
-        "shr.u32 q, s1, 29;\n\t"                // second fold: (s & p) + (s >> 61)
-        "and.b32 s1, s1, 0x1FFFFFFF;\n\t"
-        "add.cc.u32 s0, s0, q;\n\t"
-        "addc.u32 s1, s1, 0;\n\t"
-        "mov.b64 %0, {s0, s1};\n\t"
+        "mov.b64 %0, {t0, t1};\n\t"
+        "mov.b64 %1, {h0, h1};\n\t"
         "}"
-        : "=l"(r)
-        : "l"(y), "l"(x), "l"(a));
-    return r;
+        : "=l"(lo), "=l"(hi)
+        : "l"(y), "l"(x));
+    return lo + hi + a;
+}
+
+// Horner over K (compile-time) coefficients, lowest first in c[]: leading
+// coefficient c[K-1] (polyhash.cpp:67-69), key already folded by h61_key64.
+template <int K>
+__device__ __forceinline__ u64 h61_eval64(const u64* c, u64 x) {
+    u64 y = c[K - 1];
+#pragma unroll
+    for (int i = K - 2; i >= 0; --i) {
+        if ((K - 2 - i) > 0 && (K - 2 - i) % kLazySteps == 0) y = h61_fold(y);
+        y = h61_step64(y, x, c[i]);
+    }
+    return y;
+}
+// runtime k
+__device__ __forceinline__ u64 h61_eval64_rt(const u64* c, int k, u64 x) {
+    u64 y = c[k - 1];
+    int lazy = 0;
+#pragma unroll 1
+    for (int i = k - 2; i >= 0; --i) {
+        if (lazy == kLazySteps) {
+            y = h61_fold(y);
+            lazy = 0;
+        }
+        y = h61_step64(y, x, c[i]);
+        ++lazy;
+    }
+    return y;
 }
 
 // ---------------------------------------------------------------------------

@@ -43,16 +43,8 @@ __device__ __forceinline__ u64 hash_small(const SketchParams& sp, uint32_t f, u6
         return h61_finish(y);
     } else if (MODE == M61_K64) {
         const u64 xr = h61_key64(x);
-        if (K > 0) {
-            u64 y = c[K - 1];
-#pragma unroll
-            for (int i = K - 2; i >= 0; --i) y = h61_step64(y, xr, c[i]);
-            return h61_finish(y);
-        }
-        u64 y = c[sp.k - 1];
-#pragma unroll 1
-        for (int i = (int)sp.k - 2; i >= 0; --i) y = h61_step64(y, xr, c[i]);
-        return h61_finish(y);
+        if (K > 0) return h61_finish(h61_eval64<K>(c, xr));
+        return h61_finish(h61_eval64_rt(c, (int)sp.k, xr));
     } else {
         u64 y = c[sp.k - 1];
 #pragma unroll 1

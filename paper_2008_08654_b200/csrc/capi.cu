@@ -375,8 +375,8 @@ int mb200_cs_update(const mb200_sketch_desc* desc, const void* d_keys, int key_w
     if (key_width != 32 && key_width != 64) return fail(MB200_INVALID_ARGUMENT, "key width must be 32 or 64");
     if (weight_kind != MB200_W_NONE && weight_kind != MB200_W_I32 && weight_kind != MB200_W_I64)
         return fail(MB200_INVALID_ARGUMENT, "unknown weight kind");
+    if (n == 0) return MB200_OK;  // an empty batch touches nothing (empty tensors may be null)
     if (weight_kind != MB200_W_NONE && !d_weights) return fail(MB200_INVALID_ARGUMENT, "null weights");
-    if (n == 0) return MB200_OK;
     if (!d_keys || !d_counters) return fail(MB200_INVALID_ARGUMENT, "null buffer");
     cudaStream_t s = (cudaStream_t)stream;
     if (int rc = check_keys(d_keys, key_width, n, desc->key_bits, s)) return rc;

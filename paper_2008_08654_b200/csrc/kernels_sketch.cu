@@ -144,6 +144,84 @@ __global__ void __launch_bounds__(kThreads) cs_update_kernel(const SketchParams 
     }
 }
 
+// ---- one row, Pow2 split, 32-bit keys, b = 61 (config 1's shape) ------------
+// Whole 16-byte vectors of 4 keys (and 4 weights) per lane, two in flight, no
+// per-item bounds checks; 1024-thread CTAs so the per-CTA merge of the private
+// table into HBM (one red.global per non-zero cell) stays small.
+constexpr int kSmallThreads = 1024;
+
+template <int K, int WK, int STRAT>
+__device__ __forceinline__ void small_vec(const SketchParams& sp, const u64* c, uint4 kv, const int4& wv,
+                                          void* smem) {
+    const u32 kk[4] = {kv.x, kv.y, kv.z, kv.w};
+    const i32 ww[4] = {wv.x, wv.y, wv.z, wv.w};
+    u64 y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) y[u] = c[K - 1];
+#pragma unroll
+    for (int i = K - 2; i >= 0; --i)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) y[u] = h61_step32(y[u], kk[u], c[i]);
+    const u32 mask = (u32)(sp.width - 1);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const u64 h = h61_finish(y[u]);  // < p: index = low bits, sign = bit 60 (sketch.cpp:13-19)
+        const u64 d = WK == W_NONE ? 1ull : (u64)(i64)ww[u];
+        table_add<STRAT>(smem, nullptr, lo32(h) & mask, ((hi32(h) >> 28) & 1) ? 0ull - d : d);
+    }
+}
+
+template <int K, int WK, int STRAT>
+__global__ void __launch_bounds__(kSmallThreads) cs_small_k32_kernel(const SketchParams sp,
+                                                                      const u32* __restrict__ keys,
+                                                                      const void* __restrict__ w, uint64_t n,
+                                                                      i64* __restrict__ table) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    void* smem = smem_raw;
+    const uint64_t cells = sp.width;
+    if (STRAT == SMEM_LOHI) {
+        for (uint64_t i = threadIdx.x; i < 2 * kLohiCells; i += kSmallThreads)
+            reinterpret_cast<u32*>(smem)[i] = i < kLohiCells ? 0x80000000u : 0u;
+    } else {
+        for (uint64_t i = threadIdx.x; i < cells; i += kSmallThreads) reinterpret_cast<u32*>(smem)[i] = 0;
+    }
+    u64 c[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) c[i] = sp.lo[i];
+    __syncthreads();
+    const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+    const int4* w4 = reinterpret_cast<const int4*>(w);
+    const uint64_t nv = n / 4, stride = (uint64_t)gridDim.x * kSmallThreads;
+    const int4 ones = make_int4(1, 1, 1, 1);
+    uint64_t i = (uint64_t)blockIdx.x * kSmallThreads + threadIdx.x;
+    for (; i + stride < nv; i += 2 * stride) {
+        const uint4 ka = ld_stream(k4 + i), kb = ld_stream(k4 + i + stride);
+        const int4 wa = WK == W_NONE ? ones : ld_stream(w4 + i);
+        const int4 wb = WK == W_NONE ? ones : ld_stream(w4 + i + stride);
+        small_vec<K, WK, STRAT>(sp, c, ka, wa, smem);
+        small_vec<K, WK, STRAT>(sp, c, kb, wb, smem);
+    }
+    if (i < nv) small_vec<K, WK, STRAT>(sp, c, ld_stream(k4 + i), WK == W_NONE ? ones : ld_stream(w4 + i), smem);
+    if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {  // the last n % 4 items
+        const uint64_t j = (n & ~3ull) + threadIdx.x;
+        u64 y = c[K - 1];
+#pragma unroll
+        for (int t = K - 2; t >= 0; --t) y = h61_step32(y, keys[j], c[t]);
+        const u64 h = h61_finish(y);
+        const u64 d = WK == W_NONE ? 1ull : (u64)(i64)reinterpret_cast<const i32*>(w)[j];
+        table_add<STRAT>(smem, nullptr, lo32(h) & (u32)(sp.width - 1), ((hi32(h) >> 28) & 1) ? 0ull - d : d);
+    }
+    __syncthreads();
+    for (uint64_t cc = threadIdx.x; cc < cells; cc += kSmallThreads) {
+        u64 v;
+        if (STRAT == SMEM32) v = (u64)(i64)(i32)reinterpret_cast<u32*>(smem)[cc];
+        else
+            v = (((u64)reinterpret_cast<u32*>(smem)[kLohiCells + cc] << 32) | reinterpret_cast<u32*>(smem)[cc]) -
+                0x80000000ull;
+        if (v) red_add_u64(reinterpret_cast<uint64_t*>(table) + cc, v);
+    }
+}
+
 // ---- K5: exact sum of squares per row, 192-bit accumulation ------------------
 struct U192 {
     u64 w0, w1, w2;
@@ -237,9 +315,34 @@ int blocks_per_sm_cache(const void* fn, size_t smem) {
     return v > 0 ? v : 1;
 }
 
+template <int K, int WK, int STRAT>
+cudaError_t launch_small_k32(const SketchParams& sp, const void* keys, const void* w, uint64_t n, int64_t* table,
+                             cudaStream_t s) {
+    auto fn = cs_small_k32_kernel<K, WK, STRAT>;
+    const size_t smem = STRAT == SMEM_LOHI ? (size_t)kLohiCells * 8 : (size_t)sp.width * 4;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    // one 1024-thread CTA per SM (two when the batch is large): the merge costs
+    // one red.global per cell per CTA
+    const uint64_t nv = n / 4;
+    uint64_t grid = (nv + 2 * kSmallThreads - 1) / (2 * kSmallThreads);
+    const uint64_t cap = (uint64_t)sm_count() * (n >= (1ull << 22) ? 2 : 1);
+    if (grid > cap) grid = cap;
+    if (grid == 0) grid = 1;
+    fn<<<(unsigned)grid, kSmallThreads, smem, s>>>(sp, (const u32*)keys, w, n, table);
+    return cudaGetLastError();
+}
+
 template <int MODE, int K, typename KeyT, int WK, int STRAT, int FAM = 0>
 cudaError_t launch_strat(const SketchParams& sp, const void* keys, const void* w, uint64_t n, int64_t* table,
                          cudaStream_t s, bool aggregate) {
+    // one row, Pow2, 32-bit keys, b = 61, k = 4, 16-byte aligned buffers: the vector kernel
+    if (MODE == M61_K32 && K == 4 && (STRAT == SMEM32 || STRAT == SMEM_LOHI) && WK != W_I64 &&
+        sp.families == 1 && sp.rows == 1 && sp.splitter == SPLIT_POW2 && sp.width <= kLohiCells &&
+        ((uintptr_t)keys & 15) == 0 && ((uintptr_t)w & 15) == 0)
+        return launch_small_k32<4, WK, STRAT == SMEM32 ? SMEM32 : SMEM_LOHI>(sp, keys, w, n, table, s);
     // one family with the Pow2 splitter (config 1's shape) gets a loop-free body
     if (FAM == 0 && STRAT != GLOBAL && sp.families == 1 && sp.rows == 1 && sp.splitter == SPLIT_POW2)
         return launch_strat<MODE, K, KeyT, WK, STRAT, 1>(sp, keys, w, n, table, s, aggregate);

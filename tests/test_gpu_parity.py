@@ -336,6 +336,33 @@ def test_sketch_random_vs_oracle(cuda, mb, orc, case):
     assert mb.lower_median(m) == orc.second_moment(exp, rows, width, True)
 
 
+@pytest.mark.parametrize("width", [2, 4, 1024, 8192])
+@pytest.mark.parametrize("weights", [None, "small", "extreme"])
+@pytest.mark.parametrize("n,offset", [(0, 0), (1, 0), (3, 0), (5, 0), (4099, 0), (1000003, 0), (1000003, 1)])
+def test_one_row_vector_kernel(cuda, mb, orc, width, weights, n, offset):
+    """Config 1's shape (one row, Pow2, 32-bit keys, b = 61, k = 4) runs the 16-byte
+    vector kernel when the buffers are aligned (offset 0) and the generic one when
+    not; both equal the oracle for every tail length, width and weight range (the
+    extreme weights drive the exact two-word shared counters across 2^32)."""
+    import torch
+
+    spec, fams = make_spec(mb, orc, 1, width, 61, 32, 0, 0xC1 + width)
+    rng = np.random.default_rng(n + width)
+    keys = rng.integers(0, 2**32, size=n + offset, dtype=np.uint64).astype(np.uint32)
+    w = None
+    if weights == "small":
+        w = rng.integers(-100, 101, size=n + offset).astype(np.int32)
+    elif weights == "extreme":
+        w = rng.choice(np.array([np.iinfo(np.int32).max, np.iinfo(np.int32).min, 2**30], np.int32),
+                       size=n + offset)
+    cnt = torch.zeros(width, dtype=torch.int64, device="cuda")
+    dk = dev(keys)[offset:]
+    dw = None if w is None else dev(w)[offset:]
+    mb.cs_update(spec, dk, cnt, dw)
+    exp = orc.cs_process(1, width, 61, fams, 32, 0, keys[offset:], None if w is None else w[offset:])
+    assert (cnt.cpu().numpy() == exp).all()
+
+
 HOT_CASES = [
     # rows, width, b, key_bits, splitter, key kind, weights: batches >= 2^22 take the
     # heavy-hitter path (shared-memory accumulation of sampled hot keys)

@@ -290,6 +290,7 @@ def main():
         ints = units * lpu / kernel_s
         frac_h, frac_i = hbm / hbm_peak, ints / imad_peak
         tr = (traffic.get(kname) or {}).get("dram_bytes_per_launch")
+        pipes = (traffic.get(kname) or {}).get("pipes")
         if l2_reds is not None:
             red_rate = l2_reds / kernel_s
             views = {"hbm": {"achieved": hbm, "peak": hbm_peak, "unit": "GB/s", "frac": frac_h,
@@ -304,16 +305,21 @@ def main():
             out = {"bound": bound, **{k: views[bound][k] for k in ("achieved", "peak", "unit", "frac")},
                    "traffic": tr, "peak_kind": views[bound]["peak_kind"]}
             out.update({k: v for k, v in views.items() if k != bound})
+            if pipes:
+                out["ncu_pipes"] = {**pipes, "source": f"profiles/{traffic.get('round')}/ncu_{kname}.txt"}
             return out
+        extra = {}
+        if pipes:  # which pipe actually binds, from the committed ncu capture of this kernel
+            extra["ncu_pipes"] = {**pipes, "source": f"profiles/{traffic.get('round')}/ncu_{kname}.txt"}
         if frac_h >= frac_i:
             return {"bound": "hbm", "achieved": hbm, "peak": hbm_peak, "unit": "GB/s", "frac": frac_h,
                     "traffic": tr, "peak_kind": peak_kind,
                     "int_pipe": {"achieved": ints / 1e12, "peak": imad_peak / 1e12, "unit": "T IMAD.WIDE/s",
-                                 "frac": frac_i}}
+                                 "frac": frac_i}, **extra}
         return {"bound": "int", "achieved": ints / 1e12, "peak": imad_peak / 1e12, "unit": "T IMAD.WIDE/s",
                 "frac": frac_i, "traffic": tr, "peak_kind": "measured (probe_imad, this run)",
                 "hbm": {"achieved": hbm, "peak": hbm_peak, "unit": "GB/s", "frac": frac_h,
-                        "peak_kind": peak_kind, "frac_of_8TBs": hbm / 8000.0}}
+                        "peak_kind": peak_kind, "frac_of_8TBs": hbm / 8000.0}, **extra}
 
     # ---------------------------------------------------------- config 5 headline
     n_total = args.items

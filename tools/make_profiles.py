@@ -70,7 +70,15 @@ def main(tag):
                                                            1e6 if u[h.index("dram__bytes_read.sum")] == "Mbyte" else 1)
         wr = float(v[h.index("dram__bytes_write.sum")]) * (1e9 if u[h.index("dram__bytes_write.sum")] == "Gbyte" else
                                                             1e6 if u[h.index("dram__bytes_write.sum")] == "Mbyte" else 1)
-        traffic[t] = {"kernel": v[h.index("Kernel Name")].split("(")[0], "dram_bytes_per_launch": rd + wr}
+        def pct(metric):
+            return float(v[h.index(metric)]) / 100.0 if metric in h else None
+
+        traffic[t] = {"kernel": v[h.index("Kernel Name")].split("(")[0], "dram_bytes_per_launch": rd + wr,
+                      "pipes": {"alu": pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                                "fma": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                                "issue": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                                "dram": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                                "lts": pct("lts__throughput.avg.pct_of_peak_sustained_elapsed")}}
     with open(os.path.join(dst, "ncu_traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:

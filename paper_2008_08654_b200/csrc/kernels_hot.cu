@@ -7,7 +7,7 @@
 // L2 and the lever is the NUMBER of L2 reductions.  Count Sketch is linear:
 // the updates of one key can be summed anywhere and applied once.
 //
-//   1. hh_count  : exact key counts over a sample (the batch's first 2^18 items)
+//   1. hh_count  : exact key counts over a sample (the batch's first 2^20 items)
 //                  in an open-addressing table in global memory;
 //   2. hh_hist /
 //      hh_select : the most frequent sampled keys (count >= a threshold picked
@@ -55,64 +55,76 @@ using namespace sk;
 
 constexpr int kHotThreads = 1024;
 constexpr int kHotWarps = kHotThreads / 32;
-constexpr uint32_t kHotSample = 1u << 18;
-constexpr uint32_t kCountLog2 = 20;
+constexpr uint32_t kHotSample = 1u << 20;
+constexpr uint32_t kCountLog2 = 21;  // sample count table at <= 50% load
 constexpr uint32_t kCountSlots = 1u << kCountLog2;
 constexpr int kQueue = 64;     // < 32 queued + one slot of 32 misses
 constexpr uint32_t kMissChunk = 1024;  // miss-buffer slots a warp reserves at once
 
 template <typename KeyT>
 struct HotGeom;
+// shared slot = key + the low word of its exact sum (the rarely used wrap
+// counter lives in HBM, one array per CTA); slot counts need not be powers of 2
 template <>
 struct HotGeom<u32> {
-    static constexpr uint32_t kLog2 = 14;  // 16384 slots x (4 B key + 8 B sum) = 192 KiB
-    static constexpr uint32_t kCap = 8192;
+    static constexpr uint32_t kSlots = 24576;  // x (4 B key + 4 B low sum) = 192 KiB
+    static constexpr uint32_t kCap = 16384;
     static constexpr u32 kEmpty = 0xffffffffu;
     using Cas = unsigned;
 };
 template <>
 struct HotGeom<u64> {
-    static constexpr uint32_t kLog2 = 13;  // 8192 slots x (8 B key + 8 B sum) = 128 KiB
-    static constexpr uint32_t kCap = 4096;
+    static constexpr uint32_t kSlots = 16384;  // x (8 B key + 4 B low sum) = 192 KiB
+    static constexpr uint32_t kCap = 8192;
     static constexpr u64 kEmpty = ~0ull;
     using Cas = unsigned long long;
 };
 
-// two independent slot choices from the HIGH bits of multiplicative / mixing hashes
-template <uint32_t LOG2>
+// two independent slot choices in [0, S): multiply-high range reduction of two
+// independent 32-bit mixes (any S, not only powers of two)
+template <uint32_t S>
+__device__ __forceinline__ u32 slot_of(u32 h) {
+    return (u32)(((u64)h * S) >> 32);
+}
+template <uint32_t S>
 __device__ __forceinline__ u32 slot1(u32 key) {
-    return (key * 0x9E3779B1u) >> (32 - LOG2);
+    return slot_of<S>(key * 0x9E3779B1u);
 }
-template <uint32_t LOG2>
+template <uint32_t S>
 __device__ __forceinline__ u32 slot2(u32 key) {
-    return ((key ^ (key >> 15)) * 0x2C1B3C6Du) >> (32 - LOG2);
+    return slot_of<S>((key ^ (key >> 15)) * 0x2C1B3C6Du);
 }
-template <uint32_t LOG2>
+template <uint32_t S>
 __device__ __forceinline__ u32 slot1(u64 key) {
-    return (u32)(mix64(key) >> (64 - LOG2));
+    return slot_of<S>((u32)(mix64(key) >> 32));
 }
-template <uint32_t LOG2>
+template <uint32_t S>
 __device__ __forceinline__ u32 slot2(u64 key) {
-    return (u32)(mix64(key) >> 20) & ((1u << LOG2) - 1);
+    return slot_of<S>((u32)mix64(key));
 }
 
+// Exact key counts of the sample in a global open-addressing table.  Equal
+// keys of a warp are merged first (__match_any_sync), so the hottest keys of a
+// skewed stream cost one atomic per warp instead of one per item.
 template <typename KeyT>
 __global__ void hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT* tk, u32* tc) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const KeyT key = ld_nc(keys + i);
-        if (key == G::kEmpty) continue;
-        u32 h = slot1<kCountLog2>(key);
+    const uint64_t n_pad = (n + 31) & ~31ull;  // whole warps stay in the loop (match_any)
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
+        const KeyT key = i < n ? ld_nc(keys + i) : G::kEmpty;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (key == G::kEmpty || (threadIdx.x & 31) != __ffs(peers) - 1) continue;
+        u32 h = slot1<kCountSlots>(key);
         for (;;) {
             KeyT cur = tk[h];
             if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(tk + h), (C)G::kEmpty, (C)key);
             if (cur == G::kEmpty || cur == key) {
-                atomicAdd(tc + h, 1u);
+                atomicAdd(tc + h, (u32)__popc(peers));
                 break;
             }
-            h = (h + 1) & (kCountSlots - 1);
+            h = h + 1 == kCountSlots ? 0 : h + 1;
         }
     }
 }
@@ -133,27 +145,38 @@ __global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist) {
 template <typename KeyT>
 __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restrict__ tc, const u32* __restrict__ hist,
                                  u32 cap, KeyT* hot, u32* hot_cnt, u32* hot_count, u32* hot_sum) {
-    __shared__ u32 thr;
+    __shared__ u32 thr, sh[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = hist[i];  // one parallel load
+    __syncthreads();
     if (threadIdx.x == 0) {  // smallest threshold >= 2 whose tail fits the shared table
         u32 tail = 0, c = 255;
         for (; c >= 2; --c) {
-            if (tail + hist[c] > cap) break;
-            tail += hist[c];
+            if (tail + sh[c] > cap) break;
+            tail += sh[c];
         }
         thr = c + 1;
     }
     __syncthreads();
     const u32 t = thr;
+    const int lane = threadIdx.x & 31;
+    // whole warps in the loop (kCountSlots is a multiple of the grid); one
+    // atomic per warp reserves the selected keys' slots and adds their counts
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < kCountSlots; s += gridDim.x * blockDim.x) {
         const u32 c = tc[s];
-        if (c >= t) {
-            const u32 idx = atomicAdd(hot_count, 1u);
-            if (idx < cap) {
-                hot[idx] = tk[s];
-                hot_cnt[idx] = c;
-                atomicAdd(hot_sum, c);  // sampled items the hot set covers
-            }
+        const bool sel = c >= t;
+        const unsigned m = __ballot_sync(0xffffffffu, sel);
+        if (!m) continue;
+        u32 base = 0;
+        if (lane == 0) base = atomicAdd(hot_count, (u32)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const u32 idx = base + __popc(m & ((1u << lane) - 1));
+        const bool keep = sel && idx < cap;
+        if (keep) {
+            hot[idx] = tk[s];
+            hot_cnt[idx] = c;
         }
+        const u32 covered = __reduce_add_sync(0xffffffffu, keep ? c : 0u);
+        if (lane == 0 && covered) atomicAdd(hot_sum, covered);  // sampled items the hot set covers
     }
 }
 
@@ -167,7 +190,7 @@ __device__ __forceinline__ void hot_accumulate(u32* lo, u32* hi, u32 h, i32 d) {
     const u32 old = atomicAdd(lo + h, dd);
     const u32 nw = old + dd;
     const int carry = d >= 0 ? (int)(nw < old) : -(int)(nw > old);
-    if (carry) atomicAdd(hi + h, (u32)carry);
+    if (carry) atomicAdd(hi + h, (u32)carry);  // hi may be shared or global memory
 }
 
 // Raw mode: the hot set covers under 30% of the sample, so the hot pass would
@@ -242,7 +265,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     cs_hot_kernel(const SketchParams sp, const KeyT* __restrict__ keys, const void* __restrict__ w, uint64_t n,
                   i64* __restrict__ table, const KeyT* __restrict__ hot, const u32* __restrict__ hot_cnt,
                   const u32* __restrict__ hot_count, const u32* __restrict__ hot_sum, uint32_t sample,
-                  const MissBuf<KeyT> mb, bool vec_ok) {
+                  const MissBuf<KeyT> mb, bool vec_ok, u32* __restrict__ wraps, u32 band_scale) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
     using KV = KeyVec<KeyT>;
@@ -250,12 +273,12 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     constexpr int kVT = 8 / kV;        // vectors per lane per tile
     constexpr int kIt = kV * kVT;      // items per lane per tile (8 u32 / 4 u64)
     constexpr uint64_t kT = 32ull * kIt;
-    constexpr uint32_t S = 1u << G::kLog2;
+    constexpr uint32_t S = G::kSlots;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
     u32* lo = reinterpret_cast<u32*>(hk + S);
-    u32* hi = lo + S;
-    KeyT* qk = reinterpret_cast<KeyT*>(hi + S);
+    u32* hi = wraps + (uint64_t)blockIdx.x * S;  // this CTA's wrap counters (HBM, zeroed by the launcher)
+    KeyT* qk = reinterpret_cast<KeyT*>(lo + S);
     i32* qd = reinterpret_cast<i32*>(qk + kHotWarps * kQueue);
     __shared__ u32 s_next;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -281,7 +304,6 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
         hk[s] = G::kEmpty;
         lo[s] = 0x80000000u;
-        hi[s] = 0;
     }
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
@@ -290,15 +312,15 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     // Slots are never freed, so a lookup whose slot1 is empty is a miss without
     // touching slot2.  Hottest keys are placed first so they own their slot1.
     const u32 nhot = min(*hot_count, G::kCap);
-    const u32 bands[3] = {64u, 8u, 0u};
+    const u32 bands[3] = {64u * band_scale, 8u * band_scale, 0u};  // counts scale with the sample
     u32 upper = 0xffffffffu;
     for (int r = 0; r < 3; ++r) {
         for (u32 j = threadIdx.x; j < nhot; j += kHotThreads) {
             const u32 c = hot_cnt[j];
             if (c < bands[r] || c >= upper) continue;
             const KeyT key = hot[j];
-            if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + slot1<G::kLog2>(key)), (C)G::kEmpty, (C)key) != G::kEmpty)
-                atomicCAS(reinterpret_cast<C*>(hk + slot2<G::kLog2>(key)), (C)G::kEmpty, (C)key);
+            if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + slot1<S>(key)), (C)G::kEmpty, (C)key) != G::kEmpty)
+                atomicCAS(reinterpret_cast<C*>(hk + slot2<S>(key)), (C)G::kEmpty, (C)key);
         }
         upper = bands[r];
         __syncthreads();
@@ -313,7 +335,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     auto item = [&](KeyT key, i32 d, bool valid) {
         // both slots probed speculatively (no divergent second probe); a key never
         // sits in its slot2 unless its slot1 was taken first, so this is exact
-        const u32 h1 = slot1<G::kLog2>(key), h2 = slot2<G::kLog2>(key);
+        const u32 h1 = slot1<S>(key), h2 = slot2<S>(key);
         const KeyT c1 = hk[h1], c2 = hk[h2];
         const u32 h = c1 == key ? h1 : h2;
         const bool hit = valid && (c1 == key || c2 == key) && key != G::kEmpty;
@@ -745,9 +767,9 @@ struct HotPlan {
     uint32_t chunks = 0;       // (pass 4, pass 5) round trips
     uint64_t chunk_items = 0;  // items per round trip
     uint64_t cap_m = 0;        // miss-buffer capacity
-    size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, hot_bytes = 0, mk_bytes = 0, md_bytes = 0,
-           bin_bytes = 0;
-    size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes; }  // tc .. gcnt are contiguous
+    size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, wraps_bytes = 0, hot_bytes = 0, mk_bytes = 0,
+           md_bytes = 0, bin_bytes = 0;
+    size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes + wraps_bytes; }  // tc .. wraps contiguous
     size_t total() const { return tk_bytes + zero_bytes() + hot_bytes + mk_bytes + md_bytes + bin_bytes; }
 };
 
@@ -787,6 +809,7 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     P.tc_bytes = (size_t)kCountSlots * 4;
     P.misc = 256 * 4 + 64;  // hist[256], hot_count, hot_sum, miss count (u64)
     P.gcnt_bytes = align256((size_t)P.chunks * g.nb * 8 + 8);
+    P.wraps_bytes = align256((size_t)sm_count() * G::kSlots * 4);
     P.hot_bytes = align256((size_t)G::kCap * (sizeof(KeyT) + 4));
     P.mk_bytes = align256((size_t)P.cap_m * sizeof(KeyT));
     P.md_bytes = align256((size_t)P.cap_m * 4);
@@ -808,6 +831,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     u32* hot_sum = hot_count + 1;
     unsigned long long* mcount = reinterpret_cast<unsigned long long*>(hot_count + 2);
     g.gcnt = reinterpret_cast<unsigned long long*>(ws + P.tk_bytes + P.tc_bytes + P.misc);
+    u32* wraps = reinterpret_cast<u32*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes);
     unsigned char* p = ws + P.tk_bytes + P.zero_bytes();
     KeyT* hot = reinterpret_cast<KeyT*>(p);
     u32* hot_cnt = reinterpret_cast<u32*>(hot + G::kCap);
@@ -818,10 +842,10 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     cudaMemsetAsync(tk, 0xff, P.tk_bytes, s);
     cudaMemsetAsync(tc, 0, P.zero_bytes(), s);
     hh_count_kernel<KeyT><<<sms * 4, 256, 0, s>>>(keys, P.m, tk, tc);
-    hh_hist_kernel<<<sms, 256, 0, s>>>(tc, hist);
-    hh_select_kernel<KeyT><<<sms, 256, 0, s>>>(tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum);
+    hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist);
+    hh_select_kernel<KeyT><<<sms * 8, 256, 0, s>>>(tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum);
     auto fn = cs_hot_kernel<MODE, K, KeyT, WK>;
-    const size_t smem = ((size_t)sizeof(KeyT) + 8) << G::kLog2;
+    const size_t smem = ((size_t)sizeof(KeyT) + 4) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes));
     if (e != cudaSuccess) return e;
@@ -829,8 +853,9 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     if (grid > (uint64_t)sms) grid = sms;
     const bool vec_ok = (reinterpret_cast<uintptr_t>(keys) & 15) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
     // without bins (cap 0) every miss takes the direct path and raw mode is off
+    const u32 band_scale = P.m >= (1u << 18) ? P.m >> 18 : 1;
     fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, hot, hot_cnt, hot_count, hot_sum,
-                                                          binned ? P.m : 0, mb, vec_ok);
+                                                          binned ? P.m : 0, mb, vec_ok, wraps, band_scale);
     if ((e = cudaGetLastError()) != cudaSuccess || !binned) return e;
     auto fb_raw = g.bpr == 1 ? cs_bin_kernel<MODE, K, SPL, KeyT, WK, true, true>
                              : cs_bin_kernel<MODE, K, SPL, KeyT, WK, true, false>;

@@ -55,9 +55,9 @@ using namespace sk;
 
 constexpr int kHotThreads = 1024;
 constexpr int kHotWarps = kHotThreads / 32;
-constexpr uint32_t kHotSample = 1u << 20;
-constexpr uint32_t kCountLog2 = 21;  // sample count table at <= 50% load
-constexpr uint32_t kCountSlots = 1u << kCountLog2;
+// sample = n / 2048 items, clamped to [2^18, 2^20] (so a shard of a multi-GPU
+// run pays a proportionally smaller prepass); count table = 2 x sample slots
+constexpr uint32_t kMinSample = 1u << 18, kMaxSample = 1u << 20;
 constexpr int kQueue = 64;     // < 32 queued + one slot of 32 misses
 constexpr uint32_t kMissChunk = 1024;  // miss-buffer slots a warp reserves at once
 
@@ -107,7 +107,7 @@ __device__ __forceinline__ u32 slot2(u64 key) {
 // keys of a warp are merged first (__match_any_sync), so the hottest keys of a
 // skewed stream cost one atomic per warp instead of one per item.
 template <typename KeyT>
-__global__ void hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT* tk, u32* tc) {
+__global__ void hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT* tk, u32* tc, u32 slots) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -116,7 +116,7 @@ __global__ void hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT*
         const KeyT key = i < n ? ld_nc(keys + i) : G::kEmpty;
         const unsigned peers = __match_any_sync(0xffffffffu, key);
         if (key == G::kEmpty || (threadIdx.x & 31) != __ffs(peers) - 1) continue;
-        u32 h = slot1<kCountSlots>(key);
+        u32 h = (u32)(((u64)((u32)(mix64((u64)key) >> 32)) * slots) >> 32);
         for (;;) {
             KeyT cur = tk[h];
             if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(tk + h), (C)G::kEmpty, (C)key);
@@ -124,16 +124,16 @@ __global__ void hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT*
                 atomicAdd(tc + h, (u32)__popc(peers));
                 break;
             }
-            h = h + 1 == kCountSlots ? 0 : h + 1;
+            h = h + 1 == slots ? 0 : h + 1;
         }
     }
 }
 
-__global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist) {
+__global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist, u32 slots) {
     __shared__ u32 sh[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
     __syncthreads();
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < kCountSlots; s += gridDim.x * blockDim.x) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x) {
         const u32 c = tc[s];
         if (c) atomicAdd(&sh[c < 255 ? c : 255], 1u);
     }
@@ -144,7 +144,7 @@ __global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist) {
 
 template <typename KeyT>
 __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restrict__ tc, const u32* __restrict__ hist,
-                                 u32 cap, KeyT* hot, u32* hot_cnt, u32* hot_count, u32* hot_sum) {
+                                 u32 cap, KeyT* hot, u32* hot_cnt, u32* hot_count, u32* hot_sum, u32 slots) {
     __shared__ u32 thr, sh[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = hist[i];  // one parallel load
     __syncthreads();
@@ -159,9 +159,9 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
     __syncthreads();
     const u32 t = thr;
     const int lane = threadIdx.x & 31;
-    // whole warps in the loop (kCountSlots is a multiple of the grid); one
-    // atomic per warp reserves the selected keys' slots and adds their counts
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < kCountSlots; s += gridDim.x * blockDim.x) {
+    // whole warps in the loop (slots is a multiple of 32); one atomic per warp
+    // reserves the selected keys' slots and adds their counts
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x) {
         const u32 c = tc[s];
         const bool sel = c >= t;
         const unsigned m = __ballot_sync(0xffffffffu, sel);
@@ -764,6 +764,7 @@ template <typename KeyT>
 struct HotPlan {
     BinGeom g{};
     uint32_t m = 0;            // sample size
+    uint32_t slots = 0;        // sample count table slots (power of two >= 2m)
     uint32_t chunks = 0;       // (pass 4, pass 5) round trips
     uint64_t chunk_items = 0;  // items per round trip
     uint64_t cap_m = 0;        // miss-buffer capacity
@@ -777,7 +778,11 @@ template <typename KeyT>
 HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     using G = HotGeom<KeyT>;
     HotPlan<KeyT> P;
-    P.m = (uint32_t)(n < kHotSample ? n : kHotSample);
+    uint64_t m = n / 2048;
+    m = m < kMinSample ? kMinSample : m > kMaxSample ? kMaxSample : m;
+    P.m = (uint32_t)(n < m ? n : m);
+    P.slots = 64;
+    while (P.slots < 2ull * P.m) P.slots *= 2;
     BinGeom& g = P.g;
     // bin geometry: rows x ceil(width / 8192) bins of <= 8192 cells
     g.width = sp.width;
@@ -805,8 +810,8 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
         const uint64_t grp = (uint64_t)g.cap_s * 17 / 20 * g.nb / ((uint64_t)kBinThreads * 4 * sp.rows);
         g.groups = (uint32_t)(grp < 1 ? 1 : grp > 16 ? 16 : grp);
     }
-    P.tk_bytes = align256((size_t)kCountSlots * sizeof(KeyT));
-    P.tc_bytes = (size_t)kCountSlots * 4;
+    P.tk_bytes = align256((size_t)P.slots * sizeof(KeyT));
+    P.tc_bytes = (size_t)P.slots * 4;
     P.misc = 256 * 4 + 64;  // hist[256], hot_count, hot_sum, miss count (u64)
     P.gcnt_bytes = align256((size_t)P.chunks * g.nb * 8 + 8);
     P.wraps_bytes = align256((size_t)sm_count() * G::kSlots * 4);
@@ -826,7 +831,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     const bool binned = g.nb != 0;
     KeyT* tk = reinterpret_cast<KeyT*>(ws);
     u32* tc = reinterpret_cast<u32*>(ws + P.tk_bytes);
-    u32* hist = tc + kCountSlots;
+    u32* hist = tc + P.slots;
     u32* hot_count = hist + 256;
     u32* hot_sum = hot_count + 1;
     unsigned long long* mcount = reinterpret_cast<unsigned long long*>(hot_count + 2);
@@ -841,9 +846,9 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     g.bins = reinterpret_cast<u32*>(p);
     cudaMemsetAsync(tk, 0xff, P.tk_bytes, s);
     cudaMemsetAsync(tc, 0, P.zero_bytes(), s);
-    hh_count_kernel<KeyT><<<sms * 4, 256, 0, s>>>(keys, P.m, tk, tc);
-    hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist);
-    hh_select_kernel<KeyT><<<sms * 8, 256, 0, s>>>(tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum);
+    hh_count_kernel<KeyT><<<sms * 4, 256, 0, s>>>(keys, P.m, tk, tc, P.slots);
+    hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots);
+    hh_select_kernel<KeyT><<<sms * 8, 256, 0, s>>>(tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum, P.slots);
     auto fn = cs_hot_kernel<MODE, K, KeyT, WK>;
     const size_t smem = ((size_t)sizeof(KeyT) + 4) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);

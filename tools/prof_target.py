@@ -18,8 +18,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("which", choices=["c1", "c2k4", "c2k8", "c3", "c4", "c5"])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--binned", action="store_true", help="large tables: binned strategy")
     a = ap.parse_args()
     w = a.which
+    if a.binned:
+        mb.set_large_table_strategy(mb.LARGE_BINNED)
     if w == "c5":
         zs = mb.ZipfStream(S)
         keys, wts = zs.generate(0, 1 << 31)

@@ -216,10 +216,56 @@ __device__ __forceinline__ i32 load_w32(const void* w, uint64_t i) {
     return ld_nc(reinterpret_cast<const i32*>(w) + i);
 }
 
-// a full warp of misses whose miss-buffer slots are gone: the direct path (rare)
-template <int MODE, int K, typename KeyT>
+enum SplitC { SPC_POW2 = 0, SPC_TFO = 1, SPC_ANY = 2 };  // compile-time splitter (Pow2 / two-for-one / other)
+
+// bucket index (< 2^32) and sign of sub-row s, splitter known
+// at compile time where it is Pow2 / two-for-one (sketch.cpp:13-19, SURVEY 7.4)
+template <int MODE, int SPL>
+__device__ __forceinline__ u32 split_c(const SketchParams& sp, u64 hlo, u64 hhi, uint32_t s, bool& neg) {
+    if (MODE == M89) return (u32)split89(sp, hlo, hhi, s, neg);
+    if (MODE != MGEN && SPL == SPC_POW2) {  // b = 61: sign = bit 60, index = low bits
+        neg = (hi32(hlo) >> 28) & 1;
+        return lo32(hlo) & (u32)(sp.width - 1);
+    }
+    if (MODE != MGEN && SPL == SPC_TFO) {
+        neg = (hlo >> (60 - s)) & 1;
+        return (u32)(hlo >> (sp.lw * s)) & (u32)(sp.width - 1);
+    }
+    return (u32)split_small(sp, hlo, s, neg);
+}
+
+// One item straight to L2: every family, every sub-row, hash -> split ->
+// red.global (process_item with the splitter fixed at compile time where it is
+// Pow2 or two-for-one; sketch.cpp:133-140).
+template <int MODE, int K, int SPL>
+__device__ __forceinline__ void rows_direct(const SketchParams& sp, u64 x, i64 delta, i64* table) {
+    if (SPL == SPC_ANY) {
+        process_item<MODE, K, GLOBAL>(sp, x, delta, nullptr, table);
+        return;
+    }
+    const u64 dp = (u64)delta, dn = 0ull - dp;
+    constexpr uint32_t subs = SPL == SPC_TFO ? 2 : 1;
+    uint64_t* base = reinterpret_cast<uint64_t*>(table);
+#pragma unroll 1
+    for (uint32_t f = 0; f < sp.families; ++f) {
+        u64 hlo, hhi = 0;
+        if (MODE == M89) hash89<K>(sp, f, x, hlo, hhi);
+        else hlo = hash_small<MODE, K>(sp, f, x);
+#pragma unroll
+        for (uint32_t s = 0; s < subs; ++s) {
+            const uint32_t row = subs * f + s;
+            if (row >= sp.rows) break;
+            bool neg;
+            const u32 idx = split_c<MODE, SPL>(sp, hlo, hhi, s, neg);
+            red_add_u64(base + (u64)row * sp.width + idx, neg ? dn : dp);
+        }
+    }
+}
+
+// a full warp of misses: the direct path
+template <int MODE, int K, int SPL, typename KeyT>
 __device__ __forceinline__ void misses_direct(const SketchParams& sp, KeyT key, i32 d, bool valid, i64* table) {
-    if (valid) process_item<MODE, K, GLOBAL>(sp, (u64)key, (i64)d, nullptr, table);
+    if (valid) rows_direct<MODE, K, SPL>(sp, (u64)key, (i64)d, table);
 }
 
 // 16-byte vector of keys / weights (4 u32 or 2 u64 keys per vector)
@@ -260,7 +306,7 @@ struct WVec {
     }
 };
 
-template <int MODE, int K, typename KeyT, int WK>
+template <int MODE, int K, int SPL, typename KeyT, int WK>
 __global__ void __launch_bounds__(kHotThreads, 1)
     cs_hot_kernel(const SketchParams sp, const KeyT* __restrict__ keys, const void* __restrict__ w, uint64_t n,
                   i64* __restrict__ table, const KeyT* __restrict__ hot, const u32* __restrict__ hot_cnt,
@@ -351,7 +397,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         misses += __popc(m);
         if (qn >= 32 && mb.cap == 0) {  // a full warp of misses -> hash, split, red.global
             __syncwarp();
-            misses_direct<MODE, K, KeyT>(sp, wqk[lane], wqd[lane], true, table);
+            misses_direct<MODE, K, SPL, KeyT>(sp, wqk[lane], wqd[lane], true, table);
             direct += sp.rows;
             __syncwarp();
             if (lane < qn - 32) {
@@ -373,7 +419,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
                 mb.keys[pos + lane] = wqk[lane];
                 mb.deltas[pos + lane] = wqd[lane];
             } else {
-                misses_direct<MODE, K, KeyT>(sp, wqk[lane], wqd[lane], true, table);
+                misses_direct<MODE, K, SPL, KeyT>(sp, wqk[lane], wqd[lane], true, table);
                 direct += sp.rows;
             }
             __syncwarp();
@@ -436,7 +482,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         item(v ? ld_nc(keys + i) : G::kEmpty, v ? load_w32<WK>(w, i) : 0, v);
     }
     if (lane < qn) {
-        misses_direct<MODE, K, KeyT>(sp, wqk[lane], wqd[lane], true, table);
+        misses_direct<MODE, K, SPL, KeyT>(sp, wqk[lane], wqd[lane], true, table);
         direct += sp.rows;
     }
     // unused reserved slots become no-op items (delta 0)
@@ -450,7 +496,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         if (hk[s] == G::kEmpty) continue;
         const u64 v = (((u64)hi[s] << 32) | lo[s]) - 0x80000000ull;
         if (v) {
-            process_item<MODE, K, GLOBAL>(sp, (u64)hk[s], (i64)v, nullptr, table);
+            rows_direct<MODE, K, SPL>(sp, (u64)hk[s], (i64)v, table);
             ++flushed;
         }
     }
@@ -477,7 +523,6 @@ constexpr size_t kStageBytes = 200 * 1024;
 constexpr uint64_t kMinBinChunk = 1ull << 26;  // items binned per (pass 4, pass 5) round trip
 constexpr uint32_t kMaxChunks = 8;
 constexpr int kAccThreads = 1024;
-enum SplitC { SPC_POW2 = 0, SPC_TFO = 1, SPC_ANY = 2 };  // compile-time splitter of the binned path
 
 struct BinGeom {
     u32* bins;                 // [nb][cap] 4-byte entries
@@ -542,22 +587,6 @@ struct BinSink {
         }
     }
 };
-
-// bucket index (< 2^22 on the binned path) and sign of sub-row s, splitter known
-// at compile time where it is Pow2 / two-for-one (sketch.cpp:13-19, SURVEY 7.4)
-template <int MODE, int SPL>
-__device__ __forceinline__ u32 split_c(const SketchParams& sp, u64 hlo, u64 hhi, uint32_t s, bool& neg) {
-    if (MODE == M89) return (u32)split89(sp, hlo, hhi, s, neg);
-    if (MODE != MGEN && SPL == SPC_POW2) {  // b = 61: sign = bit 60, index = low bits
-        neg = (hi32(hlo) >> 28) & 1;
-        return lo32(hlo) & (u32)(sp.width - 1);
-    }
-    if (MODE != MGEN && SPL == SPC_TFO) {
-        neg = (hlo >> (60 - s)) & 1;
-        return (u32)(hlo >> (sp.lw * s)) & (u32)(sp.width - 1);
-    }
-    return (u32)split_small(sp, hlo, s, neg);
-}
 
 // U items: per family the U Horner chains are interleaved, then every sub-row
 // of every item goes to the sink (same arithmetic as process_item); warp-uniform.
@@ -849,7 +878,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     hh_count_kernel<KeyT><<<sms * 4, 256, 0, s>>>(keys, P.m, tk, tc, P.slots);
     hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots);
     hh_select_kernel<KeyT><<<sms * 8, 256, 0, s>>>(tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum, P.slots);
-    auto fn = cs_hot_kernel<MODE, K, KeyT, WK>;
+    auto fn = cs_hot_kernel<MODE, K, SPL, KeyT, WK>;
     const size_t smem = ((size_t)sizeof(KeyT) + 4) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes));
@@ -896,9 +925,10 @@ cudaError_t launch_hot(const SketchParams& sp, const void* keys, const void* w, 
     cudaError_t e = cudaMallocAsync(&ws, P.total(), s);
     if (e != cudaSuccess) return e;
     const KeyT* kk = reinterpret_cast<const KeyT*>(keys);
-    if (MODE != MGEN && sp.splitter == SPLIT_POW2)
+    const bool narrow = sp.width <= (1ull << 32);  // compile-time splitters return u32 indices
+    if (MODE != MGEN && narrow && sp.splitter == SPLIT_POW2)
         e = run_hot<MODE, K, SPC_POW2, KeyT, WK>(sp, kk, w, n, table, s, ws, P);
-    else if (MODE != MGEN && sp.splitter == SPLIT_TWO_FOR_ONE)
+    else if (MODE != MGEN && narrow && sp.splitter == SPLIT_TWO_FOR_ONE)
         e = run_hot<MODE, K, SPC_TFO, KeyT, WK>(sp, kk, w, n, table, s, ws, P);
     else
         e = run_hot<MODE, K, SPC_ANY, KeyT, WK>(sp, kk, w, n, table, s, ws, P);

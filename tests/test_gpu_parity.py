@@ -410,6 +410,40 @@ def test_hot_path_large_batches(cuda, mb, orc, case, strategy):
         assert st["binned"] > 0  # the binned passes really ran
 
 
+@pytest.mark.parametrize("shape", ["overflow", "wide", "bigdelta"])
+def test_binned_strategy_edge_paths(cuda, mb, orc, shape):
+    """The binned strategy's fall-backs stay exact: more misses than the miss buffer
+    holds (35% one key, 65% distinct keys: not raw mode, misses > n/2), rows wider
+    than one 65536-cell bin (several bins per row, ballot grouping), and deltas
+    outside the 16-bit entry field (direct reductions from the sink)."""
+    import torch
+
+    n = (1 << 22) + 333
+    rng = np.random.default_rng({"overflow": 1, "wide": 2, "bigdelta": 3}[shape])
+    rows, width = (3, 1 << 18) if shape == "wide" else (5, 65536)
+    spec, fams = make_spec(mb, orc, rows, width, 61, 32, 0, 0x5EED)
+    if shape == "overflow":
+        keys = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+        keys[rng.random(n) < 0.35] = 12345
+    else:
+        keys, _ = orc.gen_zipf_items(11, 0, n)
+    w = rng.integers(-100, 101, size=n).astype(np.int32)
+    if shape == "bigdelta":
+        big = rng.random(n) < 0.1
+        w[big] = rng.integers(-(2**31), 2**31, size=int(big.sum())).astype(np.int32)
+    cnt = torch.zeros(rows * width, dtype=torch.int64, device="cuda")
+    prev = mb.set_large_table_strategy(mb.LARGE_BINNED)
+    mb.hot_stats(reset=True)
+    try:
+        mb.cs_update(spec, dev(keys), cnt, dev(w))
+    finally:
+        mb.set_large_table_strategy(prev)
+    st = mb.hot_stats(reset=True)
+    exp = orc.cs_process(rows, width, 61, fams, 32, 0, keys, w)
+    assert (cnt.cpu().numpy() == exp).all()
+    assert st["binned"] > 0 and st["direct"] > 0  # both the bins and a fall-back path ran
+
+
 def test_large_table_strategy_rejects_unknown(cuda, mb):
     with pytest.raises(mb.InvalidArgument):
         mb.set_large_table_strategy(7)

@@ -382,13 +382,14 @@ def main():
         "roofline": roofline("c5", n_local, kern, "c5", l2_reds=c5_reds),
         "kernel_ms": kern * 1e3,
         "hot_path": {"miss_fraction": hs["misses"] / max(1, hs["items"]),
-                     "hot_keys_per_cta": hs["hot_keys"] / max(1, args.steps * mb_sm_count(torch)),
+                     "hot_keys": hs["hot_keys"] / max(1, args.steps),
                      "l2_reds_per_item": c5_reds / max(1, n_local),
                      "binned_entries_per_item": hs["binned"] / max(1, hs["items"]),
                      "direct_row_updates": hs["direct"] / args.steps,
                      "raw_batches": hs["raw_batches"]},
-        # per step: hh_count, hh_hist, hh_select, cs_hot, cs_moments (the table zeroing is a torch fill)
-        "gpu_launches": 5 * args.steps,
+        # per step: hh_count, hh_hist, hh_select, hh_layout, cs_hot, hh_merge, cs_moments
+        # (the table zeroing is a torch fill)
+        "gpu_launches": 7 * args.steps,
         "clocks": clocks,
         "peaks": {"imad_wide_per_s": imad_peak, "l2_red_per_s": red_peak, "hbm_gbs": hbm_peak,
                   "hbm_kind": peak_kind},

@@ -55,8 +55,8 @@ using namespace sk;
 
 constexpr int kHotThreads = 1024;
 constexpr int kHotWarps = kHotThreads / 32;
-// sample = n / 2048 items, clamped to [2^18, 2^20] (so a shard of a multi-GPU
-// run pays a proportionally smaller prepass); count table = 2 x sample slots
+// sample = n / 256 items, clamped to [2^18, 2^20] (a shard of a multi-GPU run
+// still gets the full-size hot set from 2^28 items on); count table = 2 x sample
 constexpr uint32_t kMinSample = 1u << 18, kMaxSample = 1u << 20;
 constexpr int kQueue = 64;     // < 32 queued + one slot of 32 misses
 constexpr uint32_t kMissChunk = 1024;  // miss-buffer slots a warp reserves at once
@@ -103,30 +103,61 @@ __device__ __forceinline__ u32 slot2(u64 key) {
     return slot_of<S>((u32)mix64(key));
 }
 
-// Exact key counts of the sample in a global open-addressing table.  Equal
-// keys of a warp are merged first (__match_any_sync), so the hottest keys of a
-// skewed stream cost one atomic per warp instead of one per item.
+// Exact key counts of the sample in a global open-addressing table.  Each CTA
+// first counts its share in a shared-memory table (so the hottest keys of a
+// skewed stream cost one global atomic per CTA, not one per warp: 32K warps
+// incrementing one counter serialise at L2), then merges its distinct keys.
+constexpr int kCountThreads = 512;
+constexpr uint32_t kLocalSlots = 4096;
+
 template <typename KeyT>
-__global__ void hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT* tk, u32* tc, u32 slots) {
+__device__ __forceinline__ void count_global(KeyT* tk, u32* tc, u32 slots, KeyT key, u32 cnt) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t n_pad = (n + 31) & ~31ull;  // whole warps stay in the loop (match_any)
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
-        const KeyT key = i < n ? ld_nc(keys + i) : G::kEmpty;
-        const unsigned peers = __match_any_sync(0xffffffffu, key);
-        if (key == G::kEmpty || (threadIdx.x & 31) != __ffs(peers) - 1) continue;
-        u32 h = (u32)(((u64)((u32)(mix64((u64)key) >> 32)) * slots) >> 32);
-        for (;;) {
-            KeyT cur = tk[h];
-            if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(tk + h), (C)G::kEmpty, (C)key);
-            if (cur == G::kEmpty || cur == key) {
-                atomicAdd(tc + h, (u32)__popc(peers));
-                break;
-            }
-            h = h + 1 == slots ? 0 : h + 1;
+    u32 h = (u32)(((u64)((u32)(mix64((u64)key) >> 32)) * slots) >> 32);
+    for (;;) {
+        KeyT cur = tk[h];
+        if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(tk + h), (C)G::kEmpty, (C)key);
+        if (cur == G::kEmpty || cur == key) {
+            atomicAdd(tc + h, cnt);
+            return;
         }
+        h = h + 1 == slots ? 0 : h + 1;
     }
+}
+
+template <typename KeyT>
+__global__ void __launch_bounds__(kCountThreads) hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT* tk,
+                                                                 u32* tc, u32 slots) {
+    using G = HotGeom<KeyT>;
+    using C = typename G::Cas;
+    __shared__ KeyT lk[kLocalSlots];
+    __shared__ u32 lc[kLocalSlots];
+    for (u32 i = threadIdx.x; i < kLocalSlots; i += kCountThreads) {
+        lk[i] = G::kEmpty;
+        lc[i] = 0;
+    }
+    __syncthreads();
+    const uint64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += kCountThreads) {
+        const KeyT key = ld_nc(keys + i);
+        if (key == G::kEmpty) continue;  // the sentinel key is never hot
+        u32 h = (u32)mix64((u64)key) & (kLocalSlots - 1);
+        bool done = false;
+        for (int probe = 0; probe < 8 && !done; ++probe) {
+            KeyT cur = lk[h];
+            if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(lk + h), (C)G::kEmpty, (C)key);
+            if (cur == G::kEmpty || cur == key) {
+                atomicAdd(lc + h, 1u);
+                done = true;
+            }
+            h = (h + 1) & (kLocalSlots - 1);
+        }
+        if (!done) count_global(tk, tc, slots, key, 1u);  // local table crowded
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < kLocalSlots; i += kCountThreads)
+        if (lc[i]) count_global(tk, tc, slots, lk[i], lc[i]);
 }
 
 __global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist, u32 slots) {
@@ -158,26 +189,36 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
     }
     __syncthreads();
     const u32 t = thr;
-    const int lane = threadIdx.x & 31;
-    // whole warps in the loop (slots is a multiple of 32); one atomic per warp
-    // reserves the selected keys' slots and adds their counts
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x) {
-        const u32 c = tc[s];
-        const bool sel = c >= t;
-        const unsigned m = __ballot_sync(0xffffffffu, sel);
-        if (!m) continue;
-        u32 base = 0;
-        if (lane == 0) base = atomicAdd(hot_count, (u32)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        const u32 idx = base + __popc(m & ((1u << lane) - 1));
-        const bool keep = sel && idx < cap;
-        if (keep) {
-            hot[idx] = tk[s];
+    // each thread scans kSelPer consecutive slots; the CTA's selected keys get
+    // their output range with ONE global atomic (16K selections from warps
+    // hitting one counter serialise at L2)
+    constexpr int kSelPer = 8;
+    __shared__ u32 cta_cnt, cta_sum, cta_base;
+    if (threadIdx.x == 0) cta_cnt = cta_sum = 0;
+    __syncthreads();
+    const uint32_t s0 = (blockIdx.x * blockDim.x + threadIdx.x) * kSelPer;
+    u32 mine = 0;
+#pragma unroll
+    for (int k = 0; k < kSelPer; ++k) mine += (s0 + k < slots && tc[s0 + k] >= t) ? 1u : 0u;
+    const u32 off = mine ? atomicAdd(&cta_cnt, mine) : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) cta_base = cta_cnt ? atomicAdd(hot_count, cta_cnt) : 0;
+    __syncthreads();
+    u32 idx = cta_base + off, covered = 0;
+    for (int k = 0; mine && k < kSelPer; ++k) {
+        const uint32_t sl = s0 + k;
+        const u32 c = sl < slots ? tc[sl] : 0;
+        if (c < t) continue;
+        if (idx < cap) {
+            hot[idx] = tk[sl];
             hot_cnt[idx] = c;
+            covered += c;
         }
-        const u32 covered = __reduce_add_sync(0xffffffffu, keep ? c : 0u);
-        if (lane == 0 && covered) atomicAdd(hot_sum, covered);  // sampled items the hot set covers
+        ++idx;
     }
+    if (covered) atomicAdd(&cta_sum, covered);
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_sum) atomicAdd(hot_sum, cta_sum);  // sampled items the hot set covers
 }
 
 // Exact 64-bit accumulation in two u32 words (|d| <= 2^31).  sm_100 has no
@@ -309,9 +350,9 @@ struct WVec {
 template <int MODE, int K, int SPL, typename KeyT, int WK>
 __global__ void __launch_bounds__(kHotThreads, 1)
     cs_hot_kernel(const SketchParams sp, const KeyT* __restrict__ keys, const void* __restrict__ w, uint64_t n,
-                  i64* __restrict__ table, const KeyT* __restrict__ hot, const u32* __restrict__ hot_cnt,
-                  const u32* __restrict__ hot_count, const u32* __restrict__ hot_sum, uint32_t sample,
-                  const MissBuf<KeyT> mb, bool vec_ok, u32* __restrict__ wraps, u32 band_scale) {
+                  i64* __restrict__ table, const KeyT* __restrict__ layout, u64* __restrict__ slot_sum,
+                  const u32* __restrict__ hot_sum, uint32_t sample, const MissBuf<KeyT> mb, bool vec_ok,
+                  u32* __restrict__ wraps) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
     using KV = KeyVec<KeyT>;
@@ -347,30 +388,14 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         return;
     }
 
+    // every CTA holds the same table layout (hh_layout_kernel), so the slot sums
+    // of all CTAs can be merged per slot before the keys are hashed
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
-        hk[s] = G::kEmpty;
+        hk[s] = layout[s];
         lo[s] = 0x80000000u;
     }
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
-    // Two-choice table, one key per slot: a key goes to slot1 if free, else to
-    // slot2 if free, else it stays cold (exactness never depends on the hot set).
-    // Slots are never freed, so a lookup whose slot1 is empty is a miss without
-    // touching slot2.  Hottest keys are placed first so they own their slot1.
-    const u32 nhot = min(*hot_count, G::kCap);
-    const u32 bands[3] = {64u * band_scale, 8u * band_scale, 0u};  // counts scale with the sample
-    u32 upper = 0xffffffffu;
-    for (int r = 0; r < 3; ++r) {
-        for (u32 j = threadIdx.x; j < nhot; j += kHotThreads) {
-            const u32 c = hot_cnt[j];
-            if (c < bands[r] || c >= upper) continue;
-            const KeyT key = hot[j];
-            if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + slot1<S>(key)), (C)G::kEmpty, (C)key) != G::kEmpty)
-                atomicCAS(reinterpret_cast<C*>(hk + slot2<S>(key)), (C)G::kEmpty, (C)key);
-        }
-        upper = bands[r];
-        __syncthreads();
-    }
 
     int qn = 0;
     unsigned misses = 0, direct = 0;
@@ -491,25 +516,76 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         mb.deltas[p] = 0;
     }
     __syncthreads();
-    unsigned flushed = 0;
+    // this CTA's exact per-slot sums into the shared per-slot totals (wrapping
+    // u64 adds commute); hh_merge_kernel hashes each hot key once
+    unsigned merged = 0;
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
         if (hk[s] == G::kEmpty) continue;
         const u64 v = (((u64)hi[s] << 32) | lo[s]) - 0x80000000ull;
         if (v) {
-            rows_direct<MODE, K, SPL>(sp, (u64)hk[s], (i64)v, table);
-            ++flushed;
+            red_add_u64(slot_sum + s, v);
+            ++merged;
         }
     }
     // instrumentation for the L2-reduction roofline (mb200_hot_stats)
     if (lane == 0) atomicAdd(&g_hot_stats[1], (unsigned long long)misses);
     direct = __reduce_add_sync(kFull, direct);
     if (lane == 0 && direct) atomicAdd(&g_hot_stats[5], (unsigned long long)direct);
-    flushed = __reduce_add_sync(kFull, flushed);
-    if (lane == 0) atomicAdd(&g_hot_stats[2], (unsigned long long)flushed);
-    if (threadIdx.x == 0) {
-        atomicAdd(&g_hot_stats[0], (unsigned long long)((t_hi - t_lo) * kT + (tail_hi - tail_lo)));
-        atomicAdd(&g_hot_stats[3], (unsigned long long)nhot);
+    merged = __reduce_add_sync(kFull, merged);
+    if (lane == 0 && merged) atomicAdd(&g_hot_stats[6], (unsigned long long)merged);
+    if (threadIdx.x == 0) atomicAdd(&g_hot_stats[0], (unsigned long long)((t_hi - t_lo) * kT + (tail_hi - tail_lo)));
+}
+
+// One CTA lays out the hot set in the two-choice table once for every CTA: a key
+// goes to slot1 if free, else to slot2 if free, else it stays cold (exactness
+// never depends on the hot set).  Slots are never freed, and a key only sits in
+// its slot2 when its slot1 was taken first.  Hottest keys are placed first so
+// they own their slot1.
+template <typename KeyT>
+__global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict__ hot, const u32* __restrict__ hot_cnt,
+                                                         const u32* __restrict__ hot_count, u32 band_scale,
+                                                         KeyT* __restrict__ layout) {
+    using G = HotGeom<KeyT>;
+    using C = typename G::Cas;
+    constexpr uint32_t S = G::kSlots;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
+    for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) hk[s] = G::kEmpty;
+    __syncthreads();
+    const u32 nhot = min(*hot_count, G::kCap);
+    const u32 bands[3] = {64u * band_scale, 8u * band_scale, 0u};  // counts scale with the sample
+    u32 upper = 0xffffffffu;
+    for (int r = 0; r < 3; ++r) {
+        for (u32 j = threadIdx.x; j < nhot; j += blockDim.x) {
+            const u32 c = hot_cnt[j];
+            if (c < bands[r] || c >= upper) continue;
+            const KeyT key = hot[j];
+            if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + slot1<S>(key)), (C)G::kEmpty, (C)key) != G::kEmpty)
+                atomicCAS(reinterpret_cast<C*>(hk + slot2<S>(key)), (C)G::kEmpty, (C)key);
+        }
+        upper = bands[r];
+        __syncthreads();
     }
+    for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) layout[s] = hk[s];
+    if (threadIdx.x == 0) atomicAdd(&g_hot_stats[3], (unsigned long long)nhot);
+}
+
+// Each hot key once: hash -> split -> red.global of its total over all CTAs.
+template <int MODE, int K, int SPL, typename KeyT>
+__global__ void hh_merge_kernel(const SketchParams sp, const KeyT* __restrict__ layout,
+                                const u64* __restrict__ slot_sum, i64* __restrict__ table) {
+    using G = HotGeom<KeyT>;
+    unsigned applied = 0;
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < G::kSlots; s += gridDim.x * blockDim.x) {
+        const KeyT key = layout[s];
+        const u64 v = slot_sum[s];
+        if (key != G::kEmpty && v) {
+            rows_direct<MODE, K, SPL>(sp, (u64)key, (i64)v, table);
+            ++applied;
+        }
+    }
+    applied = __reduce_add_sync(kFull, applied);
+    if ((threadIdx.x & 31) == 0 && applied) atomicAdd(&g_hot_stats[2], (unsigned long long)applied);
 }
 
 // ---- passes 4 and 5: binned row updates ------------------------------------
@@ -797,17 +873,20 @@ struct HotPlan {
     uint32_t chunks = 0;       // (pass 4, pass 5) round trips
     uint64_t chunk_items = 0;  // items per round trip
     uint64_t cap_m = 0;        // miss-buffer capacity
-    size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, wraps_bytes = 0, hot_bytes = 0, mk_bytes = 0,
-           md_bytes = 0, bin_bytes = 0;
-    size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes + wraps_bytes; }  // tc .. wraps contiguous
-    size_t total() const { return tk_bytes + zero_bytes() + hot_bytes + mk_bytes + md_bytes + bin_bytes; }
+    size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, wraps_bytes = 0, sum_bytes = 0, hot_bytes = 0,
+           layout_bytes = 0, mk_bytes = 0, md_bytes = 0, bin_bytes = 0;
+    // tc .. slot sums are contiguous and zeroed per call
+    size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes + wraps_bytes + sum_bytes; }
+    size_t total() const {
+        return tk_bytes + zero_bytes() + hot_bytes + layout_bytes + mk_bytes + md_bytes + bin_bytes;
+    }
 };
 
 template <typename KeyT>
 HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     using G = HotGeom<KeyT>;
     HotPlan<KeyT> P;
-    uint64_t m = n / 2048;
+    uint64_t m = n / 256;
     m = m < kMinSample ? kMinSample : m > kMaxSample ? kMaxSample : m;
     P.m = (uint32_t)(n < m ? n : m);
     P.slots = 64;
@@ -844,6 +923,8 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     P.misc = 256 * 4 + 64;  // hist[256], hot_count, hot_sum, miss count (u64)
     P.gcnt_bytes = align256((size_t)P.chunks * g.nb * 8 + 8);
     P.wraps_bytes = align256((size_t)sm_count() * G::kSlots * 4);
+    P.sum_bytes = align256((size_t)G::kSlots * 8);
+    P.layout_bytes = align256((size_t)G::kSlots * sizeof(KeyT));
     P.hot_bytes = align256((size_t)G::kCap * (sizeof(KeyT) + 4));
     P.mk_bytes = align256((size_t)P.cap_m * sizeof(KeyT));
     P.md_bytes = align256((size_t)P.cap_m * 4);
@@ -866,18 +947,22 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     unsigned long long* mcount = reinterpret_cast<unsigned long long*>(hot_count + 2);
     g.gcnt = reinterpret_cast<unsigned long long*>(ws + P.tk_bytes + P.tc_bytes + P.misc);
     u32* wraps = reinterpret_cast<u32*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes);
+    u64* slot_sum = reinterpret_cast<u64*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes + P.wraps_bytes);
     unsigned char* p = ws + P.tk_bytes + P.zero_bytes();
     KeyT* hot = reinterpret_cast<KeyT*>(p);
     u32* hot_cnt = reinterpret_cast<u32*>(hot + G::kCap);
     p += P.hot_bytes;
+    KeyT* layout = reinterpret_cast<KeyT*>(p);
+    p += P.layout_bytes;
     const MissBuf<KeyT> mb{reinterpret_cast<KeyT*>(p), reinterpret_cast<i32*>(p + P.mk_bytes), mcount, P.cap_m};
     p += P.mk_bytes + P.md_bytes;
     g.bins = reinterpret_cast<u32*>(p);
     cudaMemsetAsync(tk, 0xff, P.tk_bytes, s);
     cudaMemsetAsync(tc, 0, P.zero_bytes(), s);
-    hh_count_kernel<KeyT><<<sms * 4, 256, 0, s>>>(keys, P.m, tk, tc, P.slots);
+    hh_count_kernel<KeyT><<<sms * 2, kCountThreads, 0, s>>>(keys, P.m, tk, tc, P.slots);
     hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots);
-    hh_select_kernel<KeyT><<<sms * 8, 256, 0, s>>>(tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum, P.slots);
+    hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(tk, tc, hist, G::kCap, hot, hot_cnt,
+                                                                               hot_count, hot_sum, P.slots);
     auto fn = cs_hot_kernel<MODE, K, SPL, KeyT, WK>;
     const size_t smem = ((size_t)sizeof(KeyT) + 4) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);
@@ -888,8 +973,14 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     const bool vec_ok = (reinterpret_cast<uintptr_t>(keys) & 15) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
     // without bins (cap 0) every miss takes the direct path and raw mode is off
     const u32 band_scale = P.m >= (1u << 18) ? P.m >> 18 : 1;
-    fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, hot, hot_cnt, hot_count, hot_sum,
-                                                          binned ? P.m : 0, mb, vec_ok, wraps, band_scale);
+    auto fl = hh_layout_kernel<KeyT>;
+    const size_t lbytes = sizeof(KeyT) * G::kSlots;
+    if ((e = cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbytes)) != cudaSuccess)
+        return e;
+    fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, band_scale, layout);
+    fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, layout, slot_sum, hot_sum,
+                                                          binned ? P.m : 0, mb, vec_ok, wraps);
+    hh_merge_kernel<MODE, K, SPL, KeyT><<<(G::kSlots + 255) / 256, 256, 0, s>>>(sp, layout, slot_sum, table);
     if ((e = cudaGetLastError()) != cudaSuccess || !binned) return e;
     auto fb_raw = g.bpr == 1 ? cs_bin_kernel<MODE, K, SPL, KeyT, WK, true, true>
                              : cs_bin_kernel<MODE, K, SPL, KeyT, WK, true, false>;

@@ -418,11 +418,11 @@ def main():
                 dist.all_reduce(t)
             return sk.second_moment(True)       # D2H of the estimator
 
-        for _ in range(2):  # first call sizes the pinned-copy pipeline
+        for _ in range(3):  # first call sizes the pinned-copy pipeline; host caches settle
             e2e_step()
         barrier_sync()
         t0 = time.perf_counter()
-        e2e_steps = max(1, min(args.steps, 3))
+        e2e_steps = max(1, min(args.steps, 5))
         step_ms = []
         for _ in range(e2e_steps):
             ts = time.perf_counter()

@@ -372,6 +372,9 @@ HOT_CASES = [
     (2, 65536, 89, 64, 3, "zipf64", None),
     (3, 4096, 61, 64, 0, "zipf64", np.int32),
     (16, 8192, 61, 32, 2, "zipf", np.int32),
+    (3, 65536, 61, 32, 3, "zipf", np.int32),        # two-for-one, odd rows (last family one sub-row)
+    (3, 16384, 89, 64, 0, "zipf64", np.int32),      # 89-bit Pow2
+    (2, 65536, 31, 20, 0, "zipf20", np.int32),      # generic b (runtime splitter)
 ]
 
 
@@ -392,6 +395,8 @@ def test_hot_path_large_batches(cuda, mb, orc, case, strategy):
     keys = zk if kind != "zipf64" else (zk.astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15))
     if kind == "zipf64" and kb < 64:
         keys = keys >> np.uint64(64 - kb)
+    if kind == "zipf20":  # the generic-b domain: keys < 2^20
+        keys = (zk.astype(np.uint64) & np.uint64((1 << 20) - 1)).astype(np.uint64)
     keys[:3] = [0, np.iinfo(keys.dtype).max if kb >= 32 else 1, 0]  # the empty-slot sentinel key
     w = None if wdt is None else zw.astype(wdt)
     if w is not None:

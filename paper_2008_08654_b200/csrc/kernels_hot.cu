@@ -68,7 +68,7 @@ struct HotGeom;
 template <>
 struct HotGeom<u32> {
     static constexpr uint32_t kSlots = 24576;  // x (4 B key + 4 B low sum) = 192 KiB
-    static constexpr uint32_t kCap = 16384;
+    static constexpr uint32_t kCap = 20480;
     static constexpr u32 kEmpty = 0xffffffffu;
     using Cas = unsigned;
 };
@@ -175,7 +175,8 @@ __global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist, u32 slots)
 
 template <typename KeyT>
 __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restrict__ tc, const u32* __restrict__ hist,
-                                 u32 cap, KeyT* hot, u32* hot_cnt, u32* hot_count, u32* hot_sum, u32 slots) {
+                                 u32 cap, KeyT* hot, u32* hot_cnt, u32* hot_count, u32* hot_sum, u32 slots,
+                                 int phase) {
     __shared__ u32 thr, sh[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = hist[i];  // one parallel load
     __syncthreads();
@@ -188,7 +189,11 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
         thr = c + 1;
     }
     __syncthreads();
-    const u32 t = thr;
+    // phase 0: every key with count >= thr (they fit by construction); phase 1
+    // (a second launch, after all of phase 0): keys with count == thr - 1 fill
+    // what capacity is left, first come first served
+    const u32 t = phase == 0 ? thr : thr - 1;
+    if (phase == 1 && t < 2) return;
     // each thread scans kSelPer consecutive slots; the CTA's selected keys get
     // their output range with ONE global atomic (16K selections from warps
     // hitting one counter serialise at L2)
@@ -198,8 +203,12 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
     __syncthreads();
     const uint32_t s0 = (blockIdx.x * blockDim.x + threadIdx.x) * kSelPer;
     u32 mine = 0;
+    const u32 t_hi = phase == 0 ? 0xffffffffu : thr;  // phase 1: exactly count t
 #pragma unroll
-    for (int k = 0; k < kSelPer; ++k) mine += (s0 + k < slots && tc[s0 + k] >= t) ? 1u : 0u;
+    for (int k = 0; k < kSelPer; ++k) {
+        const u32 c = s0 + k < slots ? tc[s0 + k] : 0;
+        mine += (c >= t && c < t_hi) ? 1u : 0u;
+    }
     const u32 off = mine ? atomicAdd(&cta_cnt, mine) : 0;
     __syncthreads();
     if (threadIdx.x == 0) cta_base = cta_cnt ? atomicAdd(hot_count, cta_cnt) : 0;
@@ -208,7 +217,7 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
     for (int k = 0; mine && k < kSelPer; ++k) {
         const uint32_t sl = s0 + k;
         const u32 c = sl < slots ? tc[sl] : 0;
-        if (c < t) continue;
+        if (c < t || c >= t_hi) continue;
         if (idx < cap) {
             hot[idx] = tk[sl];
             hot_cnt[idx] = c;
@@ -961,8 +970,9 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     cudaMemsetAsync(tc, 0, P.zero_bytes(), s);
     hh_count_kernel<KeyT><<<sms * 2, kCountThreads, 0, s>>>(keys, P.m, tk, tc, P.slots);
     hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots);
-    hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(tk, tc, hist, G::kCap, hot, hot_cnt,
-                                                                               hot_count, hot_sum, P.slots);
+    for (int phase = 0; phase < 2; ++phase)
+        hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(
+            tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum, P.slots, phase);
     auto fn = cs_hot_kernel<MODE, K, SPL, KeyT, WK>;
     const size_t smem = ((size_t)sizeof(KeyT) + 4) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);

@@ -226,8 +226,8 @@ int mb200_gen_zipf_items(uint64_t master_seed, const uint64_t* d_cdf, uint32_t T
 /* ------------------------------------------------------------- probes --- */
 /* Counters of the heavy-hitter Count Sketch kernels since the last reset (device-
  * wide, synchronizes the device): [0] items, [1] items that missed the shared-
- * memory hot set, [2] hot keys applied at kernel end (summed over CTAs), [3] hot-set
- * size summed over CTAs, [4] row updates written to HBM bins, [5] row updates
+ * memory hot set, [2] hot keys applied (each once per call), [3] hot keys placed in
+ * the shared table, [4] row updates written to HBM bins, [5] row updates
  * that took the direct red.global path, [6] red.global merges of bin tables,
  * [7] batches binned from the raw stream (no hot pass).  L2 reductions issued =
  * rows x [2] + [5] + [6]. */

@@ -43,10 +43,11 @@
 namespace mb200 {
 
 // per-process counters of the heavy-hitter pipeline: [0] items, [1] misses (items
-// not accumulated in a hot table), [2] hot keys applied at the end, [3] hot-set
-// size (summed over CTAs), [4] entries written to HBM bins, [5] row updates that
-// took the direct red.global path, [6] red.global merges of the bin tables,
-// [7] batches that ran in raw mode (no hot pass)
+// not accumulated in a hot table), [2] hot keys applied (once per call, by
+// hh_merge_kernel), [3] hot keys placed in the shared table, [4] entries written
+// to HBM bins, [5] row updates that took the direct red.global path,
+// [6] red.global merges (per-slot sums of every CTA, bin tables), [7] batches
+// that ran in raw mode (no hot pass)
 __device__ unsigned long long g_hot_stats[8];
 
 namespace {
@@ -575,8 +576,13 @@ __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict_
         upper = bands[r];
         __syncthreads();
     }
-    for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) layout[s] = hk[s];
-    if (threadIdx.x == 0) atomicAdd(&g_hot_stats[3], (unsigned long long)nhot);
+    unsigned placed = 0;
+    for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
+        layout[s] = hk[s];
+        placed += hk[s] != G::kEmpty ? 1u : 0u;
+    }
+    placed = __reduce_add_sync(0xffffffffu, placed);
+    if ((threadIdx.x & 31) == 0 && placed) atomicAdd(&g_hot_stats[3], (unsigned long long)placed);  // keys in the table
 }
 
 // Each hot key once: hash -> split -> red.global of its total over all CTAs.

@@ -418,8 +418,16 @@ def main():
                 dist.all_reduce(t)
             return sk.second_moment(True)       # D2H of the estimator
 
-        for _ in range(3):  # first call sizes the pinned-copy pipeline; host caches settle
+        # untimed warm-up until two consecutive steps agree within 3% (the first calls
+        # size the pinned-copy pipeline; host-side transients settle), at most 8
+        prev_ms = None
+        for _ in range(8):
+            ts = time.perf_counter()
             e2e_step()
+            cur_ms = (time.perf_counter() - ts) * 1e3
+            if prev_ms is not None and abs(cur_ms - prev_ms) <= 0.03 * prev_ms:
+                break
+            prev_ms = cur_ms
         barrier_sync()
         t0 = time.perf_counter()
         e2e_steps = max(1, min(args.steps, 5))

@@ -20,7 +20,7 @@ hk.copy_(dk)
 hw.copy_(dw)
 torch.cuda.synchronize()
 # raw H2D bandwidth of the same bytes
-for _ in range(2):
+for _ in range(4):
     t0 = time.perf_counter()
     dk.copy_(hk, non_blocking=True)
     dw.copy_(hw, non_blocking=True)
@@ -29,7 +29,7 @@ for _ in range(2):
 print(f"raw H2D: {2 * 4 * n / dt / 1e9:.1f} GB/s ({dt * 1e3:.1f} ms)")
 sk = mb.CountSketch(5, 1 << 16, 61, 32, mb.SPLIT_POW2, 1)
 hk_np, hw_np = hk.numpy(), hw.numpy()
-for rep in range(3):
+for rep in range(8):
     t0 = time.perf_counter()
     sk.process(hk_np, hw_np)
     dt = time.perf_counter() - t0

@@ -425,7 +425,12 @@ def main():
             ts = time.perf_counter()
             e2e_step()
             cur_ms = (time.perf_counter() - ts) * 1e3
-            if prev_ms is not None and abs(cur_ms - prev_ms) <= 0.03 * prev_ms:
+            stable = prev_ms is not None and abs(cur_ms - prev_ms) <= 0.03 * prev_ms
+            if world > 1:  # every rank leaves together (e2e_step holds a collective)
+                flag = torch.tensor([1 if stable else 0], dtype=torch.int32, device=dev)
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+                stable = bool(flag.item())
+            if stable:
                 break
             prev_ms = cur_ms
         barrier_sync()

@@ -622,7 +622,7 @@ def test_generators_match_oracle(cuda, mb, orc):
 
 # ---------------------------------------------------------------- full BASELINE sizes
 @pytest.mark.slow
-def test_full_size_c2_sampled(cuda, mb, orc):
+def test_full_size_c2(cuda, mb, orc):
     import torch
 
     n = 1 << 28
@@ -632,27 +632,27 @@ def test_full_size_c2_sampled(cuda, mb, orc):
         c = orc.coeffs(61, k, 1)
         out = mb.hash61(keys, c, key_bits=64)
         assert bool((out >= 0).all()) and bool((out < P61).all())  # fully reduced
-        idx = torch.randint(0, n, (1 << 18,), device="cuda")
-        exp = orc.hash_full(61, c, host_u64(keys[idx]))
-        assert (host_u64(out[idx]) == exp).all()
-        head = orc.hash_full(61, c, host_u64(keys[:1 << 20]))
-        assert (host_u64(out[:1 << 20]) == head).all()
+        # every one of the 2^28 hashes against the (OpenMP) oracle, in 2^26 chunks
+        for s0 in range(0, n, 1 << 26):
+            exp = orc.hash_full(61, c, host_u64(keys[s0:s0 + (1 << 26)]))
+            assert (host_u64(out[s0:s0 + (1 << 26)]) == exp).all()
         del out
     del keys
 
 
 @pytest.mark.slow
-def test_full_size_c3_sampled(cuda, mb, orc):
+def test_full_size_c3(cuda, mb, orc):
     import torch
 
     n = 1 << 28
     v, bad = mb.gen_pm_inputs(1 ^ mb.SALT_KEYS, 59, 0, n)
     assert int(bad.item()) == 0
     q, r = mb.pm_divmod(v, 64, 59)
-    idx = torch.randint(0, n, (1 << 18,), device="cuda")
-    flat = v[idx].cpu().numpy().reshape(-1).view(np.uint64)
-    eq, er, _ = orc.pm_divmod_batch(64, 59, flat)
-    assert (host_u64(q[idx]) == eq).all() and (host_u64(r[idx]) == er).all()
+    # every one of the 2^28 quotients and remainders against the oracle, in 2^26 chunks
+    for s0 in range(0, n, 1 << 26):
+        flat = v[s0:s0 + (1 << 26)].cpu().numpy().reshape(-1).view(np.uint64)
+        eq, er, _ = orc.pm_divmod_batch(64, 59, flat)
+        assert (host_u64(q[s0:s0 + (1 << 26)]) == eq).all() and (host_u64(r[s0:s0 + (1 << 26)]) == er).all()
     # size-independent property on every unit: r < p (u64 compare via sign flip)
     p = (1 << 64) - 59
     rr = r ^ (-(1 << 63))
@@ -690,6 +690,25 @@ def test_full_size_c1_and_c5(cuda, mb, orc):
     assert (cnt.cpu().numpy() == exp).all()
     m = mb.moments_to_python(mb.cs_moments(cnt, 5, 65536))
     assert mb.lower_median(m) == orc.second_moment(exp, 5, 65536, True)
+
+
+@pytest.mark.slow
+def test_full_size_c4(cuda, mb, orc):
+    """Config 4 in full: 2^26 u64 keys through one 89-bit family split two-for-one into
+    two rows of 2^16 counters, one call, against the oracle; both row moments."""
+    import torch
+
+    n = 1 << 26
+    keys = mb.gen_u64_keys(1 ^ mb.SALT_KEYS, 0, n)
+    c = orc.coeffs(89, 4, 1)
+    spec = mb.SketchSpec(2, 1 << 16, 89, [c], 64, mb.SPLIT_TWO_FOR_ONE)
+    cnt = torch.zeros(2 << 16, dtype=torch.int64, device="cuda")
+    mb.cs_update(spec, keys, cnt)
+    exp = orc.cs_process(2, 1 << 16, 89, [c], 64, 3, host_u64(keys))
+    assert (cnt.cpu().numpy() == exp).all()
+    m = mb.moments_to_python(mb.cs_moments(cnt, 2, 1 << 16))
+    for r in range(2):
+        assert m[r] == orc.row_moment(exp[r << 16:(r + 1) << 16], 1 << 16)
 
 
 # ---------------------------------------------------------------- moment enumeration

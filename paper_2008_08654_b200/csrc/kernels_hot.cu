@@ -127,11 +127,56 @@ __device__ __forceinline__ void count_global(KeyT* tk, u32* tc, u32 slots, KeyT 
     }
 }
 
+// Quick look at the batch's first kProbeItems items in one CTA: if keys seen at
+// least twice cover under 1/32 of them (a stream without heavy hitters, like
+// config 4's uniform 64-bit keys), the sample / selection kernels are skipped
+// (*go = 0) and every item takes the direct path.  Performance only.
+constexpr uint32_t kProbeItems = 1u << 14;
+
 template <typename KeyT>
-__global__ void __launch_bounds__(kCountThreads) hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT* tk,
-                                                                 u32* tc, u32 slots) {
+__global__ void __launch_bounds__(1024) hh_probe_kernel(const KeyT* __restrict__ keys, uint64_t n, u32* go) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
+    constexpr u32 kProbeSlots = kLocalSlots / 2;  // 2^14 items at most half distinct-heavy
+    __shared__ KeyT lk[kProbeSlots];
+    __shared__ u32 lc[kProbeSlots];
+    __shared__ u32 covered;
+    for (u32 i = threadIdx.x; i < kProbeSlots; i += blockDim.x) {
+        lk[i] = G::kEmpty;
+        lc[i] = 0;
+    }
+    if (threadIdx.x == 0) covered = 0;
+    __syncthreads();
+    const u32 m = (u32)(n < kProbeItems ? n : kProbeItems);
+    for (u32 i = threadIdx.x; i < m; i += blockDim.x) {
+        const KeyT key = ld_nc(keys + i);
+        if (key == G::kEmpty) continue;
+        u32 h = (u32)mix64((u64)key) & (kProbeSlots - 1);
+        for (int probe = 0; probe < 8; ++probe) {  // a crowded table just drops the item
+            KeyT cur = lk[h];
+            if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(lk + h), (C)G::kEmpty, (C)key);
+            if (cur == G::kEmpty || cur == key) {
+                atomicAdd(lc + h, 1u);
+                break;
+            }
+            h = (h + 1) & (kProbeSlots - 1);
+        }
+    }
+    __syncthreads();
+    u32 mine = 0;
+    for (u32 i = threadIdx.x; i < kProbeSlots; i += blockDim.x) mine += lc[i] >= 2 ? lc[i] : 0;
+    mine = __reduce_add_sync(0xffffffffu, mine);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&covered, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) *go = covered * 32 >= m ? 1u : 0u;
+}
+
+template <typename KeyT>
+__global__ void __launch_bounds__(kCountThreads) hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT* tk,
+                                                                 u32* tc, u32 slots, const u32* __restrict__ go) {
+    using G = HotGeom<KeyT>;
+    using C = typename G::Cas;
+    if (!*go) return;
     __shared__ KeyT lk[kLocalSlots];
     __shared__ u32 lc[kLocalSlots];
     for (u32 i = threadIdx.x; i < kLocalSlots; i += kCountThreads) {
@@ -161,7 +206,8 @@ __global__ void __launch_bounds__(kCountThreads) hh_count_kernel(const KeyT* __r
         if (lc[i]) count_global(tk, tc, slots, lk[i], lc[i]);
 }
 
-__global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist, u32 slots) {
+__global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist, u32 slots, const u32* __restrict__ go) {
+    if (!*go) return;
     __shared__ u32 sh[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
     __syncthreads();
@@ -177,7 +223,8 @@ __global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist, u32 slots)
 template <typename KeyT>
 __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restrict__ tc, const u32* __restrict__ hist,
                                  u32 cap, KeyT* hot, u32* hot_cnt, u32* hot_count, u32* hot_sum, u32 slots,
-                                 int phase) {
+                                 int phase, const u32* __restrict__ go) {
+    if (!*go) return;
     __shared__ u32 thr, sh[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = hist[i];  // one parallel load
     __syncthreads();
@@ -974,11 +1021,13 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     g.bins = reinterpret_cast<u32*>(p);
     cudaMemsetAsync(tk, 0xff, P.tk_bytes, s);
     cudaMemsetAsync(tc, 0, P.zero_bytes(), s);
-    hh_count_kernel<KeyT><<<sms * 2, kCountThreads, 0, s>>>(keys, P.m, tk, tc, P.slots);
-    hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots);
+    u32* go = hot_count + 4;  // misc word after the miss count
+    hh_probe_kernel<KeyT><<<1, 1024, 0, s>>>(keys, n, go);
+    hh_count_kernel<KeyT><<<sms * 2, kCountThreads, 0, s>>>(keys, P.m, tk, tc, P.slots, go);
+    hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots, go);
     for (int phase = 0; phase < 2; ++phase)
         hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(
-            tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum, P.slots, phase);
+            tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum, P.slots, phase, go);
     auto fn = cs_hot_kernel<MODE, K, SPL, KeyT, WK>;
     const size_t smem = ((size_t)sizeof(KeyT) + 4) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);

@@ -404,7 +404,7 @@ struct WVec {
     }
 };
 
-template <int MODE, int K, int SPL, typename KeyT, int WK>
+template <int MODE, int K, int SPL, typename KeyT, int WK, bool BUF>
 __global__ void __launch_bounds__(kHotThreads, 1)
     cs_hot_kernel(const SketchParams sp, const KeyT* __restrict__ keys, const void* __restrict__ w, uint64_t n,
                   i64* __restrict__ table, const KeyT* __restrict__ layout, u64* __restrict__ slot_sum,
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     const uint64_t rest = n - ntiles_all * kT;
     const uint64_t tail_lo = ntiles_all * kT + rest * blockIdx.x / gridDim.x;
     const uint64_t tail_hi = ntiles_all * kT + rest * (blockIdx.x + 1) / gridDim.x;
-    if (mb.cap != 0 && raw_mode(hot_sum, sample)) {  // the binning pass reads the stream itself
+    if (BUF && raw_mode(hot_sum, sample)) {  // the binning pass reads the stream itself
         if (threadIdx.x == 0) {
             const uint64_t cnt = (t_hi - t_lo) * kT + (tail_hi - tail_lo);
             atomicAdd(&g_hot_stats[0], (unsigned long long)cnt);
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         }
         qn += __popc(m);
         misses += __popc(m);
-        if (qn >= 32 && mb.cap == 0) {  // a full warp of misses -> hash, split, red.global
+        if (!BUF && qn >= 32) {  // a full warp of misses -> hash, split, red.global
             __syncwarp();
             misses_direct<MODE, K, SPL, KeyT>(sp, wqk[lane], wqd[lane], true, table);
             direct += sp.rows;
@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
             }
             __syncwarp();
             qn -= 32;
-        } else if (qn >= 32) {  // a full warp of misses -> 32 slots of the miss buffer
+        } else if (BUF && qn >= 32) {  // a full warp of misses -> 32 slots of the miss buffer
             __syncwarp();
             if (wfill == kMissChunk) {
                 if (lane == 0) wbase = atomicAdd(mb.count, (unsigned long long)kMissChunk);
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         direct += sp.rows;
     }
     // unused reserved slots become no-op items (delta 0)
-    for (unsigned long long p = wbase + wfill + lane; p < wbase + kMissChunk && p < mb.cap; p += 32) {
+    for (unsigned long long p = wbase + wfill + lane; BUF && p < wbase + kMissChunk && p < mb.cap; p += 32) {
         mb.keys[p] = 0;
         mb.deltas[p] = 0;
     }
@@ -1028,7 +1028,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     for (int phase = 0; phase < 2; ++phase)
         hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(
             tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum, P.slots, phase, go);
-    auto fn = cs_hot_kernel<MODE, K, SPL, KeyT, WK>;
+    auto fn = binned ? cs_hot_kernel<MODE, K, SPL, KeyT, WK, true> : cs_hot_kernel<MODE, K, SPL, KeyT, WK, false>;
     const size_t smem = ((size_t)sizeof(KeyT) + 4) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes));

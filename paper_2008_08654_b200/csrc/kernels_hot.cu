@@ -346,6 +346,13 @@ __device__ __forceinline__ void rows_direct(const SketchParams& sp, u64 x, i64 d
     uint64_t* base = reinterpret_cast<uint64_t*>(table);
 #pragma unroll 1
     for (uint32_t f = 0; f < sp.families; ++f) {
+        if constexpr ((MODE == M61_K32 || MODE == M61_K64) && K > 0 && SPL == SPC_POW2) {
+            // Pow2 split straight from the lazily reduced Horner value
+            bool neg;
+            const u32 idx = h61_pow2_split(hash61_lazy<MODE, K>(sp, f, x), (u32)(sp.width - 1), neg);
+            red_add_u64(base + (u64)f * sp.width + idx, neg ? dn : dp);
+            continue;
+        }
         u64 hlo, hhi = 0;
         if (MODE == M89) hash89<K>(sp, f, x, hlo, hhi);
         else hlo = hash_small<MODE, K>(sp, f, x);

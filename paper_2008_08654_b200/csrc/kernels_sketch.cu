@@ -165,9 +165,10 @@ __device__ __forceinline__ void small_vec(const SketchParams& sp, const u64* c, 
     const u32 mask = (u32)(sp.width - 1);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-        const u64 h = h61_finish(y[u]);  // < p: index = low bits, sign = bit 60 (sketch.cpp:13-19)
+        bool neg;  // index = low bits, sign = bit 60 of y mod p (sketch.cpp:13-19)
+        const u32 idx = h61_pow2_split(y[u], mask, neg);
         const u64 d = WK == W_NONE ? 1ull : (u64)(i64)ww[u];
-        table_add<STRAT>(smem, nullptr, lo32(h) & mask, ((hi32(h) >> 28) & 1) ? 0ull - d : d);
+        table_add<STRAT>(smem, nullptr, idx, neg ? 0ull - d : d);
     }
 }
 

@@ -67,6 +67,18 @@ __device__ __forceinline__ u64 h61_finish(u64 y) {
     return (y + z) & kP61;
 }
 
+// Alg 2 with b = 61 and a power-of-two width straight from a lazily reduced
+// y < 2^64 (sketch.cpp:13-19 on h = y mod p): after one fold y < 2^61 + 8, and
+// z = (y + 1) >> 61 is 1 exactly when y >= p, in which case h = y - p < 8 (its
+// low word is lo32(y) + 1, its bit 60 is 0).  Returns the bucket (mask < 2^32)
+// and sets neg = bit 60 of h.  Two ALU ops fewer than h61_finish + split.
+__device__ __forceinline__ u32 h61_pow2_split(u64 y, u32 mask, bool& neg) {
+    y = h61_fold(y);
+    const u32 z = (u32)((y + 1) >> 61);
+    neg = ((hi32(y) >> 28) & ~z) & 1u;
+    return (lo32(y) + z) & mask;
+}
+
 // ---------------------------------------------------------------------------
 // p = 2^61 - 1, any 64-bit key (config 2 draws keys from [0, p), beyond the
 // reference's u <= 2^60 domain; SURVEY 7.3 hard part 2).  Keys are folded once

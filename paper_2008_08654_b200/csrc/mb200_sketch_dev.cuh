@@ -53,6 +53,22 @@ __device__ __forceinline__ u64 hash_small(const SketchParams& sp, uint32_t f, u6
     }
 }
 
+// 2^61-1 hash of family f before the final reduction (any value < 2^64 that is
+// congruent to the hash mod p): for splitters that reduce on their own.
+template <int MODE, int K>
+__device__ __forceinline__ u64 hash61_lazy(const SketchParams& sp, uint32_t f, u64 x) {
+    static_assert(MODE == M61_K32 || MODE == M61_K64, "2^61-1 modes only");
+    const u64* c = sp.lo + (size_t)f * sp.k;
+    if (MODE == M61_K32) {
+        const u32 xs = (u32)x;
+        u64 y = c[K - 1];
+#pragma unroll
+        for (int i = K - 2; i >= 0; --i) y = h61_step32(y, xs, c[i]);
+        return y;
+    }
+    return h61_eval64<K>(c, h61_key64(x));
+}
+
 // 89-bit hash of family f as (lo 64 bits, hi 25 bits).
 template <int K>
 __device__ __forceinline__ void hash89(const SketchParams& sp, uint32_t f, u64 x, u64& lo, u64& hi) {

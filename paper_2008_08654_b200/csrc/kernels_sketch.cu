@@ -159,7 +159,9 @@ __device__ __forceinline__ void small_vec(const SketchParams& sp, const u64* c, 
 #pragma unroll
     for (int u = 0; u < 4; ++u) y[u] = c[K - 1];
 #pragma unroll
-    for (int i = K - 2; i >= 0; --i)
+    for (int u = 0; u < 4; ++u) y[u] = h61_step32_first(y[u], kk[u], c[K - 2]);
+#pragma unroll
+    for (int i = K - 3; i >= 0; --i)
 #pragma unroll
         for (int u = 0; u < 4; ++u) y[u] = h61_step32(y[u], kk[u], c[i]);
     const u32 mask = (u32)(sp.width - 1);

@@ -57,6 +57,30 @@ __device__ __forceinline__ u64 h61_step32(u64 y, u32 x, u64 a) {
     return lo + hi + a;
 }
 
+// The first step of a chain, y = a_{k-1} < 2^61: y x < 2^93, so (y x) >> 61 fits
+// one 32-bit word and its high word is zero (one ALU op fewer).  Same output.
+__device__ __forceinline__ u64 h61_step32_first(u64 y, u32 x, u64 a) {
+    u64 lo, hi;
+    asm("{\n\t"
+        ".reg .u32 y0, y1, A0, A1, B0, B1, m, t, s0;\n\t"
+        ".reg .u64 A, B;\n\t"
+        "mov.b64 {y0, y1}, %2;\n\t"
+        "mul.wide.u32 A, y0, %3;\n\t"
+        "mul.wide.u32 B, y1, %3;\n\t"
+        "mov.b64 {A0, A1}, A;\n\t"
+        "mov.b64 {B0, B1}, B;\n\t"
+        "add.cc.u32 m, A1, B0;\n\t"
+        "addc.u32 t, B1, 0;\n\t"
+        "shf.r.clamp.b32 s0, m, t, 29;\n\t"
+        "and.b32 m, m, 0x1FFFFFFF;\n\t"
+        "mov.b64 %0, {A0, m};\n\t"
+        "mov.b64 %1, {s0, 0};\n\t"
+        "}"
+        : "=l"(lo), "=l"(hi)
+        : "l"(y), "r"(x));
+    return lo + hi + a;
+}
+
 // Full reduction of a lazily reduced value y < 2^64 to [0, p): one fold to
 // < 2^61 + 8 < 2p, then the reference's branch-free finish
 // z = (y + 1) >> b; (y + z) & p   (polyhash.cpp:74-75).

@@ -61,9 +61,10 @@ __device__ __forceinline__ u64 hash61_lazy(const SketchParams& sp, uint32_t f, u
     const u64* c = sp.lo + (size_t)f * sp.k;
     if (MODE == M61_K32) {
         const u32 xs = (u32)x;
-        u64 y = c[K - 1];
+        if (K < 2) return c[0];
+        u64 y = h61_step32_first(c[K - 1], xs, c[K - 2]);
 #pragma unroll
-        for (int i = K - 2; i >= 0; --i) y = h61_step32(y, xs, c[i]);
+        for (int i = K - 3; i >= 0; --i) y = h61_step32(y, xs, c[i]);
         return y;
     }
     return h61_eval64<K>(c, h61_key64(x));

@@ -7,12 +7,16 @@
 // L2 and the lever is the NUMBER of L2 reductions.  Count Sketch is linear:
 // the updates of one key can be summed anywhere and applied once.
 //
-//   1. hh_count  : exact key counts over a sample (the batch's first 2^20 items)
-//                  in an open-addressing table in global memory;
+//   1. hh_count  : exact key counts over a sample (the batch's first n/256
+//                  items, clamped to [2^18, 2^22]) in an open-addressing table
+//                  in global memory;
 //   2. hh_hist /
 //      hh_select : the most frequent sampled keys (count >= a threshold picked
 //                  from the count histogram so that at most H qualify) form the
 //                  hot list, with their sample counts;
+//      hh_layout : one CTA places the hot list, hottest first, in the two-choice
+//                  shared table layout every CTA copies (one level of cuckoo
+//                  displacement; ~22.5K of 32K candidates in 24576 slots);
 //   3. cs_hot    : one 1024-thread CTA per SM keeps the hot keys in a shared-
 //                  memory table with an exact 64-bit accumulator per key.  A hit
 //                  costs one shared reduction and no hashing.  Misses are
@@ -54,11 +58,13 @@ namespace {
 
 using namespace sk;
 
+
+
 constexpr int kHotThreads = 1024;
 constexpr int kHotWarps = kHotThreads / 32;
-// sample = n / 256 items, clamped to [2^18, 2^20] (a shard of a multi-GPU run
-// still gets the full-size hot set from 2^28 items on); count table = 2 x sample
-constexpr uint32_t kMinSample = 1u << 18, kMaxSample = 1u << 20;
+// sample = n / 256 items, clamped to [2^18, 2^22] (a shard of a multi-GPU run
+// gets a 2^20-item sample from 2^28 items on); count table = 2 x sample
+constexpr uint32_t kMinSample = 1u << 18, kMaxSample = 1u << 22;
 constexpr int kQueue = 64;     // < 32 queued + one slot of 32 misses
 constexpr uint32_t kMissChunk = 1024;  // miss-buffer slots a warp reserves at once
 
@@ -69,7 +75,7 @@ struct HotGeom;
 template <>
 struct HotGeom<u32> {
     static constexpr uint32_t kSlots = 24576;  // x (4 B key + 4 B low sum) = 192 KiB
-    static constexpr uint32_t kCap = 20480;
+    static constexpr uint32_t kCap = 32768;  // selected candidates (the layout places ~22.5K)
     static constexpr u32 kEmpty = 0xffffffffu;
     using Cas = unsigned;
 };
@@ -600,34 +606,88 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     if (threadIdx.x == 0) atomicAdd(&g_hot_stats[0], (unsigned long long)((t_hi - t_lo) * kT + (tail_hi - tail_lo)));
 }
 
-// One CTA lays out the hot set in the two-choice table once for every CTA: a key
-// goes to slot1 if free, else to slot2 if free, else it stays cold (exactness
-// never depends on the hot set).  Slots are never freed, and a key only sits in
-// its slot2 when its slot1 was taken first.  Hottest keys are placed first so
-// they own their slot1.
+// One CTA lays out the hot set in the two-choice table once for every CTA.
+// The selected keys are first ordered by sample count, hottest first (counting
+// sort over kLevels count levels, counts >= kLevels - 1 share the top level),
+// then placed in that order, 1024 at a time: a key goes to slot1 if free, else
+// to slot2 if free; if both are taken, one level of cuckoo displacement moves
+// the occupant of either slot to ITS other slot when that one is free.  Keys
+// that still find no slot stay cold.  Exactness never depends on the layout:
+// a lookup picks slot1 if it holds the key, else slot2, else the item is a miss,
+// and hh_merge credits each slot's sum to the key stored there.
+constexpr u32 kLevels = 1024;
+
+template <typename KeyT>
+__device__ __forceinline__ u32 other_slot(KeyT k, u32 s) {
+    using G = HotGeom<KeyT>;
+    const u32 s1 = slot1<G::kSlots>(k);
+    return s1 == s ? slot2<G::kSlots>(k) : s1;
+}
+
 template <typename KeyT>
 __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict__ hot, const u32* __restrict__ hot_cnt,
-                                                         const u32* __restrict__ hot_count, u32 band_scale,
+                                                         const u32* __restrict__ hot_count, u32 cap,
                                                          KeyT* __restrict__ layout) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
     constexpr uint32_t S = G::kSlots;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
+    uint16_t* order = reinterpret_cast<uint16_t*>(hk + S);
+    __shared__ u32 lev[kLevels];
     for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) hk[s] = G::kEmpty;
+    for (uint32_t l = threadIdx.x; l < kLevels; l += blockDim.x) lev[l] = 0;
     __syncthreads();
-    const u32 nhot = min(*hot_count, G::kCap);
-    const u32 bands[3] = {64u * band_scale, 8u * band_scale, 0u};  // counts scale with the sample
-    u32 upper = 0xffffffffu;
-    for (int r = 0; r < 3; ++r) {
-        for (u32 j = threadIdx.x; j < nhot; j += blockDim.x) {
-            const u32 c = hot_cnt[j];
-            if (c < bands[r] || c >= upper) continue;
-            const KeyT key = hot[j];
-            if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + slot1<S>(key)), (C)G::kEmpty, (C)key) != G::kEmpty)
-                atomicCAS(reinterpret_cast<C*>(hk + slot2<S>(key)), (C)G::kEmpty, (C)key);
+    const u32 nhot = min(*hot_count, cap);
+    // level index kLevels - 1 - min(count, kLevels - 1): ascending index = descending count
+    auto level = [](u32 c) { return kLevels - 1 - min(c, kLevels - 1); };
+    for (u32 j = threadIdx.x; j < nhot; j += blockDim.x) atomicAdd(&lev[level(hot_cnt[j])], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the level counts, 32 per lane
+        constexpr u32 kPer = kLevels / 32;
+        u32 v[kPer], run = 0;
+#pragma unroll
+        for (u32 i = 0; i < kPer; ++i) {
+            v[i] = run;
+            run += lev[threadIdx.x * kPer + i];
         }
-        upper = bands[r];
+        u32 inc = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (threadIdx.x >= (u32)o) inc += t;
+        }
+        const u32 base = inc - run;
+#pragma unroll
+        for (u32 i = 0; i < kPer; ++i) lev[threadIdx.x * kPer + i] = base + v[i];
+    }
+    __syncthreads();
+    for (u32 j = threadIdx.x; j < nhot; j += blockDim.x) order[atomicAdd(&lev[level(hot_cnt[j])], 1u)] = (uint16_t)j;
+    __syncthreads();
+    for (u32 base = 0; base < nhot; base += blockDim.x) {
+        const u32 j = base + threadIdx.x;
+        const KeyT key = j < nhot ? hot[order[j]] : G::kEmpty;
+        bool left = false;
+        if (j < nhot && key != G::kEmpty) {
+            const u32 s1 = slot1<S>(key), s2 = slot2<S>(key);
+            left = (KeyT)atomicCAS(reinterpret_cast<C*>(hk + s1), (C)G::kEmpty, (C)key) != G::kEmpty &&
+                   (KeyT)atomicCAS(reinterpret_cast<C*>(hk + s2), (C)G::kEmpty, (C)key) != G::kEmpty;
+        }
+        __syncthreads();
+        if (left) {  // one level of displacement (races only cost a slot, never exactness)
+            const u32 s1 = slot1<S>(key), s2 = slot2<S>(key);
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const u32 sl = t == 0 ? s1 : s2;
+                const KeyT occ = hk[sl];
+                if (occ == G::kEmpty || occ == key) break;
+                const u32 alt = other_slot<KeyT>(occ, sl);
+                if (alt == sl) continue;
+                if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + alt), (C)G::kEmpty, (C)occ) != G::kEmpty) continue;
+                atomicCAS(reinterpret_cast<C*>(hk + sl), (C)occ, (C)key);
+                break;
+            }
+        }
         __syncthreads();
     }
     unsigned placed = 0;
@@ -1029,12 +1089,13 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     cudaMemsetAsync(tk, 0xff, P.tk_bytes, s);
     cudaMemsetAsync(tc, 0, P.zero_bytes(), s);
     u32* go = hot_count + 4;  // misc word after the miss count
+    const u32 cap = G::kCap;
     hh_probe_kernel<KeyT><<<1, 1024, 0, s>>>(keys, n, go);
     hh_count_kernel<KeyT><<<sms * 2, kCountThreads, 0, s>>>(keys, P.m, tk, tc, P.slots, go);
     hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots, go);
     for (int phase = 0; phase < 2; ++phase)
         hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(
-            tk, tc, hist, G::kCap, hot, hot_cnt, hot_count, hot_sum, P.slots, phase, go);
+            tk, tc, hist, cap, hot, hot_cnt, hot_count, hot_sum, P.slots, phase, go);
     auto fn = binned ? cs_hot_kernel<MODE, K, SPL, KeyT, WK, true> : cs_hot_kernel<MODE, K, SPL, KeyT, WK, false>;
     const size_t smem = ((size_t)sizeof(KeyT) + 4) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);
@@ -1044,12 +1105,11 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     if (grid > (uint64_t)sms) grid = sms;
     const bool vec_ok = (reinterpret_cast<uintptr_t>(keys) & 15) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
     // without bins (cap 0) every miss takes the direct path and raw mode is off
-    const u32 band_scale = P.m >= (1u << 18) ? P.m >> 18 : 1;
     auto fl = hh_layout_kernel<KeyT>;
-    const size_t lbytes = sizeof(KeyT) * G::kSlots;
+    const size_t lbytes = sizeof(KeyT) * G::kSlots + 2 * G::kCap;
     if ((e = cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbytes)) != cudaSuccess)
         return e;
-    fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, band_scale, layout);
+    fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, cap, layout);
     fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, layout, slot_sum, hot_sum,
                                                           binned ? P.m : 0, mb, vec_ok, wraps);
     hh_merge_kernel<MODE, K, SPL, KeyT><<<(G::kSlots + 255) / 256, 256, 0, s>>>(sp, layout, slot_sum, table);

@@ -31,53 +31,60 @@ __device__ __forceinline__ u32 hi32(u64 v) { return (u32)(v >> 32); }
 // One Horner step y <- y x + a, lazily reduced:
 //   in  y < 2^63, x < 2^32, a < p
 //   out (yx & p) + (yx >> 61) + a  <  2^61 + 2^34 + 2^61  <  2^63   (closed)
-// Two limb products (IMAD.WIDE.U32) A = y0 x, B = y1 x; y x = A + B 2^32 with
-// bits 32..63 = A1 + B0 (carry c) and bits 64..94 = B1 + c < 2^31; the fold is
-// one carry chain, the three-term sum one 3-input add pair (IADD3, IADD3.X).
+// Two limb products A = y0 x, B = y1 x; y x = A + B 2^32, and (y x) >> 32 =
+// B + A1 < 2^63 + 2^32 is ONE mad.wide (no carry chain).  The fold takes the
+// shift (t1, t2) >> 29 and the mask of t1, the three-term sum is one 3-input
+// add pair (IADD3, IADD3.X).  Per step: 3 IMAD.WIDE + 1 IMAD.HI on the FMA
+// pipe, 4 ops on the ALU pipe (was 3 + 6: the carry chain and the t2 >> 29
+// shift ran on the ALU pipe, the binding one of the hash kernels).
+// The two multipliers 1 (B + A1 as mad.wide A1 * 1 + y1 x) and 8
+// (t2 >> 29 = hi32(8 t2)) are runtime values from constant memory, so ptxas
+// cannot strength-reduce them back into ALU adds and shifts.
+static __constant__ u32 kFmaOne = 1;
+static __constant__ u32 kFmaEight = 8;
+
 __device__ __forceinline__ u64 h61_step32(u64 y, u32 x, u64 a) {
     u64 lo, hi;
     asm("{\n\t"
-        ".reg .u32 y0, y1, A0, A1, B0, B1, m, t, s0, s1;\n\t"
+        ".reg .u32 y0, y1, A0, A1, t1, t2, h0, h1;\n\t"
         ".reg .u64 A, B;\n\t"
         "mov.b64 {y0, y1}, %2;\n\t"
         "mul.wide.u32 A, y0, %3;\n\t"
-        "mul.wide.u32 B, y1, %3;\n\t"
         "mov.b64 {A0, A1}, A;\n\t"
-        "mov.b64 {B0, B1}, B;\n\t"
-        "add.cc.u32 m, A1, B0;\n\t"          // bits 32..63 of y x
-        "addc.u32 t, B1, 0;\n\t"             // bits 64..94
-        "shf.r.clamp.b32 s0, m, t, 29;\n\t"  // (y x) >> 61
-        "shr.u32 s1, t, 29;\n\t"
-        "and.b32 m, m, 0x1FFFFFFF;\n\t"      // (y x) & p, high word
-        "mov.b64 %0, {A0, m};\n\t"
-        "mov.b64 %1, {s0, s1};\n\t"
+        "mul.wide.u32 B, A1, %4;\n\t"      // A1 (times the runtime 1)
+        "mad.wide.u32 B, y1, %3, B;\n\t"   // (y x) >> 32 = (t1, t2) < 2^63 + 2^32
+        "mov.b64 {t1, t2}, B;\n\t"
+        "shf.r.clamp.b32 h0, t1, t2, 29;\n\t"  // (y x) >> 61
+        "mul.hi.u32 h1, t2, %5;\n\t"           // t2 >> 29 = hi32(8 t2)
+        "and.b32 t1, t1, 0x1FFFFFFF;\n\t"      // (y x) & p, high word
+        "mov.b64 %0, {A0, t1};\n\t"
+        "mov.b64 %1, {h0, h1};\n\t"
         "}"
         : "=l"(lo), "=l"(hi)
-        : "l"(y), "r"(x));
+        : "l"(y), "r"(x), "r"(kFmaOne), "r"(kFmaEight));
     return lo + hi + a;
 }
 
-// The first step of a chain, y = a_{k-1} < 2^61: y x < 2^93, so (y x) >> 61 fits
-// one 32-bit word and its high word is zero (one ALU op fewer).  Same output.
+// The first step of a chain, y = a_{k-1} < 2^61: y1 x + A1 <= (2^29 - 1)(2^32 - 1)
+// + 2^32 - 1 < 2^61, so t2 < 2^29 and (y x) >> 61 fits one word (no IMAD.HI).
 __device__ __forceinline__ u64 h61_step32_first(u64 y, u32 x, u64 a) {
     u64 lo, hi;
     asm("{\n\t"
-        ".reg .u32 y0, y1, A0, A1, B0, B1, m, t, s0;\n\t"
+        ".reg .u32 y0, y1, A0, A1, t1, t2, h0;\n\t"
         ".reg .u64 A, B;\n\t"
         "mov.b64 {y0, y1}, %2;\n\t"
         "mul.wide.u32 A, y0, %3;\n\t"
-        "mul.wide.u32 B, y1, %3;\n\t"
         "mov.b64 {A0, A1}, A;\n\t"
-        "mov.b64 {B0, B1}, B;\n\t"
-        "add.cc.u32 m, A1, B0;\n\t"
-        "addc.u32 t, B1, 0;\n\t"
-        "shf.r.clamp.b32 s0, m, t, 29;\n\t"
-        "and.b32 m, m, 0x1FFFFFFF;\n\t"
-        "mov.b64 %0, {A0, m};\n\t"
-        "mov.b64 %1, {s0, 0};\n\t"
+        "mul.wide.u32 B, A1, %4;\n\t"
+        "mad.wide.u32 B, y1, %3, B;\n\t"
+        "mov.b64 {t1, t2}, B;\n\t"
+        "shf.r.clamp.b32 h0, t1, t2, 29;\n\t"
+        "and.b32 t1, t1, 0x1FFFFFFF;\n\t"
+        "mov.b64 %0, {A0, t1};\n\t"
+        "mov.b64 %1, {h0, 0};\n\t"
         "}"
         : "=l"(lo), "=l"(hi)
-        : "l"(y), "r"(x));
+        : "l"(y), "r"(x), "r"(kFmaOne));
     return lo + hi + a;
 }
 

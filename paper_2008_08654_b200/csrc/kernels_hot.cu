@@ -289,12 +289,17 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
 // to an ATOMS.CAST.SPIN.64 loop, which serialises on hot keys: 101 ms instead
 // of 13 ms on config 5), so: the low word carries a 2^31 bias, so a sum hovering
 // around zero never wraps, and the high word counts the wraps.
+// The wrap of one add is the high word of the 64-bit sum old + sext(d), in
+// {-1, 0, 1}: one carry chain instead of compares and selects.
 __device__ __forceinline__ void hot_accumulate(u32* lo, u32* hi, u32 h, i32 d) {
-    const u32 dd = (u32)d;
-    const u32 old = atomicAdd(lo + h, dd);
-    const u32 nw = old + dd;
-    const int carry = d >= 0 ? (int)(nw < old) : -(int)(nw > old);
-    if (carry) atomicAdd(hi + h, (u32)carry);  // hi may be shared or global memory
+    const u32 old = atomicAdd(lo + h, (u32)d);
+    u32 c;
+    asm("{\n\t.reg .u32 t;\n\t"
+        "add.cc.u32 t, %1, %2;\n\t"
+        "addc.u32 %0, 0, %3;\n\t}"
+        : "=r"(c)
+        : "r"(old), "r"((u32)d), "r"((u32)(d >> 31)));
+    if (c) atomicAdd(hi + h, c);  // hi may be shared or global memory
 }
 
 // Raw mode: the hot set covers under 30% of the sample, so the hot pass would
@@ -439,6 +444,8 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     i32* qd = reinterpret_cast<i32*>(qk + kHotWarps * kQueue);
     __shared__ u32 s_next;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u32 lanes_below;  // evaluated once (a volatile read is never rematerialised)
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(lanes_below));
     KeyT* wqk = qk + warp * kQueue;
     i32* wqd = qd + warp * kQueue;
     // CTAs own whole tiles (16-byte vector loads) and a share of the < kT tail
@@ -484,7 +491,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         const bool miss = valid && !hit;
         const unsigned m = __ballot_sync(kFull, miss);
         if (miss) {
-            const int pos = qn + __popc(m & ((1u << lane) - 1));
+            const int pos = qn + __popc(m & lanes_below);
             wqk[pos] = key;
             wqd[pos] = d;
         }

@@ -70,6 +70,12 @@ constexpr uint32_t kMissChunk = 1024;  // miss-buffer slots a warp reserves at o
 
 template <typename KeyT>
 struct HotGeom;
+// a queued miss: key and delta side by side (one 8-byte shared store for u32 keys)
+template <typename KeyT>
+struct alignas(sizeof(KeyT) * 2) QEnt {
+    KeyT k;
+    i32 d;
+};
 // shared slot = key + the low word of its exact sum (the rarely used wrap
 // counter lives in HBM, one array per CTA); slot counts need not be powers of 2
 template <>
@@ -440,14 +446,14 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
     u32* lo = reinterpret_cast<u32*>(hk + S);
     u32* hi = wraps + (uint64_t)blockIdx.x * S;  // this CTA's wrap counters (HBM, zeroed by the launcher)
-    KeyT* qk = reinterpret_cast<KeyT*>(lo + S);
-    i32* qd = reinterpret_cast<i32*>(qk + kHotWarps * kQueue);
+    QEnt<KeyT>* q = reinterpret_cast<QEnt<KeyT>*>(lo + S);
     __shared__ u32 s_next;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     u32 lanes_below;  // evaluated once (a volatile read is never rematerialised)
     asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(lanes_below));
-    KeyT* wqk = qk + warp * kQueue;
-    i32* wqd = qd + warp * kQueue;
+    u32 wq_off;  // this warp's queue offset, held in a register (not re-derived from tid per item)
+    asm volatile("mov.u32 %0, %1;" : "=r"(wq_off) : "r"((u32)warp * kQueue));
+    QEnt<KeyT>* wq = q + wq_off;
     // CTAs own whole tiles (16-byte vector loads) and a share of the < kT tail
     // items (scalar loads; everything, when the buffers are not 16-byte aligned)
     const uint64_t ntiles_all = vec_ok ? n / kT : 0;
@@ -486,25 +492,23 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         const u32 h1 = slot1<S>(key), h2 = slot2<S>(key);
         const KeyT c1 = hk[h1], c2 = hk[h2];
         const u32 h = c1 == key ? h1 : h2;
-        const bool hit = valid && (c1 == key || c2 == key) && key != G::kEmpty;
+        const bool hit = valid && (c1 == key || c2 == key);  // empty slots hold foreign keys
         if (hit) hot_accumulate(lo, hi, h, d);
         const bool miss = valid && !hit;
         const unsigned m = __ballot_sync(kFull, miss);
         if (miss) {
             const int pos = qn + __popc(m & lanes_below);
-            wqk[pos] = key;
-            wqd[pos] = d;
+            wq[pos] = QEnt<KeyT>{key, d};  // one 8-byte store (u32 keys)
         }
         qn += __popc(m);
         misses += __popc(m);
         if (!BUF && qn >= 32) {  // a full warp of misses -> hash, split, red.global
             __syncwarp();
-            misses_direct<MODE, K, SPL, KeyT>(sp, wqk[lane], wqd[lane], true, table);
+            misses_direct<MODE, K, SPL, KeyT>(sp, wq[lane].k, wq[lane].d, true, table);
             direct += sp.rows;
             __syncwarp();
             if (lane < qn - 32) {
-                wqk[lane] = wqk[32 + lane];
-                wqd[lane] = wqd[32 + lane];
+                wq[lane] = wq[32 + lane];
             }
             __syncwarp();
             qn -= 32;
@@ -518,16 +522,15 @@ __global__ void __launch_bounds__(kHotThreads, 1)
             const unsigned long long pos = wbase + wfill;
             wfill += 32;
             if (pos + 32 <= mb.cap) {
-                mb.keys[pos + lane] = wqk[lane];
-                mb.deltas[pos + lane] = wqd[lane];
+                mb.keys[pos + lane] = wq[lane].k;
+                mb.deltas[pos + lane] = wq[lane].d;
             } else {
-                misses_direct<MODE, K, SPL, KeyT>(sp, wqk[lane], wqd[lane], true, table);
+                misses_direct<MODE, K, SPL, KeyT>(sp, wq[lane].k, wq[lane].d, true, table);
                 direct += sp.rows;
             }
             __syncwarp();
             if (lane < qn - 32) {
-                wqk[lane] = wqk[32 + lane];
-                wqd[lane] = wqd[32 + lane];
+                wq[lane] = wq[32 + lane];
             }
             __syncwarp();
             qn -= 32;
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         item(v ? ld_nc(keys + i) : G::kEmpty, v ? load_w32<WK>(w, i) : 0, v);
     }
     if (lane < qn) {
-        misses_direct<MODE, K, SPL, KeyT>(sp, wqk[lane], wqd[lane], true, table);
+        misses_direct<MODE, K, SPL, KeyT>(sp, wq[lane].k, wq[lane].d, true, table);
         direct += sp.rows;
     }
     // unused reserved slots become no-op items (delta 0)
@@ -597,8 +600,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     // u64 adds commute); hh_merge_kernel hashes each hot key once
     unsigned merged = 0;
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
-        if (hk[s] == G::kEmpty) continue;
-        const u64 v = (((u64)hi[s] << 32) | lo[s]) - 0x80000000ull;
+        const u64 v = (((u64)hi[s] << 32) | lo[s]) - 0x80000000ull;  // 0 in empty (foreign-key) slots
         if (v) {
             red_add_u64(slot_sum + s, v);
             ++merged;
@@ -697,10 +699,20 @@ __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict_
         }
         __syncthreads();
     }
+    // an empty slot s gets a FOREIGN key, one with slot1 != s and slot2 != s: no
+    // lookup can match it, so the hot kernel needs no empty-slot test
     unsigned placed = 0;
     for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
-        layout[s] = hk[s];
-        placed += hk[s] != G::kEmpty ? 1u : 0u;
+        KeyT k = hk[s];
+        if (k == G::kEmpty) {
+            for (KeyT t = 0;; ++t) {
+                k = G::kEmpty - t;
+                if (slot1<S>(k) != s && slot2<S>(k) != s) break;
+            }
+        } else {
+            ++placed;
+        }
+        layout[s] = k;
     }
     placed = __reduce_add_sync(0xffffffffu, placed);
     if ((threadIdx.x & 31) == 0 && placed) atomicAdd(&g_hot_stats[3], (unsigned long long)placed);  // keys in the table
@@ -715,7 +727,7 @@ __global__ void hh_merge_kernel(const SketchParams sp, const KeyT* __restrict__ 
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < G::kSlots; s += gridDim.x * blockDim.x) {
         const KeyT key = layout[s];
         const u64 v = slot_sum[s];
-        if (key != G::kEmpty && v) {
+        if (v) {  // (empty slots: foreign keys with no sum)
             rows_direct<MODE, K, SPL>(sp, (u64)key, (i64)v, table);
             ++applied;
         }
@@ -1105,7 +1117,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
             tk, tc, hist, cap, hot, hot_cnt, hot_count, hot_sum, P.slots, phase, go);
     auto fn = binned ? cs_hot_kernel<MODE, K, SPL, KeyT, WK, true> : cs_hot_kernel<MODE, K, SPL, KeyT, WK, false>;
     const size_t smem = ((size_t)sizeof(KeyT) + 4) * G::kSlots;
-    const size_t qbytes = (size_t)kHotWarps * kQueue * (sizeof(KeyT) + 4);
+    const size_t qbytes = (size_t)kHotWarps * kQueue * sizeof(QEnt<KeyT>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes));
     if (e != cudaSuccess) return e;
     uint64_t grid = (n + 256 * kHotWarps - 1) / (256 * kHotWarps);

@@ -474,6 +474,37 @@ def test_hot_path_accumulator_wraps(cuda, mb, orc, weight):
     assert (cnt.cpu().numpy() == exp).all()
 
 
+@pytest.mark.parametrize("kb", [32, 64])
+def test_hot_path_sentinel_keys_heavy(cuda, mb, orc, kb):
+    """Empty hot-table slots hold foreign keys (keys whose two slot choices are
+    elsewhere), so the lookup has no empty-slot test: the all-ones key (the
+    empty marker, never selected as hot) and its neighbours -- the foreign-key
+    candidates -- are frequent here, next to a few genuinely hot keys, with most
+    slots empty.  The table equals the oracle's."""
+    import torch
+
+    n = (1 << 22) + 101
+    rng = np.random.default_rng(kb)
+    top = (1 << kb) - 1
+    keys = rng.integers(0, 1 << min(kb, 62), size=n, dtype=np.uint64)
+    u = rng.random(n)
+    keys[u < 0.25] = top
+    keys[(u >= 0.25) & (u < 0.40)] = top - 1
+    keys[(u >= 0.40) & (u < 0.50)] = top - 2
+    keys[(u >= 0.50) & (u < 0.60)] = 12345
+    if kb == 32:
+        keys = keys.astype(np.uint32)
+    w = rng.integers(-100, 101, size=n).astype(np.int32)
+    spec, fams = make_spec(mb, orc, 5, 65536, 61, kb, 0, 0xFEE)
+    cnt = torch.zeros(5 * 65536, dtype=torch.int64, device="cuda")
+    mb.hot_stats(reset=True)
+    mb.cs_update(spec, dev(keys), cnt, dev(w))
+    st = mb.hot_stats(reset=True)
+    assert st["items"] == n and 0 < st["hot_keys"] < 100  # a nearly empty hot table
+    exp = orc.cs_process(5, 65536, 61, fams, kb, 0, keys, w)
+    assert (cnt.cpu().numpy() == exp).all()
+
+
 def test_sketch_empty_and_single(cuda, mb, orc):
     import torch
 

@@ -139,17 +139,21 @@ __device__ __forceinline__ void count_global(KeyT* tk, u32* tc, u32 slots, KeyT 
     }
 }
 
-// Quick look at the batch's first kProbeItems items in one CTA: if keys seen at
-// least twice cover under 1/32 of them (a stream without heavy hitters, like
-// config 4's uniform 64-bit keys), the sample / selection kernels are skipped
-// (*go = 0) and every item takes the direct path.  Performance only.
+// Quick look at the batch's first kProbeItems items (kProbeCtas CTAs, each
+// counting its contiguous share in a shared table): if keys seen at least twice
+// within a share cover under 1/32 of the items (a stream without heavy
+// hitters, like config 4's uniform 64-bit keys), the sample / selection kernels
+// are skipped (go[0] = 0) and every item takes the direct path.  go[1] sums the
+// covered items, go[2] is the ticket of the last CTA, which decides.
+// Performance only.
 constexpr uint32_t kProbeItems = 1u << 14;
+constexpr int kProbeCtas = 8;
 
 template <typename KeyT>
 __global__ void __launch_bounds__(1024) hh_probe_kernel(const KeyT* __restrict__ keys, uint64_t n, u32* go) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
-    constexpr u32 kProbeSlots = kLocalSlots / 2;  // 2^14 items at most half distinct-heavy
+    constexpr u32 kProbeSlots = kLocalSlots / 2;  // a share of 2^11 items fits
     __shared__ KeyT lk[kProbeSlots];
     __shared__ u32 lc[kProbeSlots];
     __shared__ u32 covered;
@@ -160,7 +164,8 @@ __global__ void __launch_bounds__(1024) hh_probe_kernel(const KeyT* __restrict__
     if (threadIdx.x == 0) covered = 0;
     __syncthreads();
     const u32 m = (u32)(n < kProbeItems ? n : kProbeItems);
-    for (u32 i = threadIdx.x; i < m; i += blockDim.x) {
+    const u32 lo = m * blockIdx.x / gridDim.x, hi = m * (blockIdx.x + 1) / gridDim.x;
+    for (u32 i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         const KeyT key = ld_nc(keys + i);
         if (key == G::kEmpty) continue;
         u32 h = (u32)mix64((u64)key) & (kProbeSlots - 1);
@@ -180,7 +185,14 @@ __global__ void __launch_bounds__(1024) hh_probe_kernel(const KeyT* __restrict__
     mine = __reduce_add_sync(0xffffffffu, mine);
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&covered, mine);
     __syncthreads();
-    if (threadIdx.x == 0) *go = covered * 32 >= m ? 1u : 0u;
+    if (threadIdx.x == 0) {
+        if (covered) atomicAdd(go + 1, covered);
+        __threadfence();
+        if (atomicAdd(go + 2, 1u) == gridDim.x - 1) {  // the last CTA: every share is counted
+            __threadfence();
+            go[0] = atomicAdd(go + 1, 0u) * 32 >= m ? 1u : 0u;
+        }
+    }
 }
 
 template <typename KeyT>
@@ -650,7 +662,28 @@ __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict_
     const u32 nhot = min(*hot_count, cap);
     // level index kLevels - 1 - min(count, kLevels - 1): ascending index = descending count
     auto level = [](u32 c) { return kLevels - 1 - min(c, kLevels - 1); };
-    for (u32 j = threadIdx.x; j < nhot; j += blockDim.x) atomicAdd(&lev[level(hot_cnt[j])], 1u);
+    // level histogram and scatter with one shared atomic per distinct level per
+    // warp (most candidates share the few lowest counts: per-key atomics on one
+    // counter serialise)
+    const u32 lane = threadIdx.x & 31;
+    u32 below;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(below));
+    // counts are read 8 per thread at a time (one global latency per batch);
+    // launched with 1024 threads
+    constexpr u32 kB = 8;
+    for (u32 j0 = 0; j0 < nhot; j0 += kB * 1024) {
+        u32 lv[kB];
+#pragma unroll
+        for (u32 b = 0; b < kB; ++b) {
+            const u32 j = j0 + b * 1024 + threadIdx.x;
+            lv[b] = j < nhot ? level(hot_cnt[j]) : kLevels;
+        }
+#pragma unroll
+        for (u32 b = 0; b < kB; ++b) {
+            const u32 peers = __match_any_sync(0xffffffffu, lv[b]);
+            if (lv[b] < kLevels && (peers & below) == 0) atomicAdd(&lev[lv[b]], (u32)__popc(peers));
+        }
+    }
     __syncthreads();
     if (threadIdx.x < 32) {  // exclusive scan of the level counts, 32 per lane
         constexpr u32 kPer = kLevels / 32;
@@ -671,19 +704,56 @@ __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict_
         for (u32 i = 0; i < kPer; ++i) lev[threadIdx.x * kPer + i] = base + v[i];
     }
     __syncthreads();
-    for (u32 j = threadIdx.x; j < nhot; j += blockDim.x) order[atomicAdd(&lev[level(hot_cnt[j])], 1u)] = (uint16_t)j;
+    for (u32 j0 = 0; j0 < nhot; j0 += kB * 1024) {
+        u32 lv[kB];
+#pragma unroll
+        for (u32 b = 0; b < kB; ++b) {
+            const u32 j = j0 + b * 1024 + threadIdx.x;
+            lv[b] = j < nhot ? level(hot_cnt[j]) : kLevels;
+        }
+#pragma unroll
+        for (u32 b = 0; b < kB; ++b) {
+            const u32 peers = __match_any_sync(0xffffffffu, lv[b]);
+            const int leader = __ffs(peers) - 1;
+            u32 base = 0;
+            if (lv[b] < kLevels && (int)lane == leader) base = atomicAdd(&lev[lv[b]], (u32)__popc(peers));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (lv[b] < kLevels) order[base + __popc(peers & below)] = (uint16_t)(j0 + b * 1024 + threadIdx.x);
+        }
+    }
     __syncthreads();
-    for (u32 base = 0; base < nhot; base += blockDim.x) {
-        const u32 j = base + threadIdx.x;
-        const KeyT key = j < nhot ? hot[order[j]] : G::kEmpty;
-        bool left = false;
-        if (j < nhot && key != G::kEmpty) {
+    // every key this thread places, loaded up front (one global-load latency
+    // instead of one per 1024-key round); launched with 1024 threads
+    constexpr u32 kRounds = G::kCap / 1024;
+    KeyT kk[kRounds];
+#pragma unroll
+    for (u32 r = 0; r < kRounds; ++r) {
+        const u32 j = r * 1024 + threadIdx.x;
+        kk[r] = j < nhot ? hot[order[j]] : G::kEmpty;
+    }
+    // placement rounds of doubling size (1, 1, 2, 4, 8, 16 keys per thread):
+    // priority is fine-grained where counts differ (the hottest keys) and coarse
+    // where they are nearly equal (the many keys seen twice or three times)
+    u32 left = 0;  // bit r: key kk[r] found both slots taken
+#pragma unroll
+    for (u32 g = 0; g < 6; ++g) {
+        const u32 r0 = g == 0 ? 0u : min(1u << (g - 1), kRounds), r1 = min(1u << g, kRounds);
+        if (r0 >= r1 || r0 * 1024 >= nhot) continue;  // CTA-uniform
+#pragma unroll
+        for (u32 r = r0; r < r1; ++r) {
+            const KeyT key = kk[r];
+            if (key == G::kEmpty) continue;
             const u32 s1 = slot1<S>(key), s2 = slot2<S>(key);
-            left = (KeyT)atomicCAS(reinterpret_cast<C*>(hk + s1), (C)G::kEmpty, (C)key) != G::kEmpty &&
-                   (KeyT)atomicCAS(reinterpret_cast<C*>(hk + s2), (C)G::kEmpty, (C)key) != G::kEmpty;
+            if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + s1), (C)G::kEmpty, (C)key) != G::kEmpty &&
+                (KeyT)atomicCAS(reinterpret_cast<C*>(hk + s2), (C)G::kEmpty, (C)key) != G::kEmpty)
+                left |= 1u << r;
         }
         __syncthreads();
-        if (left) {  // one level of displacement (races only cost a slot, never exactness)
+#pragma unroll
+        for (u32 r = r0; r < r1; ++r) {
+            if (!((left >> r) & 1u)) continue;
+            // one level of displacement (races only cost a slot, never exactness)
+            const KeyT key = kk[r];
             const u32 s1 = slot1<S>(key), s2 = slot2<S>(key);
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
@@ -1107,9 +1177,9 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     g.bins = reinterpret_cast<u32*>(p);
     cudaMemsetAsync(tk, 0xff, P.tk_bytes, s);
     cudaMemsetAsync(tc, 0, P.zero_bytes(), s);
-    u32* go = hot_count + 4;  // misc word after the miss count
+    u32* go = hot_count + 4;  // misc words after the miss count: go, covered, ticket
     const u32 cap = G::kCap;
-    hh_probe_kernel<KeyT><<<1, 1024, 0, s>>>(keys, n, go);
+    hh_probe_kernel<KeyT><<<kProbeCtas, 1024, 0, s>>>(keys, n, go);
     hh_count_kernel<KeyT><<<sms * 2, kCountThreads, 0, s>>>(keys, P.m, tk, tc, P.slots, go);
     hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots, go);
     for (int phase = 0; phase < 2; ++phase)

@@ -76,19 +76,20 @@ struct alignas(sizeof(KeyT) * 2) QEnt {
     KeyT k;
     i32 d;
 };
-// shared slot = key + the low word of its exact sum (the rarely used wrap
-// counter lives in HBM, one array per CTA); slot counts need not be powers of 2
+// shared slot = key + a 16-bit cell, the low 16 bits of its exact sum (the
+// rarely used wrap counter lives in HBM, one u64 array per CTA); slot counts
+// need not be powers of 2 (they are even: two cells per 32-bit word)
 template <>
 struct HotGeom<u32> {
-    static constexpr uint32_t kSlots = 24576;  // x (4 B key + 4 B low sum) = 192 KiB
-    static constexpr uint32_t kCap = 32768;  // selected candidates (the layout places ~22.5K)
+    static constexpr uint32_t kSlots = 35840;  // x (4 B key + 2 B cell) = 210 KiB
+    static constexpr uint32_t kCap = 36864;    // selected candidates (the layout places ~32K)
     static constexpr u32 kEmpty = 0xffffffffu;
     using Cas = unsigned;
 };
 template <>
 struct HotGeom<u64> {
-    static constexpr uint32_t kSlots = 16384;  // x (8 B key + 4 B low sum) = 192 KiB
-    static constexpr uint32_t kCap = 8192;
+    static constexpr uint32_t kSlots = 19456;  // x (8 B key + 2 B cell) = 190 KiB
+    static constexpr uint32_t kCap = 16384;
     static constexpr u64 kEmpty = ~0ull;
     using Cas = unsigned long long;
 };
@@ -302,22 +303,34 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
     if (threadIdx.x == 0 && cta_sum) atomicAdd(hot_sum, cta_sum);  // sampled items the hot set covers
 }
 
-// Exact 64-bit accumulation in two u32 words (|d| <= 2^31).  sm_100 has no
-// native 64-bit shared-memory add (atomicAdd on u64 in shared memory compiles
-// to an ATOMS.CAST.SPIN.64 loop, which serialises on hot keys: 101 ms instead
-// of 13 ms on config 5), so: the low word carries a 2^31 bias, so a sum hovering
-// around zero never wraps, and the high word counts the wraps.
-// The wrap of one add is the high word of the 64-bit sum old + sext(d), in
-// {-1, 0, 1}: one carry chain instead of compares and selects.
-__device__ __forceinline__ void hot_accumulate(u32* lo, u32* hi, u32 h, i32 d) {
-    const u32 old = atomicAdd(lo + h, (u32)d);
-    u32 c;
-    asm("{\n\t.reg .u32 t;\n\t"
-        "add.cc.u32 t, %1, %2;\n\t"
-        "addc.u32 %0, 0, %3;\n\t}"
-        : "=r"(c)
-        : "r"(old), "r"((u32)d), "r"((u32)(d >> 31)));
-    if (c) atomicAdd(hi + h, c);  // hi may be shared or global memory
+// Exact 64-bit accumulation in a 16-bit shared cell + a u64 wrap counter in
+// HBM (units of 2^16).  sm_100 has no 16-bit (or native 64-bit) shared atomic
+// add, so two cells share a 32-bit word: cell h is bits 16 (h & 1) of word
+// h >> 1, biased by 2^15 so a sum hovering around zero rarely leaves [0, 2^16).
+// The delta is added to the word shifted to its cell.  Every atomic change x
+// of a cell whose value was c records floor((c + x) / 2^16) in the cell's wrap
+// counter, which keeps cell + 2^16 wraps = bias + sum of its deltas exactly,
+// under any interleaving: a low-cell add that leaves [0, 2^16) also carries w
+// into the high cell (recorded against the high cell's value at that same
+// atomic), and w is then taken back out of the high cell by a second atomic
+// (recorded against its value then).  Halving the cell width fits 35840
+// instead of 24576 slots into shared memory.
+__device__ __forceinline__ void hot_accumulate(u32* cells, u64* wraps_cta, u32 h, i32 d) {
+    typedef unsigned long long ull;
+    const u32 sh = (h & 1u) << 4;
+    u32* word = cells + (h >> 1);
+    const u32 old = atomicAdd(word, (u32)d << sh);
+    const i64 t = (i64)((old >> sh) & 0xFFFFu) + d;
+    if ((u64)t >= 0x10000ull) {  // rare: the cell left [0, 2^16)
+        const i64 w = t >> 16;
+        atomicAdd(reinterpret_cast<ull*>(wraps_cta + h), (ull)w);
+        if (sh == 0) {  // w also entered the high cell (slot h + 1): take it back
+            const i64 w1 = ((i64)(old >> 16) + w) >> 16;
+            const u32 old2 = atomicAdd(word, (u32)(-(i32)w) << 16);
+            const i64 w2 = ((i64)(old2 >> 16) - w) >> 16;
+            if (w1 + w2) atomicAdd(reinterpret_cast<ull*>(wraps_cta + h + 1), (ull)(w1 + w2));
+        }
+    }
 }
 
 // Raw mode: the hot set covers under 30% of the sample, so the hot pass would
@@ -445,7 +458,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     cs_hot_kernel(const SketchParams sp, const KeyT* __restrict__ keys, const void* __restrict__ w, uint64_t n,
                   i64* __restrict__ table, const KeyT* __restrict__ layout, u64* __restrict__ slot_sum,
                   const u32* __restrict__ hot_sum, uint32_t sample, const MissBuf<KeyT> mb, bool vec_ok,
-                  u32* __restrict__ wraps) {
+                  u64* __restrict__ wraps) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
     using KV = KeyVec<KeyT>;
@@ -456,9 +469,10 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     constexpr uint32_t S = G::kSlots;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
-    u32* lo = reinterpret_cast<u32*>(hk + S);
-    u32* hi = wraps + (uint64_t)blockIdx.x * S;  // this CTA's wrap counters (HBM, zeroed by the launcher)
-    QEnt<KeyT>* q = reinterpret_cast<QEnt<KeyT>*>(lo + S);
+    static_assert(S % 2 == 0, "two cells per word");
+    u32* cells = reinterpret_cast<u32*>(hk + S);  // S 16-bit cells
+    u64* hi = wraps + (uint64_t)blockIdx.x * S;   // this CTA's wrap counters (HBM, zeroed by the launcher)
+    QEnt<KeyT>* q = reinterpret_cast<QEnt<KeyT>*>(cells + S / 2);
     __shared__ u32 s_next;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     u32 lanes_below;  // evaluated once (a volatile read is never rematerialised)
@@ -485,10 +499,8 @@ __global__ void __launch_bounds__(kHotThreads, 1)
 
     // every CTA holds the same table layout (hh_layout_kernel), so the slot sums
     // of all CTAs can be merged per slot before the keys are hashed
-    for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
-        hk[s] = layout[s];
-        lo[s] = 0x80000000u;
-    }
+    for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) hk[s] = layout[s];
+    for (uint32_t s = threadIdx.x; s < S / 2; s += kHotThreads) cells[s] = 0x80008000u;
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
 
@@ -505,7 +517,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         const KeyT c1 = hk[h1], c2 = hk[h2];
         const u32 h = c1 == key ? h1 : h2;
         const bool hit = valid && (c1 == key || c2 == key);  // empty slots hold foreign keys
-        if (hit) hot_accumulate(lo, hi, h, d);
+        if (hit) hot_accumulate(cells, hi, h, d);
         const bool miss = valid && !hit;
         const unsigned m = __ballot_sync(kFull, miss);
         if (miss) {
@@ -612,7 +624,8 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     // u64 adds commute); hh_merge_kernel hashes each hot key once
     unsigned merged = 0;
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
-        const u64 v = (((u64)hi[s] << 32) | lo[s]) - 0x80000000ull;  // 0 in empty (foreign-key) slots
+        const u64 v = (hi[s] << 16) + ((cells[s >> 1] >> ((s & 1) << 4)) & 0xFFFFu) -
+                      0x8000ull;  // 0 in empty (foreign-key) slots
         if (v) {
             red_add_u64(slot_sum + s, v);
             ++merged;
@@ -731,12 +744,12 @@ __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict_
         const u32 j = r * 1024 + threadIdx.x;
         kk[r] = j < nhot ? hot[order[j]] : G::kEmpty;
     }
-    // placement rounds of doubling size (1, 1, 2, 4, 8, 16 keys per thread):
+    // placement rounds of doubling size (1, 1, 2, 4, 8, 16, 4 keys per thread):
     // priority is fine-grained where counts differ (the hottest keys) and coarse
     // where they are nearly equal (the many keys seen twice or three times)
-    u32 left = 0;  // bit r: key kk[r] found both slots taken
+    unsigned long long left = 0;  // bit r: key kk[r] found both slots taken
 #pragma unroll
-    for (u32 g = 0; g < 6; ++g) {
+    for (u32 g = 0; g < 7; ++g) {
         const u32 r0 = g == 0 ? 0u : min(1u << (g - 1), kRounds), r1 = min(1u << g, kRounds);
         if (r0 >= r1 || r0 * 1024 >= nhot) continue;  // CTA-uniform
 #pragma unroll
@@ -746,12 +759,12 @@ __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict_
             const u32 s1 = slot1<S>(key), s2 = slot2<S>(key);
             if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + s1), (C)G::kEmpty, (C)key) != G::kEmpty &&
                 (KeyT)atomicCAS(reinterpret_cast<C*>(hk + s2), (C)G::kEmpty, (C)key) != G::kEmpty)
-                left |= 1u << r;
+                left |= 1ull << r;
         }
         __syncthreads();
 #pragma unroll
         for (u32 r = r0; r < r1; ++r) {
-            if (!((left >> r) & 1u)) continue;
+            if (!((left >> r) & 1ull)) continue;
             // one level of displacement (races only cost a slot, never exactness)
             const KeyT key = kk[r];
             const u32 s1 = slot1<S>(key), s2 = slot2<S>(key);
@@ -1140,7 +1153,7 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     P.tc_bytes = (size_t)P.slots * 4;
     P.misc = 256 * 4 + 64;  // hist[256], hot_count, hot_sum, miss count (u64)
     P.gcnt_bytes = align256((size_t)P.chunks * g.nb * 8 + 8);
-    P.wraps_bytes = align256((size_t)sm_count() * G::kSlots * 4);
+    P.wraps_bytes = align256((size_t)sm_count() * G::kSlots * 8);
     P.sum_bytes = align256((size_t)G::kSlots * 8);
     P.layout_bytes = align256((size_t)G::kSlots * sizeof(KeyT));
     P.hot_bytes = align256((size_t)G::kCap * (sizeof(KeyT) + 4));
@@ -1164,7 +1177,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     u32* hot_sum = hot_count + 1;
     unsigned long long* mcount = reinterpret_cast<unsigned long long*>(hot_count + 2);
     g.gcnt = reinterpret_cast<unsigned long long*>(ws + P.tk_bytes + P.tc_bytes + P.misc);
-    u32* wraps = reinterpret_cast<u32*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes);
+    u64* wraps = reinterpret_cast<u64*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes);
     u64* slot_sum = reinterpret_cast<u64*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes + P.wraps_bytes);
     unsigned char* p = ws + P.tk_bytes + P.zero_bytes();
     KeyT* hot = reinterpret_cast<KeyT*>(p);
@@ -1186,7 +1199,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
         hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(
             tk, tc, hist, cap, hot, hot_cnt, hot_count, hot_sum, P.slots, phase, go);
     auto fn = binned ? cs_hot_kernel<MODE, K, SPL, KeyT, WK, true> : cs_hot_kernel<MODE, K, SPL, KeyT, WK, false>;
-    const size_t smem = ((size_t)sizeof(KeyT) + 4) * G::kSlots;
+    const size_t smem = ((size_t)sizeof(KeyT) + 2) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * sizeof(QEnt<KeyT>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes));
     if (e != cudaSuccess) return e;

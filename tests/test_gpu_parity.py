@@ -474,6 +474,33 @@ def test_hot_path_accumulator_wraps(cuda, mb, orc, weight):
     assert (cnt.cpu().numpy() == exp).all()
 
 
+@pytest.mark.parametrize("wset", ["extreme", "cell_edges"])
+def test_hot_path_cells_wrap_under_contention(cuda, mb, orc, wset):
+    """Hot sums live in 16-bit shared cells, two per 32-bit word, with wraps
+    recorded in HBM: a Zipf stream (thousands of hot keys, so both cells of
+    most words are busy) whose weights make nearly every add leave the cell
+    range -- the full i32 extremes, or values around the 2^15 / 2^16 cell
+    edges -- still gives the oracle's table bit for bit."""
+    import torch
+
+    n = (1 << 22) + 77
+    zk, _ = orc.gen_zipf_items(13, 0, n)
+    rng = np.random.default_rng(17 if wset == "extreme" else 19)
+    if wset == "extreme":
+        vals = np.array([np.iinfo(np.int32).max, np.iinfo(np.int32).min, 1 << 30, -(1 << 30), 65537, -65537], np.int64)
+    else:
+        vals = np.array([32767, -32768, 32768, -32769, 65535, -65535, 65536, -65536, 1, -1], np.int64)
+    w = rng.choice(vals, size=n).astype(np.int32)
+    spec, fams = make_spec(mb, orc, 5, 65536, 61, 32, 0, 0xCE11)
+    cnt = torch.zeros(5 * 65536, dtype=torch.int64, device="cuda")
+    mb.hot_stats(reset=True)
+    mb.cs_update(spec, dev(zk), cnt, dev(w))
+    st = mb.hot_stats(reset=True)
+    assert st["items"] == n and st["hot_keys"] > 1000
+    exp = orc.cs_process(5, 65536, 61, fams, 32, 0, zk, w)
+    assert (cnt.cpu().numpy() == exp).all()
+
+
 @pytest.mark.parametrize("kb", [32, 64])
 def test_hot_path_sentinel_keys_heavy(cuda, mb, orc, kb):
     """Empty hot-table slots hold foreign keys (keys whose two slot choices are

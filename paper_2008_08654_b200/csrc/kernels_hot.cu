@@ -82,7 +82,7 @@ struct alignas(sizeof(KeyT) * 2) QEnt {
 template <>
 struct HotGeom<u32> {
     static constexpr uint32_t kSlots = 35840;  // x (4 B key + 2 B cell) = 210 KiB
-    static constexpr uint32_t kCap = 36864;    // selected candidates (the layout places ~32K)
+    static constexpr uint32_t kCap = 40960;    // selected candidates (the layout places ~31K)
     static constexpr u32 kEmpty = 0xffffffffu;
     using Cas = unsigned;
 };
@@ -661,13 +661,12 @@ __device__ __forceinline__ u32 other_slot(KeyT k, u32 s) {
 template <typename KeyT>
 __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict__ hot, const u32* __restrict__ hot_cnt,
                                                          const u32* __restrict__ hot_count, u32 cap,
-                                                         KeyT* __restrict__ layout) {
+                                                         KeyT* __restrict__ sorted, KeyT* __restrict__ layout) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
     constexpr uint32_t S = G::kSlots;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
-    uint16_t* order = reinterpret_cast<uint16_t*>(hk + S);
     __shared__ u32 lev[kLevels];
     for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) hk[s] = G::kEmpty;
     for (uint32_t l = threadIdx.x; l < kLevels; l += blockDim.x) lev[l] = 0;
@@ -731,42 +730,40 @@ __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict_
             u32 base = 0;
             if (lv[b] < kLevels && (int)lane == leader) base = atomicAdd(&lev[lv[b]], (u32)__popc(peers));
             base = __shfl_sync(0xffffffffu, base, leader);
-            if (lv[b] < kLevels) order[base + __popc(peers & below)] = (uint16_t)(j0 + b * 1024 + threadIdx.x);
+            if (lv[b] < kLevels) sorted[base + __popc(peers & below)] = hot[j0 + b * 1024 + threadIdx.x];
         }
     }
     __syncthreads();
-    // every key this thread places, loaded up front (one global-load latency
-    // instead of one per 1024-key round); launched with 1024 threads
+    // placement rounds of doubling size (1, 1, 2, 4, 8, 16, ... keys per thread,
+    // read coalesced from the count-sorted list): priority is fine-grained where
+    // counts differ (the hottest keys) and coarse where they are nearly equal
+    // (the many keys seen twice or three times); launched with 1024 threads
     constexpr u32 kRounds = G::kCap / 1024;
-    KeyT kk[kRounds];
+    constexpr u32 kMaxPer = 16;
+#pragma unroll 1
+    for (u32 r0 = 0, r1 = 1; r0 < kRounds && r0 * 1024 < nhot; r0 = r1, r1 = min(2 * r1, min(r1 + kMaxPer, kRounds))) {
+        KeyT rk[kMaxPer];
 #pragma unroll
-    for (u32 r = 0; r < kRounds; ++r) {
-        const u32 j = r * 1024 + threadIdx.x;
-        kk[r] = j < nhot ? hot[order[j]] : G::kEmpty;
-    }
-    // placement rounds of doubling size (1, 1, 2, 4, 8, 16, 4 keys per thread):
-    // priority is fine-grained where counts differ (the hottest keys) and coarse
-    // where they are nearly equal (the many keys seen twice or three times)
-    unsigned long long left = 0;  // bit r: key kk[r] found both slots taken
+        for (u32 i = 0; i < kMaxPer; ++i) {
+            const u32 j = (r0 + i) * 1024 + threadIdx.x;
+            rk[i] = (r0 + i < r1 && j < nhot) ? sorted[j] : G::kEmpty;
+        }
+        u32 left = 0;  // bit i: key rk[i] found both slots taken
 #pragma unroll
-    for (u32 g = 0; g < 7; ++g) {
-        const u32 r0 = g == 0 ? 0u : min(1u << (g - 1), kRounds), r1 = min(1u << g, kRounds);
-        if (r0 >= r1 || r0 * 1024 >= nhot) continue;  // CTA-uniform
-#pragma unroll
-        for (u32 r = r0; r < r1; ++r) {
-            const KeyT key = kk[r];
+        for (u32 i = 0; i < kMaxPer; ++i) {
+            const KeyT key = rk[i];
             if (key == G::kEmpty) continue;
             const u32 s1 = slot1<S>(key), s2 = slot2<S>(key);
             if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + s1), (C)G::kEmpty, (C)key) != G::kEmpty &&
                 (KeyT)atomicCAS(reinterpret_cast<C*>(hk + s2), (C)G::kEmpty, (C)key) != G::kEmpty)
-                left |= 1ull << r;
+                left |= 1u << i;
         }
         __syncthreads();
 #pragma unroll
-        for (u32 r = r0; r < r1; ++r) {
-            if (!((left >> r) & 1ull)) continue;
+        for (u32 i = 0; i < kMaxPer; ++i) {
+            if (!((left >> i) & 1u)) continue;
             // one level of displacement (races only cost a slot, never exactness)
-            const KeyT key = kk[r];
+            const KeyT key = rk[i];
             const u32 s1 = slot1<S>(key), s2 = slot2<S>(key);
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
@@ -1156,7 +1153,7 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     P.wraps_bytes = align256((size_t)sm_count() * G::kSlots * 8);
     P.sum_bytes = align256((size_t)G::kSlots * 8);
     P.layout_bytes = align256((size_t)G::kSlots * sizeof(KeyT));
-    P.hot_bytes = align256((size_t)G::kCap * (sizeof(KeyT) + 4));
+    P.hot_bytes = align256((size_t)G::kCap * (2 * sizeof(KeyT) + 4));  // hot list, counts, sorted keys
     P.mk_bytes = align256((size_t)P.cap_m * sizeof(KeyT));
     P.md_bytes = align256((size_t)P.cap_m * 4);
     P.bin_bytes = (size_t)g.nb * g.cap * 4;
@@ -1208,10 +1205,10 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     const bool vec_ok = (reinterpret_cast<uintptr_t>(keys) & 15) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
     // without bins (cap 0) every miss takes the direct path and raw mode is off
     auto fl = hh_layout_kernel<KeyT>;
-    const size_t lbytes = sizeof(KeyT) * G::kSlots + 2 * G::kCap;
+    const size_t lbytes = sizeof(KeyT) * G::kSlots;
     if ((e = cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbytes)) != cudaSuccess)
         return e;
-    fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, cap, layout);
+    fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, cap, reinterpret_cast<KeyT*>(hot_cnt + G::kCap), layout);
     fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, layout, slot_sum, hot_sum,
                                                           binned ? P.m : 0, mb, vec_ok, wraps);
     hh_merge_kernel<MODE, K, SPL, KeyT><<<(G::kSlots + 255) / 256, 256, 0, s>>>(sp, layout, slot_sum, table);

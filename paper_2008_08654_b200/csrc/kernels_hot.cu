@@ -16,14 +16,17 @@
 //                  hot list, with their sample counts;
 //      hh_layout : one CTA places the hot list, hottest first, in the two-choice
 //                  shared table layout every CTA copies (one level of cuckoo
-//                  displacement; ~22.5K of 32K candidates in 24576 slots);
+//                  displacement; ~31K of 40960 candidates in 35840 slots);
 //   3. cs_hot    : one 1024-thread CTA per SM keeps the hot keys in a shared-
-//                  memory table with an exact 64-bit accumulator per key.  A hit
-//                  costs one shared reduction and no hashing.  Misses are
-//                  compacted per warp into full-warp batches of 32 (key, delta)
-//                  pairs appended to a miss buffer in HBM.  Warps pull 128-item
-//                  tiles of their CTA's contiguous range from a shared counter,
-//                  so they finish together.  Finally each CTA applies every hot
+//                  memory table with an exact 64-bit accumulator per key (a
+//                  16-bit shared cell + a wrap counter in HBM).  A hit costs one
+//                  shared atomic and no hashing.  Misses are compacted per warp
+//                  into full-warp batches of 32 (key, delta) pairs that are
+//                  hashed, split and sent to L2 as red.global (or, binned
+//                  strategy, appended to a miss buffer in HBM).  Warps pull
+//                  256-item tiles of their CTA's contiguous range from a shared
+//                  counter, so they finish together.  Each CTA adds its slot
+//                  sums into per-slot totals, and hh_merge applies every hot
 //                  key once (hash -> split -> red).
 //   4. cs_bin    : the misses (or, when the sample shows no heavy hitters, the
 //                  raw stream -- pass 3 is then skipped) are hashed, split and
@@ -642,8 +645,9 @@ __global__ void __launch_bounds__(kHotThreads, 1)
 
 // One CTA lays out the hot set in the two-choice table once for every CTA.
 // The selected keys are first ordered by sample count, hottest first (counting
-// sort over kLevels count levels, counts >= kLevels - 1 share the top level),
-// then placed in that order, 1024 at a time: a key goes to slot1 if free, else
+// sort over kLevels count levels, counts >= kLevels - 1 share the top level,
+// into an HBM staging list), then placed in that order, in rounds of growing
+// size: a key goes to slot1 if free, else
 // to slot2 if free; if both are taken, one level of cuckoo displacement moves
 // the occupant of either slot to ITS other slot when that one is free.  Keys
 // that still find no slot stay cold.  Exactness never depends on the layout:

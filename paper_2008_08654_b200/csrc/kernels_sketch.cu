@@ -237,12 +237,33 @@ __device__ __forceinline__ void add192(U192& a, u64 b0, u64 b1, u64 b2) {
         : "l"(b0), "l"(b1), "l"(b2));
 }
 
-__global__ void __launch_bounds__(1024) cs_moments_kernel(const i64* __restrict__ table, uint64_t width,
-                                                          u64* __restrict__ out) {
+// One row is split over gridDim.y CTAs (span cells each); each CTA adds
+// its exact 192-bit partial into the row's out[0..2] with carry-propagating
+// u64 atomics (integer addition commutes, so the total is exact in any order),
+// and the last CTA of the row -- ticket in out[3], zeroed by the launcher --
+// applies the reference's saturation and clears the ticket.
+constexpr uint32_t kMomThreads = 256, kMomCells = 4096;
+
+__device__ __forceinline__ void atomic_add192(unsigned long long* o, u64 w0, u64 w1, u64 w2) {
+    const u64 o0 = atomicAdd(o, (unsigned long long)w0);
+    const u64 c0 = o0 + w0 < o0 ? 1 : 0;
+    const u64 o1 = atomicAdd(o + 1, (unsigned long long)w1);
+    u64 c1 = o1 + w1 < o1 ? 1 : 0;
+    if (c0) {
+        const u64 o1b = atomicAdd(o + 1, 1ull);
+        c1 += o1b + 1 == 0 ? 1 : 0;
+    }
+    if (w2 + c1) atomicAdd(o + 2, (unsigned long long)(w2 + c1));
+}
+
+__global__ void __launch_bounds__(kMomThreads) cs_moments_kernel(const i64* __restrict__ table, uint64_t width,
+                                                                 uint64_t span, u64* __restrict__ out) {
     const uint32_t row = blockIdx.x;
     const i64* base = table + (uint64_t)row * width;
+    const uint64_t lo = (uint64_t)blockIdx.y * span;
+    const uint64_t hi = lo + span < width ? lo + span : width;
     U192 acc = {0, 0, 0};
-    for (uint64_t i = threadIdx.x; i < width; i += blockDim.x) {
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += kMomThreads) {
         const i64 c = base[i];
         const u64 mag = c < 0 ? 0ull - (u64)c : (u64)c;  // sketch.cpp:149 (INT64_MIN-safe)
         add192(acc, mag * mag, __umul64hi(mag, mag), 0);
@@ -254,20 +275,30 @@ __global__ void __launch_bounds__(1024) cs_moments_kernel(const i64* __restrict_
         const u64 b2 = __shfl_xor_sync(kFull, acc.w2, off);
         add192(acc, b0, b1, b2);
     }
-    __shared__ U192 part[32];
+    __shared__ U192 part[kMomThreads / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) part[warp] = acc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        U192 t = {0, 0, 0};
-        for (int wdx = 0; wdx < (int)(blockDim.x >> 5); ++wdx) add192(t, part[wdx].w0, part[wdx].w1, part[wdx].w2);
-        // sketch.cpp:150-154: saturate at 2^128 - 1 and flag it
-        const bool sat = t.w2 != 0;
-        out[4 * row + 0] = sat ? ~0ull : t.w0;
-        out[4 * row + 1] = sat ? ~0ull : t.w1;
-        out[4 * row + 2] = sat ? 1 : 0;
-        out[4 * row + 3] = 0;
+    if (threadIdx.x != 0) return;
+    U192 t = {0, 0, 0};
+    for (int wdx = 0; wdx < (int)(kMomThreads / 32); ++wdx) add192(t, part[wdx].w0, part[wdx].w1, part[wdx].w2);
+    u64 s0 = t.w0, s1 = t.w1, s2 = t.w2;
+    if (gridDim.y > 1) {  // (one CTA per row: out is written directly, not zeroed first)
+        unsigned long long* o = reinterpret_cast<unsigned long long*>(out + 4 * row);
+        atomic_add192(o, t.w0, t.w1, t.w2);
+        __threadfence();
+        if (atomicAdd(o + 3, 1ull) != gridDim.y - 1) return;
+        __threadfence();  // the last CTA of the row: every partial is in
+        s0 = atomicAdd(o, 0ull);
+        s1 = atomicAdd(o + 1, 0ull);
+        s2 = atomicAdd(o + 2, 0ull);
     }
+    // sketch.cpp:150-154: saturate at 2^128 - 1 and flag it
+    const bool sat = s2 != 0;
+    out[4 * row + 0] = sat ? ~0ull : s0;
+    out[4 * row + 1] = sat ? ~0ull : s1;
+    out[4 * row + 2] = sat ? 1 : 0;
+    out[4 * row + 3] = 0;
 }
 
 __global__ void cs_merge_kernel(u64* __restrict__ dst, const u64* __restrict__ src, uint64_t count) {
@@ -426,7 +457,16 @@ cudaError_t launch_cs_update(const SketchParams& sp, const void* keys, int key_w
 cudaError_t launch_cs_moments(const int64_t* table, uint32_t rows, uint64_t width, uint64_t* out,
                               cudaStream_t s) {
     if (rows == 0) return cudaSuccess;
-    cs_moments_kernel<<<rows, 1024, 0, s>>>(table, width, out);
+    uint64_t span = kMomCells, parts = width ? (width + span - 1) / span : 1;
+    if (parts > 65535) {  // huge rows: fewer, longer CTAs (gridDim.y <= 65535)
+        span = (width + 65534) / 65535;
+        parts = (width + span - 1) / span;
+    }
+    if (parts > 1) {  // the partials are accumulated in out (the ticket in out[3])
+        const cudaError_t e = cudaMemsetAsync(out, 0, (size_t)rows * 4 * sizeof(uint64_t), s);
+        if (e != cudaSuccess) return e;
+    }
+    cs_moments_kernel<<<dim3(rows, (unsigned)parts), kMomThreads, 0, s>>>(table, width, span, out);
     return cudaGetLastError();
 }
 

@@ -564,6 +564,28 @@ def test_estimator_saturation(cuda, mb, orc):
         assert m[0] == orc.row_moment(c, len(vals))
 
 
+def test_estimator_rows_over_many_ctas(cuda, mb, orc):
+    """The estimator splits each row over CTAs of 4096 cells and adds the
+    192-bit partials with carry-propagating atomics: rows whose partial sums
+    carry across words between CTAs, just below and exactly at the 2^128
+    saturation boundary, and a width that is not a multiple of 4096."""
+    import torch
+
+    width = 20000
+    rng = np.random.default_rng(5)
+    rows = [rng.integers(-(2**40), 2**40, size=width, dtype=np.int64),
+            rng.integers(np.iinfo(np.int64).min, np.iinfo(np.int64).max, size=width, dtype=np.int64),
+            rng.integers(-(2**20), 2**20, size=width, dtype=np.int64),
+            np.zeros(width, np.int64)]
+    rows[2][[0, 8000, 16000]] = np.iinfo(np.int64).min  # 3 * 2^126 + small: below 2^128
+    rows[3][[1, 5000, 9000, 19999]] = np.iinfo(np.int64).min  # exactly 2^128: saturated
+    c = np.concatenate(rows)
+    m = mb.moments_to_python(mb.cs_moments(torch.from_numpy(c).cuda(), len(rows), width))
+    for r in range(len(rows)):
+        assert m[r] == orc.row_moment(rows[r], width), r
+    assert m[3][1] and not m[2][1]
+
+
 def test_merge_equals_concatenation(cuda, mb, orc):
     import torch
 

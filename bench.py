@@ -387,9 +387,9 @@ def main():
                      "binned_entries_per_item": hs["binned"] / max(1, hs["items"]),
                      "direct_row_updates": hs["direct"] / args.steps,
                      "raw_batches": hs["raw_batches"]},
-        # per step: hh_probe, hh_count, hh_hist, hh_select x 2 (two phases), hh_layout, cs_hot, hh_merge,
-        # cs_moments (the table zeroing is a torch fill)
-        "gpu_launches": 9 * args.steps,
+        # per step: hh_probe, hh_count, hh_hist, hh_select, hh_layout, cs_hot, hh_merge, cs_moments
+        # (the table zeroing is a torch fill)
+        "gpu_launches": 8 * args.steps,
         "clocks": clocks,
         "peaks": {"imad_wide_per_s": imad_peak, "l2_red_per_s": red_peak, "hbm_gbs": hbm_peak,
                   "hbm_kind": peak_kind},

@@ -248,58 +248,64 @@ __global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist, u32 slots,
         if (sh[i]) atomicAdd(hist + i, sh[i]);
 }
 
+// One pass over the count table: keys with count >= thr (they fit by
+// construction) take hot-list entries [0, tail) through hot_count[0]; keys with
+// count == thr - 1 fill what capacity is left, [tail, cap), first come first
+// served, through hot_count[7].  thr and tail come from the count histogram.
 template <typename KeyT>
 __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restrict__ tc, const u32* __restrict__ hist,
                                  u32 cap, KeyT* hot, u32* hot_cnt, u32* hot_count, u32* hot_sum, u32 slots,
-                                 int phase, const u32* __restrict__ go) {
+                                 const u32* __restrict__ go) {
     if (!*go) return;
-    __shared__ u32 thr, sh[256];
+    __shared__ u32 thr, tail, sh[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = hist[i];  // one parallel load
     __syncthreads();
-    if (threadIdx.x == 0) {  // smallest threshold >= 2 whose tail fits the shared table
-        u32 tail = 0, c = 255;
+    if (threadIdx.x == 0) {  // smallest threshold >= 2 whose tail fits the candidate list
+        u32 tl = 0, c = 255;
         for (; c >= 2; --c) {
-            if (tail + sh[c] > cap) break;
-            tail += sh[c];
+            if (tl + sh[c] > cap) break;
+            tl += sh[c];
         }
         thr = c + 1;
+        tail = tl;
     }
     __syncthreads();
-    // phase 0: every key with count >= thr (they fit by construction); phase 1
-    // (a second launch, after all of phase 0): keys with count == thr - 1 fill
-    // what capacity is left, first come first served
-    const u32 t = phase == 0 ? thr : thr - 1;
-    if (phase == 1 && t < 2) return;
+    const u32 t0 = thr, t1 = thr - 1;  // class 1 (count == t1) only when t1 >= 2
     // each thread scans kSelPer consecutive slots; the CTA's selected keys get
-    // their output range with ONE global atomic (16K selections from warps
-    // hitting one counter serialise at L2)
+    // their output ranges with ONE global atomic per class (16K selections from
+    // warps hitting one counter serialise at L2)
     constexpr int kSelPer = 8;
-    __shared__ u32 cta_cnt, cta_sum, cta_base;
-    if (threadIdx.x == 0) cta_cnt = cta_sum = 0;
+    __shared__ u32 cta_cnt0, cta_cnt1, cta_sum, cta_base0, cta_base1;
+    if (threadIdx.x == 0) cta_cnt0 = cta_cnt1 = cta_sum = 0;
     __syncthreads();
     const uint32_t s0 = (blockIdx.x * blockDim.x + threadIdx.x) * kSelPer;
-    u32 mine = 0;
-    const u32 t_hi = phase == 0 ? 0xffffffffu : thr;  // phase 1: exactly count t
+    u32 mine0 = 0, mine1 = 0;
 #pragma unroll
     for (int k = 0; k < kSelPer; ++k) {
         const u32 c = s0 + k < slots ? tc[s0 + k] : 0;
-        mine += (c >= t && c < t_hi) ? 1u : 0u;
+        mine0 += c >= t0 ? 1u : 0u;
+        mine1 += (c == t1 && t1 >= 2) ? 1u : 0u;
     }
-    const u32 off = mine ? atomicAdd(&cta_cnt, mine) : 0;
+    const u32 off0 = mine0 ? atomicAdd(&cta_cnt0, mine0) : 0;
+    const u32 off1 = mine1 ? atomicAdd(&cta_cnt1, mine1) : 0;
     __syncthreads();
-    if (threadIdx.x == 0) cta_base = cta_cnt ? atomicAdd(hot_count, cta_cnt) : 0;
+    if (threadIdx.x == 0) {
+        cta_base0 = cta_cnt0 ? atomicAdd(hot_count, cta_cnt0) : 0;
+        cta_base1 = cta_cnt1 ? tail + atomicAdd(hot_count + 7, cta_cnt1) : 0;
+    }
     __syncthreads();
-    u32 idx = cta_base + off, covered = 0;
-    for (int k = 0; mine && k < kSelPer; ++k) {
+    u32 i0 = cta_base0 + off0, i1 = cta_base1 + off1, covered = 0;
+    for (int k = 0; (mine0 | mine1) && k < kSelPer; ++k) {
         const uint32_t sl = s0 + k;
         const u32 c = sl < slots ? tc[sl] : 0;
-        if (c < t || c >= t_hi) continue;
+        const bool c0 = c >= t0, c1 = c == t1 && t1 >= 2;
+        if (!c0 && !c1) continue;
+        const u32 idx = c0 ? i0++ : i1++;
         if (idx < cap) {
             hot[idx] = tk[sl];
             hot_cnt[idx] = c;
             covered += c;
         }
-        ++idx;
     }
     if (covered) atomicAdd(&cta_sum, covered);
     __syncthreads();
@@ -675,7 +681,7 @@ __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict_
     for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) hk[s] = G::kEmpty;
     for (uint32_t l = threadIdx.x; l < kLevels; l += blockDim.x) lev[l] = 0;
     __syncthreads();
-    const u32 nhot = min(*hot_count, cap);
+    const u32 nhot = min(hot_count[0] + hot_count[7], cap);  // both select classes
     // level index kLevels - 1 - min(count, kLevels - 1): ascending index = descending count
     auto level = [](u32 c) { return kLevels - 1 - min(c, kLevels - 1); };
     // level histogram and scatter with one shared atomic per distinct level per
@@ -1152,7 +1158,7 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     }
     P.tk_bytes = align256((size_t)P.slots * sizeof(KeyT));
     P.tc_bytes = (size_t)P.slots * 4;
-    P.misc = 256 * 4 + 64;  // hist[256], hot_count, hot_sum, miss count (u64)
+    P.misc = 256 * 4 + 64;  // hist[256], hot_count, hot_sum, miss count (u64), go words, class-1 count
     P.gcnt_bytes = align256((size_t)P.chunks * g.nb * 8 + 8);
     P.wraps_bytes = align256((size_t)sm_count() * G::kSlots * 8);
     P.sum_bytes = align256((size_t)G::kSlots * 8);
@@ -1196,9 +1202,8 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     hh_probe_kernel<KeyT><<<kProbeCtas, 1024, 0, s>>>(keys, n, go);
     hh_count_kernel<KeyT><<<sms * 2, kCountThreads, 0, s>>>(keys, P.m, tk, tc, P.slots, go);
     hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots, go);
-    for (int phase = 0; phase < 2; ++phase)
-        hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(
-            tk, tc, hist, cap, hot, hot_cnt, hot_count, hot_sum, P.slots, phase, go);
+    hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(tk, tc, hist, cap, hot, hot_cnt,
+                                                                            hot_count, hot_sum, P.slots, go);
     auto fn = binned ? cs_hot_kernel<MODE, K, SPL, KeyT, WK, true> : cs_hot_kernel<MODE, K, SPL, KeyT, WK, false>;
     const size_t smem = ((size_t)sizeof(KeyT) + 2) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * sizeof(QEnt<KeyT>);

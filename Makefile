@@ -9,7 +9,7 @@ CUDA     ?= /usr/local/cuda
 NVCC     ?= $(CUDA)/bin/nvcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
-CXXFLAGS := -O3 -g -std=c++20 -fPIC -Wall -Wextra -I$(CUDA)/include
+CXXFLAGS := -O3 -g -std=c++20 -fPIC -Wall -Wextra -fopenmp -I$(CUDA)/include
 BUILD    := build
 
 CU_SRCS  := $(wildcard $(PKG)/csrc/*.cu)
@@ -33,7 +33,7 @@ $(BUILD)/%.cpp.o: $(PKG)/host/%.cpp $(HDRS)
 	g++ $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(CU_OBJS) $(CPP_OBJS)
-	$(NVCC) $(ARCH) -shared -cudart shared -o $@ $^ -Xlinker -rpath,'$$ORIGIN'
+	$(NVCC) $(ARCH) -shared -cudart shared -o $@ $^ -Xcompiler -fopenmp -Xlinker -rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle all

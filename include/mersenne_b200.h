@@ -184,6 +184,10 @@ void mb200_sketch_destroy(mb200_sketch* s);
  * chunks against the scatter kernel; returns after the batch is applied. */
 int mb200_sketch_process(mb200_sketch* s, const void* h_keys, int key_width, const void* h_weights,
                          int weight_kind, uint64_t n);
+/* bytes mb200_sketch_process has moved host -> device for this sketch (keys
+ * plus deltas; deltas travel narrowed to i8 / i16 when a chunk fits).  A
+ * transport statistic with no reference counterpart. */
+int mb200_sketch_h2d_bytes(const mb200_sketch* s, uint64_t* out);
 /* same on DEVICE arrays, asynchronous on `stream` */
 int mb200_sketch_process_device(mb200_sketch* s, const void* d_keys, int key_width,
                                 const void* d_weights, int weight_kind, uint64_t n, void* stream);

@@ -139,6 +139,8 @@ public:
     void process(u128 x, i64 delta);  // API parity (one-item batch)
     // host batch: key_width 32/64, weight_kind MB200_W_* (h_weights may be null = +1)
     void process_batch(const void* h_keys, int key_width, const void* h_weights, int weight_kind, u64 n);
+    // bytes process_batch has moved host -> device over this sketch's lifetime
+    u64 h2d_bytes() const;
     // device batch, asynchronous on `stream`
     void process_device(const void* d_keys, int key_width, const void* d_weights, int weight_kind, u64 n,
                         void* stream = nullptr);

@@ -446,6 +446,12 @@ class CountSketch:
                 wk = W_I64
         check(lib.mb200_sketch_process(self._h, _p(keys), kw, _p(weights), wk, len(keys)))
 
+    def h2d_bytes(self) -> int:
+        """Bytes process() has moved host -> device (deltas narrowed when they fit)."""
+        v = C.c_uint64()
+        check(lib.mb200_sketch_h2d_bytes(self._h, C.byref(v)))
+        return v.value
+
     def process_one(self, key: int, delta: int):
         self.process(np.array([key], np.uint64), np.array([delta], np.int64))
 

@@ -94,6 +94,7 @@ SIGNATURES = [
     ("mb200_sketch_destroy", None, [P]),
     ("mb200_sketch_process", I, [P, P, I, P, I, u64]),
     ("mb200_sketch_process_device", I, [P, P, I, P, I, u64, P]),
+    ("mb200_sketch_h2d_bytes", I, [P, P]),
     ("mb200_sketch_row_second_moment", I, [P, U, P, P, P]),
     ("mb200_sketch_second_moment", I, [P, I, P, P, P]),
     ("mb200_sketch_point_query", I, [P, P, I, u64, P]),

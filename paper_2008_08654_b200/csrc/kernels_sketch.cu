@@ -497,4 +497,37 @@ cudaError_t launch_cs_point_query(const SketchParams& sp, const int64_t* table, 
     return cudaGetLastError();
 }
 
+// ---- delta widening (host API transport) --------------------------------------
+// mb200_sketch_process ships deltas over PCIe in the narrowest of i8 / i16 that
+// holds every delta of a chunk; this sign-extends them back to the API's weight
+// kind before the scatter.  Four deltas per thread, stores coalesced.
+template <typename Src, typename Dst>
+__global__ void widen_deltas_kernel(const Src* __restrict__ src, Dst* __restrict__ dst, uint64_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (i + e < n) dst[i + e] = (Dst)ld_nc(src + i + e);
+    }
+}
+
+cudaError_t launch_widen_deltas(const void* src, int src_bits, void* dst, int dst_bits, uint64_t n,
+                                cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t need = (n + 1023) / 1024;
+    const uint64_t cap = (uint64_t)sm_count() * 8;
+    const int grid = (int)(need < cap ? need : cap);
+    if (src_bits == 8 && dst_bits == 32)
+        widen_deltas_kernel<<<grid, 256, 0, s>>>((const int8_t*)src, (int32_t*)dst, n);
+    else if (src_bits == 8 && dst_bits == 64)
+        widen_deltas_kernel<<<grid, 256, 0, s>>>((const int8_t*)src, (int64_t*)dst, n);
+    else if (src_bits == 16 && dst_bits == 32)
+        widen_deltas_kernel<<<grid, 256, 0, s>>>((const int16_t*)src, (int32_t*)dst, n);
+    else if (src_bits == 16 && dst_bits == 64)
+        widen_deltas_kernel<<<grid, 256, 0, s>>>((const int16_t*)src, (int64_t*)dst, n);
+    else
+        return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
 }  // namespace mb200

@@ -49,6 +49,10 @@ cudaError_t launch_count_out_of_domain(const void* keys, int key_width, uint64_t
                                        unsigned long long* d_count, cudaStream_t s);
 
 // sketch (kernels_sketch.cu)
+// Sign-extend host-narrowed deltas (i8 or i16, see CountSketch::process_batch)
+// back to the API's weight kind (i32 or i64) in device memory.
+cudaError_t launch_widen_deltas(const void* src, int src_bits, void* dst, int dst_bits, uint64_t n,
+                                cudaStream_t s);
 cudaError_t launch_cs_update(const SketchParams& sp, const void* keys, int key_width, const void* w,
                              int w_kind, uint64_t n, int64_t* table, cudaStream_t s);
 // heavy-hitter pipeline for tables larger than shared memory (kernels_hot.cu);

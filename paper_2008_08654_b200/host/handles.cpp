@@ -81,6 +81,12 @@ int mb200_sketch_process(mb200_sketch* s, const void* h_keys, int key_width, con
     return guarded([&] { s->sk.process_batch(h_keys, key_width, h_weights, weight_kind, n); });
 }
 
+int mb200_sketch_h2d_bytes(const mb200_sketch* s, uint64_t* out) {
+    if (!s || !out) return mb200::fail(MB200_INVALID_ARGUMENT, "null argument");
+    *out = s->sk.h2d_bytes();
+    return MB200_OK;
+}
+
 int mb200_sketch_process_device(mb200_sketch* s, const void* d_keys, int key_width, const void* d_weights,
                                 int weight_kind, uint64_t n, void* stream) {
     if (!s) return mb200::fail(MB200_INVALID_ARGUMENT, "null sketch");

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <limits>
 #include <stdexcept>
 #include <string>
 
@@ -193,19 +194,53 @@ struct CountSketch::Staging {
     cudaStream_t copy = nullptr;
     cudaEvent_t ready[2] = {nullptr, nullptr};
     cudaEvent_t freed[2] = {nullptr, nullptr};
+    cudaEvent_t shipped[2] = {nullptr, nullptr};  // narrowed deltas of the slot have left host memory
     void* d_keys[2] = {nullptr, nullptr};
     void* d_w[2] = {nullptr, nullptr};
+    void* d_wn[2] = {nullptr, nullptr};  // narrowed deltas as they arrive
+    void* h_wn[2] = {nullptr, nullptr};  // pinned host staging of the narrowed deltas
     u64 chunk = 0;
+    int narrow_bits = 8;  // width tried first for the next chunk
+    u64 h2d_bytes = 0;    // bytes process_batch moved host -> device
     ~Staging() {
         for (int i = 0; i < 2; ++i) {
             cudaFree(d_keys[i]);
             cudaFree(d_w[i]);
+            cudaFree(d_wn[i]);
+            cudaFreeHost(h_wn[i]);
             if (ready[i]) cudaEventDestroy(ready[i]);
             if (freed[i]) cudaEventDestroy(freed[i]);
+            if (shipped[i]) cudaEventDestroy(shipped[i]);
         }
         if (copy) cudaStreamDestroy(copy);
     }
 };
+
+namespace {
+// Copies src[0, m) into dst as Dst while checking that every value fits Dst;
+// false if one does not (dst is then garbage).  Parallel over the host cores.
+template <typename Dst, typename Src>
+bool pack_narrow(const Src* src, Dst* dst, u64 m) {
+    constexpr Src lo = std::numeric_limits<Dst>::min(), hi = std::numeric_limits<Dst>::max();
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad) if (m >= (u64(1) << 16))
+    for (long long i = 0; i < (long long)m; ++i) {
+        const Src v = src[i];
+        bad |= (v < lo) | (v > hi);
+        dst[i] = Dst(v);
+    }
+    return !bad;
+}
+
+// Narrowest of {i8, i16} holding every delta of the chunk, starting at `first`
+// (the width the previous chunk needed); 0 = ship the deltas as they are.
+template <typename Src>
+int narrow_chunk(const Src* src, void* dst, u64 m, int first) {
+    if (first <= 8 && pack_narrow<int8_t>(src, (int8_t*)dst, m)) return 8;
+    if (first <= 16 && pack_narrow<int16_t>(src, (int16_t*)dst, m)) return 16;
+    return 0;
+}
+}  // namespace
 
 CountSketch::CountSketch(unsigned rows, u64 width, const MersenneModulus& modulus, u128 key_domain,
                          Splitter splitter, u64 seed, unsigned independence)
@@ -310,12 +345,17 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
     Staging& st = *staging_;
     const u64 want = std::min<u64>(n, u64(1) << 24);
     if (st.chunk < want) {
+        // the previous call's copies and kernels have completed (it synchronised)
         for (int i = 0; i < 2; ++i) {
             cudaFree(st.d_keys[i]);
             cudaFree(st.d_w[i]);
-            st.d_keys[i] = st.d_w[i] = nullptr;
+            cudaFree(st.d_wn[i]);
+            cudaFreeHost(st.h_wn[i]);
+            st.d_keys[i] = st.d_w[i] = st.d_wn[i] = st.h_wn[i] = nullptr;
             cuda_check(cudaMalloc(&st.d_keys[i], want * 8), "cudaMalloc staging");
             cuda_check(cudaMalloc(&st.d_w[i], want * 8), "cudaMalloc staging");
+            cuda_check(cudaMalloc(&st.d_wn[i], want * 2), "cudaMalloc staging");
+            cuda_check(cudaHostAlloc(&st.h_wn[i], want * 2, cudaHostAllocDefault), "cudaHostAlloc staging");
         }
         st.chunk = want;
     }
@@ -324,25 +364,50 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
         for (int i = 0; i < 2; ++i) {
             cuda_check(cudaEventCreateWithFlags(&st.ready[i], cudaEventDisableTiming), "event");
             cuda_check(cudaEventCreateWithFlags(&st.freed[i], cudaEventDisableTiming), "event");
+            cuda_check(cudaEventCreateWithFlags(&st.shipped[i], cudaEventDisableTiming), "event");
         }
     }
     const mb200_sketch_desc d = desc();
     cudaStream_t cs = (cudaStream_t)stream_;
     const u64 chunks = (n + st.chunk - 1) / st.chunk;
+    st.narrow_bits = 8;
     for (u64 c = 0; c < chunks; ++c) {
         const int slot = int(c & 1);
         const u64 off = c * st.chunk;
         const u64 m = std::min<u64>(st.chunk, n - off);
+        // Deltas cross PCIe in the narrowest of i8 / i16 that holds the whole
+        // chunk (packed here on the host cores while the previous chunk is in
+        // flight, sign-extended back on the device): PCIe is the bound of this
+        // call, and config 5's |delta| <= 100 ship 5 instead of 8 bytes per item.
+        // Updates are bit-identical; a chunk that fits neither ships as is.
+        int nbits = 0;
+        if (wbytes) {
+            if (c >= 2) cuda_check(cudaEventSynchronize(st.shipped[slot]), "sync staging");
+            const char* src = (const char*)h_weights + off * wbytes;
+            nbits = weight_kind == MB200_W_I32 ? narrow_chunk((const int32_t*)src, st.h_wn[slot], m, st.narrow_bits)
+                                               : narrow_chunk((const int64_t*)src, st.h_wn[slot], m, st.narrow_bits);
+            st.narrow_bits = nbits ? nbits : 64;
+        }
         if (c >= 2) cuda_check(cudaStreamWaitEvent(st.copy, st.freed[slot], 0), "wait");
         cuda_check(cudaMemcpyAsync(st.d_keys[slot], (const char*)h_keys + off * kbytes, m * kbytes,
                                    cudaMemcpyHostToDevice, st.copy),
                    "H2D keys");
-        if (wbytes)
+        st.h2d_bytes += m * kbytes;
+        if (nbits) {
+            cuda_check(cudaMemcpyAsync(st.d_wn[slot], st.h_wn[slot], m * (nbits / 8), cudaMemcpyHostToDevice, st.copy),
+                       "H2D weights");
+            cuda_check(cudaEventRecord(st.shipped[slot], st.copy), "record");
+            st.h2d_bytes += m * (nbits / 8);
+        } else if (wbytes) {
             cuda_check(cudaMemcpyAsync(st.d_w[slot], (const char*)h_weights + off * wbytes, m * wbytes,
                                        cudaMemcpyHostToDevice, st.copy),
                        "H2D weights");
+            cuda_check(cudaEventRecord(st.shipped[slot], st.copy), "record");
+            st.h2d_bytes += m * wbytes;
+        }
         cuda_check(cudaEventRecord(st.ready[slot], st.copy), "record");
         cuda_check(cudaStreamWaitEvent(cs, st.ready[slot], 0), "wait");
+        if (nbits) cuda_check(mb200::launch_widen_deltas(st.d_wn[slot], nbits, st.d_w[slot], weight_kind, m, cs), "widen");
         // keys were validated on the host above: skip the per-chunk device check
         throw_status(mb200::cs_update_nocheck(&d, st.d_keys[slot], key_width, wbytes ? st.d_w[slot] : nullptr, weight_kind,
                                      m, d_counters_, cs));
@@ -350,6 +415,8 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
     }
     cuda_check(cudaStreamSynchronize(cs), "sync");
 }
+
+u64 CountSketch::h2d_bytes() const { return staging_ ? staging_->h2d_bytes : 0; }
 
 void CountSketch::process(u128 x, i64 delta) {
     if (x >= key_domain()) throw std::domain_error("key outside domain");

@@ -844,3 +844,53 @@ def test_enum_moment_mean_exact_b7(cuda, mb):
         assert all(x["pass"] for x in rep["checks"]), rep["checks"]
         f1, f2 = 1, 25 + 49 + 4 + 1
         assert Fraction(rep["sums"]["sum_x"], 127 ** 4) == Fraction(f2 * 127 ** 2 + f1 * f1 - f2, 127 ** 2)
+
+
+# ------------------------------------------------- host API delta transport
+@pytest.mark.parametrize("wdtype", [np.int32, np.int64])
+@pytest.mark.parametrize("mag,nbytes", [(100, 1), (128, 2), (30000, 2), (1 << 20, None)])
+def test_host_process_narrowed_deltas(cuda, mb, orc, wdtype, mag, nbytes):
+    """mb200_sketch_process ships each chunk's deltas in the narrowest of i8 / i16
+    that holds them (else as given) and widens them on the device: counters equal
+    the oracle's for deltas at and just past each width's edge, and the reported
+    H2D bytes show which width crossed."""
+    rng = np.random.default_rng(mag)
+    n = 5000
+    keys = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    d = rng.integers(-mag, mag + 1, n).astype(wdtype)
+    d[:4] = [mag, -mag, mag - 1, -mag - 1 if mag < 1 << 20 else -mag]
+    sk = mb.CountSketch(5, 1 << 16, 61, 32, mb.SPLIT_POW2, 0x5EED)
+    b0 = sk.h2d_bytes()
+    sk.process(keys, d)
+    fams = [orc.coeffs(61, 4, s) for s in orc.row_seeds(0x5EED, 5)]
+    exp = orc.cs_process(5, 1 << 16, 61, fams, 32, mb.SPLIT_POW2, keys.astype(np.uint64), d.astype(np.int64))
+    assert (sk.counters() == exp).all()
+    wb = nbytes if nbytes else np.dtype(wdtype).itemsize
+    if mag == 128:  # -129 is in the stream: i8 fails, i16 holds it
+        wb = 2
+    assert sk.h2d_bytes() - b0 == n * 4 + n * wb
+
+
+def test_host_process_mixed_width_chunks(cuda, mb):
+    """Three 2^24-item chunks in one call: i8-sized deltas, a chunk with one i32
+    extreme (ships at full width), then small deltas again; equal to the device
+    entry on the same items (itself pinned to the oracle above)."""
+    import torch
+
+    C = 1 << 24
+    n = 2 * C + 1000
+    rng = np.random.default_rng(7)
+    keys = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    d = rng.integers(-100, 101, n).astype(np.int32)
+    d[C + 12345] = np.iinfo(np.int32).max
+    d[C + 99] = np.iinfo(np.int32).min
+    sk = mb.CountSketch(5, 1 << 16, 61, 32, mb.SPLIT_POW2, 3)
+    sk.process(keys, d)
+    assert sk.h2d_bytes() == n * 4 + C * 1 + (C + 1000) * 4
+    spec = mb.SketchSpec.seeded(5, 1 << 16, 61, 32, mb.SPLIT_POW2, 3)
+    table = torch.zeros(5 << 16, dtype=torch.int64, device="cuda")
+    mb.cs_update(spec, dev(keys), table, torch.from_numpy(d).cuda())
+    assert (sk.counters() == table.cpu().numpy()).all()
+    # a second call starts narrow again
+    sk.process(keys[:1000], d[:1000])
+    assert sk.h2d_bytes() == n * 4 + C * 1 + (C + 1000) * 4 + 1000 * 5

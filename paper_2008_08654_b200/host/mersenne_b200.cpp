@@ -199,6 +199,7 @@ struct CountSketch::Staging {
     void* d_w[2] = {nullptr, nullptr};
     void* d_wn[2] = {nullptr, nullptr};  // narrowed deltas as they arrive
     void* h_wn[2] = {nullptr, nullptr};  // pinned host staging of the narrowed deltas
+    void* h_kn[2] = {nullptr, nullptr};  // pinned host staging of u64 keys narrowed to u32
     u64 chunk = 0;
     int narrow_bits = 8;  // width tried first for the next chunk
     u64 h2d_bytes = 0;    // bytes process_batch moved host -> device
@@ -208,6 +209,7 @@ struct CountSketch::Staging {
             cudaFree(d_w[i]);
             cudaFree(d_wn[i]);
             cudaFreeHost(h_wn[i]);
+            cudaFreeHost(h_kn[i]);
             if (ready[i]) cudaEventDestroy(ready[i]);
             if (freed[i]) cudaEventDestroy(freed[i]);
             if (shipped[i]) cudaEventDestroy(shipped[i]);
@@ -334,11 +336,22 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
     const unsigned kb = families_.front().key_bits();
     if (kb < unsigned(key_width)) {  // all-or-nothing domain check before any update (polyhash.cpp:60)
         const u64 lim = u64(1) << kb;
-        for (u64 i = 0; i < n; ++i) {
-            const u64 x = key_width == 32 ? ((const uint32_t*)h_keys)[i] : ((const u64*)h_keys)[i];
-            if (x >= lim) throw std::domain_error("key outside domain");
+        int bad = 0;
+        if (key_width == 32) {
+            const uint32_t* k = (const uint32_t*)h_keys;
+#pragma omp parallel for schedule(static) reduction(| : bad) if (n >= (u64(1) << 16))
+            for (long long i = 0; i < (long long)n; ++i) bad |= k[i] >= lim;
+        } else {
+            const u64* k = (const u64*)h_keys;
+#pragma omp parallel for schedule(static) reduction(| : bad) if (n >= (u64(1) << 16))
+            for (long long i = 0; i < (long long)n; ++i) bad |= k[i] >= lim;
         }
+        if (bad) throw std::domain_error("key outside domain");
     }
+    // 64-bit keys of a <= 32-bit domain (checked above) cross PCIe as u32: the
+    // kernels hash the key's value, whatever width it arrives in
+    const bool narrow_keys = key_width == 64 && kb <= 32;
+    const int kw_dev = narrow_keys ? 32 : key_width;
     const size_t kbytes = key_width / 8;
     const size_t wbytes = weight_kind == MB200_W_NONE ? 0 : size_t(weight_kind) / 8;
     if (!staging_) staging_ = std::make_unique<Staging>();
@@ -351,11 +364,13 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
             cudaFree(st.d_w[i]);
             cudaFree(st.d_wn[i]);
             cudaFreeHost(st.h_wn[i]);
-            st.d_keys[i] = st.d_w[i] = st.d_wn[i] = st.h_wn[i] = nullptr;
+            cudaFreeHost(st.h_kn[i]);
+            st.d_keys[i] = st.d_w[i] = st.d_wn[i] = st.h_wn[i] = st.h_kn[i] = nullptr;
             cuda_check(cudaMalloc(&st.d_keys[i], want * 8), "cudaMalloc staging");
             cuda_check(cudaMalloc(&st.d_w[i], want * 8), "cudaMalloc staging");
             cuda_check(cudaMalloc(&st.d_wn[i], want * 2), "cudaMalloc staging");
             cuda_check(cudaHostAlloc(&st.h_wn[i], want * 2, cudaHostAllocDefault), "cudaHostAlloc staging");
+            cuda_check(cudaHostAlloc(&st.h_kn[i], want * 4, cudaHostAllocDefault), "cudaHostAlloc staging");
         }
         st.chunk = want;
     }
@@ -380,36 +395,45 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
         // flight, sign-extended back on the device): PCIe is the bound of this
         // call, and config 5's |delta| <= 100 ship 5 instead of 8 bytes per item.
         // Updates are bit-identical; a chunk that fits neither ships as is.
+        if (c >= 2 && (wbytes || narrow_keys)) cuda_check(cudaEventSynchronize(st.shipped[slot]), "sync staging");
         int nbits = 0;
         if (wbytes) {
-            if (c >= 2) cuda_check(cudaEventSynchronize(st.shipped[slot]), "sync staging");
             const char* src = (const char*)h_weights + off * wbytes;
             nbits = weight_kind == MB200_W_I32 ? narrow_chunk((const int32_t*)src, st.h_wn[slot], m, st.narrow_bits)
                                                : narrow_chunk((const int64_t*)src, st.h_wn[slot], m, st.narrow_bits);
             st.narrow_bits = nbits ? nbits : 64;
         }
+        if (narrow_keys) {
+            const u64* src = (const u64*)h_keys + off;
+            uint32_t* dst = (uint32_t*)st.h_kn[slot];
+#pragma omp parallel for schedule(static) if (m >= (u64(1) << 16))
+            for (long long i = 0; i < (long long)m; ++i) dst[i] = uint32_t(src[i]);
+        }
         if (c >= 2) cuda_check(cudaStreamWaitEvent(st.copy, st.freed[slot], 0), "wait");
-        cuda_check(cudaMemcpyAsync(st.d_keys[slot], (const char*)h_keys + off * kbytes, m * kbytes,
-                                   cudaMemcpyHostToDevice, st.copy),
-                   "H2D keys");
-        st.h2d_bytes += m * kbytes;
+        if (narrow_keys)
+            cuda_check(cudaMemcpyAsync(st.d_keys[slot], st.h_kn[slot], m * 4, cudaMemcpyHostToDevice, st.copy),
+                       "H2D keys");
+        else
+            cuda_check(cudaMemcpyAsync(st.d_keys[slot], (const char*)h_keys + off * kbytes, m * kbytes,
+                                       cudaMemcpyHostToDevice, st.copy),
+                       "H2D keys");
+        st.h2d_bytes += m * (narrow_keys ? 4 : kbytes);
         if (nbits) {
             cuda_check(cudaMemcpyAsync(st.d_wn[slot], st.h_wn[slot], m * (nbits / 8), cudaMemcpyHostToDevice, st.copy),
                        "H2D weights");
-            cuda_check(cudaEventRecord(st.shipped[slot], st.copy), "record");
             st.h2d_bytes += m * (nbits / 8);
         } else if (wbytes) {
             cuda_check(cudaMemcpyAsync(st.d_w[slot], (const char*)h_weights + off * wbytes, m * wbytes,
                                        cudaMemcpyHostToDevice, st.copy),
                        "H2D weights");
-            cuda_check(cudaEventRecord(st.shipped[slot], st.copy), "record");
             st.h2d_bytes += m * wbytes;
         }
+        cuda_check(cudaEventRecord(st.shipped[slot], st.copy), "record");
         cuda_check(cudaEventRecord(st.ready[slot], st.copy), "record");
         cuda_check(cudaStreamWaitEvent(cs, st.ready[slot], 0), "wait");
         if (nbits) cuda_check(mb200::launch_widen_deltas(st.d_wn[slot], nbits, st.d_w[slot], weight_kind, m, cs), "widen");
         // keys were validated on the host above: skip the per-chunk device check
-        throw_status(mb200::cs_update_nocheck(&d, st.d_keys[slot], key_width, wbytes ? st.d_w[slot] : nullptr, weight_kind,
+        throw_status(mb200::cs_update_nocheck(&d, st.d_keys[slot], kw_dev, wbytes ? st.d_w[slot] : nullptr, weight_kind,
                                      m, d_counters_, cs));
         cuda_check(cudaEventRecord(st.freed[slot], cs), "record");
     }

@@ -894,3 +894,28 @@ def test_host_process_mixed_width_chunks(cuda, mb):
     # a second call starts narrow again
     sk.process(keys[:1000], d[:1000])
     assert sk.h2d_bytes() == n * 4 + C * 1 + (C + 1000) * 4 + 1000 * 5
+
+
+@pytest.mark.parametrize("key_bits", [32, 64])
+def test_host_process_u64_keys(cuda, mb, orc, key_bits):
+    """u64 keys of a 32-bit domain cross PCIe as u32 after the (parallel)
+    all-or-nothing domain check; a 64-bit domain ships them whole.  Counters
+    equal the oracle's either way."""
+    rng = np.random.default_rng(key_bits)
+    n = (1 << 17) + 3  # the parallel check and packing paths
+    keys = rng.integers(0, 1 << key_bits, n, dtype=np.uint64)
+    keys[:3] = [0, (1 << key_bits) - 1, 1 << (key_bits - 1)]
+    d = rng.integers(-100, 101, n).astype(np.int64)
+    b = 61 if key_bits == 32 else 89
+    sk = mb.CountSketch(2, 1 << 16, b, key_bits, mb.SPLIT_POW2, 11)
+    sk.process(keys, d)
+    assert sk.h2d_bytes() == n * (4 if key_bits == 32 else 8) + n * 1
+    fams = [orc.coeffs(b, 4, s) for s in orc.row_seeds(11, 2)]
+    exp = orc.cs_process(2, 1 << 16, b, fams, key_bits, mb.SPLIT_POW2, keys, d)
+    assert (sk.counters() == exp).all()
+    if key_bits == 32:
+        bad = keys.copy()
+        bad[n - 1] = 1 << 32  # last item out of domain: nothing may be applied
+        with pytest.raises(mb.DomainError, match="key outside domain"):
+            sk.process(bad, d)
+        assert (sk.counters() == exp).all()

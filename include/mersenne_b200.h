@@ -188,6 +188,11 @@ int mb200_sketch_process(mb200_sketch* s, const void* h_keys, int key_width, con
  * plus deltas; deltas travel narrowed to i8 / i16 when a chunk fits).  A
  * transport statistic with no reference counterpart. */
 int mb200_sketch_h2d_bytes(const mb200_sketch* s, uint64_t* out);
+/* host threads mb200_sketch_process packs and checks with (0 = automatic:
+ * this process's CPUs divided by LOCAL_WORLD_SIZE); with fewer than 6 the
+ * inputs ship unnarrowed.  No reference counterpart. */
+void mb200_set_host_threads(int n);
+int mb200_host_threads(void);
 /* same on DEVICE arrays, asynchronous on `stream` */
 int mb200_sketch_process_device(mb200_sketch* s, const void* d_keys, int key_width,
                                 const void* d_weights, int weight_kind, uint64_t n, void* stream);

@@ -196,4 +196,10 @@ private:
     std::unique_ptr<Staging> staging_;
 };
 
+// Host threads CountSketch::process_batch uses to pack and check its inputs
+// (0 = automatic: this process's CPUs / LOCAL_WORLD_SIZE); below 6 the
+// deltas and keys ship unnarrowed.
+void set_host_threads(int n);
+int get_host_threads();
+
 }  // namespace mersenne::b200

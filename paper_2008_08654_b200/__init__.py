@@ -253,6 +253,15 @@ class SketchSpec:
                    splitter)
 
 
+def set_host_threads(n: int) -> None:
+    """Host threads CountSketch.process packs and checks with (0 = automatic)."""
+    lib.mb200_set_host_threads(int(n))
+
+
+def host_threads() -> int:
+    return lib.mb200_host_threads()
+
+
 def cs_update(spec: SketchSpec, keys, counters, weights=None, stream=None):
     """Fused K3+K4 scatter of a device batch into `counters` (int64, rows*width)."""
     check(lib.mb200_cs_update(C.byref(spec.desc), _dptr(keys), _key_width(keys), _dptr(weights),

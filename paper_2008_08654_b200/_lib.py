@@ -95,6 +95,8 @@ SIGNATURES = [
     ("mb200_sketch_process", I, [P, P, I, P, I, u64]),
     ("mb200_sketch_process_device", I, [P, P, I, P, I, u64, P]),
     ("mb200_sketch_h2d_bytes", I, [P, P]),
+    ("mb200_set_host_threads", None, [I]),
+    ("mb200_host_threads", I, []),
     ("mb200_sketch_row_second_moment", I, [P, U, P, P, P]),
     ("mb200_sketch_second_moment", I, [P, I, P, P, P]),
     ("mb200_sketch_point_query", I, [P, P, I, u64, P]),

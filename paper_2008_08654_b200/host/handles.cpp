@@ -81,6 +81,9 @@ int mb200_sketch_process(mb200_sketch* s, const void* h_keys, int key_width, con
     return guarded([&] { s->sk.process_batch(h_keys, key_width, h_weights, weight_kind, n); });
 }
 
+void mb200_set_host_threads(int n) { mersenne::b200::set_host_threads(n); }
+int mb200_host_threads(void) { return mersenne::b200::get_host_threads(); }
+
 int mb200_sketch_h2d_bytes(const mb200_sketch* s, uint64_t* out) {
     if (!s || !out) return mb200::fail(MB200_INVALID_ARGUMENT, "null argument");
     *out = s->sk.h2d_bytes();

@@ -6,11 +6,16 @@
 
 #include <cuda_runtime.h>
 
+#include <sched.h>
+
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 #include "../csrc/mb200_capi_util.h"
 
@@ -219,13 +224,41 @@ struct CountSketch::Staging {
 };
 
 namespace {
+// Host threads for the transport packing and the domain check: set by
+// mb200_set_host_threads, else the CPUs in this process's affinity mask shared
+// among the ranks a launcher started on this node (LOCAL_WORLD_SIZE, which
+// torchrun sets), one left free from 8 on.  OMP_NUM_THREADS is not consulted:
+// torchrun forces it to 1.  Packing loops are scheduled dynamically in 2^15-item
+// blocks so a descheduled thread does not stall the chunk.
+std::atomic<int> g_host_threads{0};
+int auto_host_threads() {
+    static const int t = [] {
+        int n = 0;
+        cpu_set_t set;
+        if (sched_getaffinity(0, sizeof set, &set) == 0) n = CPU_COUNT(&set);
+        if (n <= 0) n = int(std::thread::hardware_concurrency());
+        int local = 1;
+        if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) local = std::max(1, std::atoi(e));
+        n /= local;
+        return std::max(1, n >= 8 ? n - 1 : n);  // one core left to the caller's other threads
+    }();
+    return t;
+}
+int host_threads() {
+    const int t = g_host_threads.load(std::memory_order_relaxed);
+    return t > 0 ? t : auto_host_threads();
+}
+// Narrowing pays only when packing a chunk outruns the PCIe time it saves
+// (about 6 cores against ~55 GB/s at i32 -> i8); fewer threads ship as given.
+constexpr int kNarrowMinThreads = 6;
+
 // Copies src[0, m) into dst as Dst while checking that every value fits Dst;
 // false if one does not (dst is then garbage).  Parallel over the host cores.
 template <typename Dst, typename Src>
 bool pack_narrow(const Src* src, Dst* dst, u64 m) {
     constexpr Src lo = std::numeric_limits<Dst>::min(), hi = std::numeric_limits<Dst>::max();
     int bad = 0;
-#pragma omp parallel for schedule(static) reduction(| : bad) if (m >= (u64(1) << 16))
+#pragma omp parallel for schedule(dynamic, 1 << 15) reduction(| : bad) num_threads(host_threads()) if (m >= (u64(1) << 16))
     for (long long i = 0; i < (long long)m; ++i) {
         const Src v = src[i];
         bad |= (v < lo) | (v > hi);
@@ -339,18 +372,19 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
         int bad = 0;
         if (key_width == 32) {
             const uint32_t* k = (const uint32_t*)h_keys;
-#pragma omp parallel for schedule(static) reduction(| : bad) if (n >= (u64(1) << 16))
+#pragma omp parallel for schedule(static) reduction(| : bad) num_threads(host_threads()) if (n >= (u64(1) << 16))
             for (long long i = 0; i < (long long)n; ++i) bad |= k[i] >= lim;
         } else {
             const u64* k = (const u64*)h_keys;
-#pragma omp parallel for schedule(static) reduction(| : bad) if (n >= (u64(1) << 16))
+#pragma omp parallel for schedule(static) reduction(| : bad) num_threads(host_threads()) if (n >= (u64(1) << 16))
             for (long long i = 0; i < (long long)n; ++i) bad |= k[i] >= lim;
         }
         if (bad) throw std::domain_error("key outside domain");
     }
     // 64-bit keys of a <= 32-bit domain (checked above) cross PCIe as u32: the
     // kernels hash the key's value, whatever width it arrives in
-    const bool narrow_keys = key_width == 64 && kb <= 32;
+    const bool narrow = host_threads() >= kNarrowMinThreads;
+    const bool narrow_keys = narrow && key_width == 64 && kb <= 32;
     const int kw_dev = narrow_keys ? 32 : key_width;
     const size_t kbytes = key_width / 8;
     const size_t wbytes = weight_kind == MB200_W_NONE ? 0 : size_t(weight_kind) / 8;
@@ -395,9 +429,9 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
         // flight, sign-extended back on the device): PCIe is the bound of this
         // call, and config 5's |delta| <= 100 ship 5 instead of 8 bytes per item.
         // Updates are bit-identical; a chunk that fits neither ships as is.
-        if (c >= 2 && (wbytes || narrow_keys)) cuda_check(cudaEventSynchronize(st.shipped[slot]), "sync staging");
+        if (c >= 2 && narrow) cuda_check(cudaEventSynchronize(st.shipped[slot]), "sync staging");
         int nbits = 0;
-        if (wbytes) {
+        if (wbytes && narrow) {
             const char* src = (const char*)h_weights + off * wbytes;
             nbits = weight_kind == MB200_W_I32 ? narrow_chunk((const int32_t*)src, st.h_wn[slot], m, st.narrow_bits)
                                                : narrow_chunk((const int64_t*)src, st.h_wn[slot], m, st.narrow_bits);
@@ -406,7 +440,7 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
         if (narrow_keys) {
             const u64* src = (const u64*)h_keys + off;
             uint32_t* dst = (uint32_t*)st.h_kn[slot];
-#pragma omp parallel for schedule(static) if (m >= (u64(1) << 16))
+#pragma omp parallel for schedule(dynamic, 1 << 15) num_threads(host_threads()) if (m >= (u64(1) << 16))
             for (long long i = 0; i < (long long)m; ++i) dst[i] = uint32_t(src[i]);
         }
         if (c >= 2) cuda_check(cudaStreamWaitEvent(st.copy, st.freed[slot], 0), "wait");
@@ -441,6 +475,9 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
 }
 
 u64 CountSketch::h2d_bytes() const { return staging_ ? staging_->h2d_bytes : 0; }
+
+void set_host_threads(int n) { g_host_threads.store(n > 0 ? n : 0, std::memory_order_relaxed); }
+int get_host_threads() { return host_threads(); }
 
 void CountSketch::process(u128 x, i64 delta) {
     if (x >= key_domain()) throw std::domain_error("key outside domain");

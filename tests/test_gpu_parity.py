@@ -854,6 +854,7 @@ def test_host_process_narrowed_deltas(cuda, mb, orc, wdtype, mag, nbytes):
     that holds them (else as given) and widens them on the device: counters equal
     the oracle's for deltas at and just past each width's edge, and the reported
     H2D bytes show which width crossed."""
+    mb.set_host_threads(8)
     rng = np.random.default_rng(mag)
     n = 5000
     keys = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
@@ -877,6 +878,7 @@ def test_host_process_mixed_width_chunks(cuda, mb):
     entry on the same items (itself pinned to the oracle above)."""
     import torch
 
+    mb.set_host_threads(8)
     C = 1 << 24
     n = 2 * C + 1000
     rng = np.random.default_rng(7)
@@ -901,6 +903,7 @@ def test_host_process_u64_keys(cuda, mb, orc, key_bits):
     """u64 keys of a 32-bit domain cross PCIe as u32 after the (parallel)
     all-or-nothing domain check; a 64-bit domain ships them whole.  Counters
     equal the oracle's either way."""
+    mb.set_host_threads(8)
     rng = np.random.default_rng(key_bits)
     n = (1 << 17) + 3  # the parallel check and packing paths
     keys = rng.integers(0, 1 << key_bits, n, dtype=np.uint64)
@@ -919,3 +922,24 @@ def test_host_process_u64_keys(cuda, mb, orc, key_bits):
         with pytest.raises(mb.DomainError, match="key outside domain"):
             sk.process(bad, d)
         assert (sk.counters() == exp).all()
+
+
+def test_host_process_unnarrowed_with_few_threads(cuda, mb, orc):
+    """Below 6 host threads the inputs ship as given (packing would not outrun
+    PCIe); the counters are the same."""
+    rng = np.random.default_rng(5)
+    n = (1 << 17) + 1
+    keys = rng.integers(0, 1 << 32, n, dtype=np.uint64)
+    d = rng.integers(-100, 101, n).astype(np.int64)
+    try:
+        mb.set_host_threads(2)
+        assert mb.host_threads() == 2
+        sk = mb.CountSketch(2, 1 << 16, 61, 32, mb.SPLIT_POW2, 9)
+        sk.process(keys, d)
+        assert sk.h2d_bytes() == n * 16
+    finally:
+        mb.set_host_threads(0)
+    fams = [orc.coeffs(61, 4, s) for s in orc.row_seeds(9, 2)]
+    exp = orc.cs_process(2, 1 << 16, 61, fams, 32, mb.SPLIT_POW2, keys, d)
+    assert (sk.counters() == exp).all()
+    assert mb.host_threads() >= 1

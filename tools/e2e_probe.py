@@ -29,8 +29,33 @@ for _ in range(4):
 print(f"raw H2D: {2 * 4 * n / dt / 1e9:.1f} GB/s ({dt * 1e3:.1f} ms)")
 sk = mb.CountSketch(5, 1 << 16, 61, 32, mb.SPLIT_POW2, 1)
 hk_np, hw_np = hk.numpy(), hw.numpy()
-for rep in range(8):
-    t0 = time.perf_counter()
-    sk.process(hk_np, hw_np)
-    dt = time.perf_counter() - t0
-    print(f"process(): {n / dt / 1e9:.2f} G items/s, {2 * 4 * n / dt / 1e9:.1f} GB/s ({dt * 1e3:.1f} ms)")
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import threading  # noqa: E402
+
+# a background nvidia-smi sampler like bench.py's clocks thread (contention check)
+stop = threading.Event()
+
+
+def sampler():
+    while not stop.is_set():
+        subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm", "--format=csv,noheader"], capture_output=True)
+        time.sleep(0.2)
+
+
+threads = [int(t) for t in os.environ.get("THREADS", "0").split(",")]
+for with_sampler in (False, True):
+    if with_sampler:
+        th = threading.Thread(target=sampler, daemon=True)
+        th.start()
+    for t in threads:
+        mb.set_host_threads(t)
+        ms = []
+        for rep in range(8):
+            t0 = time.perf_counter()
+            sk.process(hk_np, hw_np)
+            ms.append((time.perf_counter() - t0) * 1e3)
+        ms = ms[2:]
+        print(f"threads={mb.host_threads():3d} sampler={with_sampler}: process() ms min {min(ms):.1f} "
+              f"median {statistics.median(ms):.1f} max {max(ms):.1f} -> {n / statistics.median(ms) / 1e6:.2f} G items/s")
+stop.set()

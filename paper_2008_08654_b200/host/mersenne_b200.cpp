@@ -227,10 +227,11 @@ namespace {
 // Host threads for the transport packing and the domain check: set by
 // mb200_set_host_threads, else the CPUs in this process's affinity mask shared
 // among the ranks a launcher started on this node (LOCAL_WORLD_SIZE, which
-// torchrun sets), one left free from 8 on.  OMP_NUM_THREADS is not consulted:
+// torchrun sets), one left free from 8 on, at most 8.  OMP_NUM_THREADS is not consulted:
 // torchrun forces it to 1.  Packing loops are scheduled dynamically in 2^15-item
 // blocks so a descheduled thread does not stall the chunk.
 std::atomic<int> g_host_threads{0};
+constexpr int kMaxAutoThreads = 8;
 int auto_host_threads() {
     static const int t = [] {
         int n = 0;
@@ -240,7 +241,8 @@ int auto_host_threads() {
         int local = 1;
         if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) local = std::max(1, std::atoi(e));
         n /= local;
-        return std::max(1, n >= 8 ? n - 1 : n);  // one core left to the caller's other threads
+        // one core left to the caller's other threads; 8 already outrun PCIe
+        return std::max(1, std::min(n >= 8 ? n - 1 : n, kMaxAutoThreads));
     }();
     return t;
 }
@@ -413,7 +415,9 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
         for (int i = 0; i < 2; ++i) {
             cuda_check(cudaEventCreateWithFlags(&st.ready[i], cudaEventDisableTiming), "event");
             cuda_check(cudaEventCreateWithFlags(&st.freed[i], cudaEventDisableTiming), "event");
-            cuda_check(cudaEventCreateWithFlags(&st.shipped[i], cudaEventDisableTiming), "event");
+            // the host sleeps on this one (it waits while the packing threads idle)
+            cuda_check(cudaEventCreateWithFlags(&st.shipped[i], cudaEventDisableTiming | cudaEventBlockingSync),
+                       "event");
         }
     }
     const mb200_sketch_desc d = desc();

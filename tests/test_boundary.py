@@ -148,3 +148,17 @@ def test_enum_moment_validation_without_gpu(mb):
     big = [(i, 1) for i in range(70)]
     with pytest.raises(mb.Unsupported, match="64 non-zero"):
         mb.enum_moment_sums(7, 4, 0, big)
+
+
+def test_host_threads_setting(mb):
+    """Packing threads of the host-buffer entry: explicit, then automatic (this
+    process's CPUs per local rank, one left free, at most 8)."""
+    try:
+        mb.set_host_threads(3)
+        assert mb.host_threads() == 3
+        mb.set_host_threads(0)
+        auto = mb.host_threads()
+        cpus = len(os.sched_getaffinity(0)) // int(os.environ.get("LOCAL_WORLD_SIZE", "1") or 1)
+        assert auto == max(1, min(cpus - 1 if cpus >= 8 else cpus, 8))
+    finally:
+        mb.set_host_threads(0)

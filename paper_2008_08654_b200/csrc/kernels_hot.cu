@@ -467,7 +467,8 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     cs_hot_kernel(const SketchParams sp, const KeyT* __restrict__ keys, const void* __restrict__ w, uint64_t n,
                   i64* __restrict__ table, const KeyT* __restrict__ layout, u64* __restrict__ slot_sum,
                   const u32* __restrict__ hot_sum, uint32_t sample, const MissBuf<KeyT> mb, bool vec_ok,
-                  u64* __restrict__ wraps) {
+                  u64* __restrict__ wraps, const u32* __restrict__ priv_go) {
+    if (priv_go && *priv_go == 0) return;  // cs_private_kernel took this stream
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
     using KV = KeyVec<KeyT>;
@@ -1094,6 +1095,84 @@ __global__ void __launch_bounds__(kAccThreads)
     if ((threadIdx.x & 31) == 0 && merged) atomicAdd(&g_hot_stats[6], (unsigned long long)merged);
 }
 
+// Private byte tables (streams without heavy hitters, unit deltas, rows x width
+// <= 200 KiB cells): every CTA keeps the WHOLE table in shared memory as 8-bit
+// cells (2^7-biased, four per 32-bit word), hashes each item once and adds +-1
+// to one cell per row with one shared atomic.  The atomic returns the word
+// before the add, so when the cell leaves [0, 2^8) every byte the carry or
+// borrow reached is compared before/after and the difference between intended
+// and displayed change goes to L2 (cell j receives intended_j - displayed_j):
+// per cell, displayed - bias + recorded = sum of its deltas, exactly, under any
+// interleaving and with no undo atomic.  The table is merged once per CTA.
+// Runs only when the probe found no heavy hitters (go[0] == 0); cs_hot_kernel
+// then returns at once.
+constexpr int kPrivThreads = 1024;
+
+__device__ __forceinline__ void byte_add(u32* words, uint64_t* cells_l2, u32 cell, i32 d) {
+    const u32 q = cell & 3u, sh = q * 8;
+    const u32 old = atomicAdd(words + (cell >> 2), (u32)d << sh);
+    const i32 nb = (i32)((old >> sh) & 0xffu) + d;
+    if ((u32)nb > 0xffu) {  // rare: the carry / borrow reached the bytes above
+        const u32 nw = old + ((u32)d << sh);
+        const u32 base = cell & ~3u;
+        for (u32 j = q; j < 4; ++j) {
+            const i32 disp = (i32)((nw >> (8 * j)) & 0xffu) - (i32)((old >> (8 * j)) & 0xffu);
+            const i32 rec = (j == q ? d : 0) - disp;
+            if (rec) red_add_u64(cells_l2 + base + j, (u64)(i64)rec);
+        }
+    }
+}
+
+template <int MODE, int K, int SPL, typename KeyT>
+__global__ void __launch_bounds__(kPrivThreads, 1)
+    cs_private_kernel(const SketchParams sp, const KeyT* __restrict__ keys, uint64_t n, i64* __restrict__ table,
+                      const u32* __restrict__ go) {
+    if (*go) return;
+    extern __shared__ __align__(16) u32 pwords[];
+    const u32 ncells = (u32)(sp.rows * sp.width), nw = ncells / 4;
+    for (u32 c = threadIdx.x; c < nw; c += kPrivThreads) pwords[c] = 0x80808080u;
+    __syncthreads();
+    constexpr uint32_t subs = SPL == SPC_TFO ? 2 : 1;
+    uint64_t* l2 = reinterpret_cast<uint64_t*>(table);
+    const u32 width = (u32)sp.width;
+    const uint64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += kPrivThreads) {
+        const u64 x = (u64)ld_nc(keys + i);
+#pragma unroll 1
+        for (uint32_t f = 0; f < sp.families; ++f) {
+            if constexpr ((MODE == M61_K32 || MODE == M61_K64) && K > 0 && SPL == SPC_POW2) {
+                bool neg;
+                const u32 idx = h61_pow2_split(hash61_lazy<MODE, K>(sp, f, x), width - 1, neg);
+                byte_add(pwords, l2, f * width + idx, neg ? -1 : 1);
+                continue;
+            }
+            u64 hlo, hhi = 0;
+            if (MODE == M89) hash89<K>(sp, f, x, hlo, hhi);
+            else hlo = hash_small<MODE, K>(sp, f, x);
+#pragma unroll
+            for (uint32_t sub = 0; sub < subs; ++sub) {
+                const uint32_t row = subs * f + sub;
+                if (row >= sp.rows) break;
+                bool neg;
+                const u32 idx = split_c<MODE, SPL>(sp, hlo, hhi, sub, neg);
+                byte_add(pwords, l2, row * width + idx, neg ? -1 : 1);
+            }
+        }
+    }
+    __syncthreads();
+    unsigned merged = 0;
+    for (u32 c = threadIdx.x; c < ncells; c += kPrivThreads) {
+        const i64 v = (i64)((pwords[c >> 2] >> ((c & 3) * 8)) & 0xffu) - 0x80;
+        if (v) {
+            red_add_u64(l2 + c, (u64)v);
+            ++merged;
+        }
+    }
+    merged = __reduce_add_sync(kFull, merged);
+    if ((threadIdx.x & 31) == 0 && merged) atomicAdd(&g_hot_stats[6], (unsigned long long)merged);
+    if (threadIdx.x == 0) atomicAdd(&g_hot_stats[0], (unsigned long long)(hi - lo));
+}
+
 inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 // large-table strategy (mb200_set_large_table_strategy): misses either go
@@ -1218,8 +1297,21 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     if ((e = cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbytes)) != cudaSuccess)
         return e;
     fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, cap, reinterpret_cast<KeyT*>(hot_cnt + G::kCap), layout);
+    // streams without heavy hitters and unit deltas whose whole table fits
+    // shared memory as bytes: private byte tables instead of one L2 reduction
+    // per row update
+    const uint64_t pcells = (uint64_t)sp.rows * sp.width;
+    const bool priv = !binned && WK == W_NONE && SPL != SPC_ANY && pcells <= 200u * 1024 && pcells % 4 == 0 &&
+                      sp.width % 4 == 0 && n >= (1u << 20);
+    if (priv) {
+        auto fp = cs_private_kernel<MODE, K, SPL, KeyT>;
+        if ((e = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcells)) != cudaSuccess)
+            return e;
+        fp<<<sms, kPrivThreads, pcells, s>>>(sp, keys, n, table, go);
+    }
     fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, layout, slot_sum, hot_sum,
-                                                          binned ? P.m : 0, mb, vec_ok, wraps);
+                                                          binned ? P.m : 0, mb, vec_ok, wraps,
+                                                          priv ? go : nullptr);
     hh_merge_kernel<MODE, K, SPL, KeyT><<<(G::kSlots + 255) / 256, 256, 0, s>>>(sp, layout, slot_sum, table);
     if ((e = cudaGetLastError()) != cudaSuccess || !binned) return e;
     auto fb_raw = g.bpr == 1 ? cs_bin_kernel<MODE, K, SPL, KeyT, WK, true, true>

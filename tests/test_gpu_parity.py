@@ -943,3 +943,28 @@ def test_host_process_unnarrowed_with_few_threads(cuda, mb, orc):
     exp = orc.cs_process(2, 1 << 16, 61, fams, 32, mb.SPLIT_POW2, keys, d)
     assert (sk.counters() == exp).all()
     assert mb.host_threads() >= 1
+
+
+@pytest.mark.parametrize("c0", [0x0123456789ABCDE, (1 << 61) - 2, 12345])
+def test_private_byte_tables_wrap_exactly(cuda, mb, orc, c0):
+    """Streams without heavy hitters, unit deltas and a table that fits shared
+    memory as bytes take the private byte tables (8-bit cells, four per word).
+    A constant polynomial sends all 2^23 distinct keys to one cell per row, so
+    every CTA's cell wraps hundreds of times (carry or borrow, any byte of the
+    word): the table still equals the oracle's, and no item went to L2
+    directly."""
+    import torch
+
+    n = 1 << 23
+    keys = (np.arange(n, dtype=np.uint64) * 2654435761 % (1 << 32)).astype(np.uint32)  # distinct
+    fam = [[c0, 0, 0, 0]]
+    spec = mb.SketchSpec(2, 1 << 16, 61, fam, 32, mb.SPLIT_TWO_FOR_ONE)
+    table = torch.zeros(2 << 16, dtype=torch.int64, device="cuda")
+    mb.hot_stats(reset=True)
+    mb.cs_update(spec, dev(keys), table)
+    hs = mb.hot_stats(reset=True)
+    exp = orc.cs_process(2, 1 << 16, 61, fam, 32, mb.SPLIT_TWO_FOR_ONE, keys)
+    got = table.cpu().numpy()
+    assert (got == exp).all()
+    assert np.count_nonzero(got) == 2 and abs(got).sum() == 2 * n
+    assert hs["direct"] == 0 and hs["bin_merges"] > 0

@@ -582,7 +582,10 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
     c4_reds = (2 * hs["hot_applied"] + hs["bin_merges"] + hs["direct"]) / (steps + max(3, args.warmup))
     out["c4"] = {"value": C4_KEYS / t, "unit": "keys/s", "row_updates_per_s": 2 * C4_KEYS / t,
                  "ms_per_step": t * 1e3, "workload": "2^89-1 two-for-one, 2^26 u64 keys, 2 x 2^16 counters",
-                 "l2": "inputs 512 MiB > L2", "roofline": roofline("c4", hi - lo, tk, "c4", l2_reds=c4_reds)}
+                 "l2": "inputs 512 MiB > L2", "roofline": roofline("c4", hi - lo, tk, "c4", l2_reds=c4_reds),
+                 "path": "cs_private_kernel (no heavy hitters, unit deltas: whole table per CTA in 8-bit shared "
+                         "cells); instruction-issue bound, see roofline.ncu_pipes.issue -- L2 reductions are only "
+                         "the per-CTA merges and byte carries"}
     del keys
 
     # ExactDivisionMap(PseudoMersenneModulus(64, 59), r) (bucketing.cpp:75-95)

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 import ncu_summary  # noqa: E402
 
-KERNEL_KEY = {"c5": "cs_update_kernel", "c1": "cs_update_kernel", "c4": "cs_update_kernel",
+KERNEL_KEY = {"c5": "cs_update_kernel", "c1": "cs_update_kernel", "c4": "cs_private_kernel",
               "c2k4": "hash61_key64_kernel", "c2k8": "hash61_key64_kernel", "c3": "pm_divmod_kernel"}
 
 

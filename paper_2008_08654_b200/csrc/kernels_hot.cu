@@ -1136,8 +1136,7 @@ __global__ void __launch_bounds__(kPrivThreads, 1)
     uint64_t* l2 = reinterpret_cast<uint64_t*>(table);
     const u32 width = (u32)sp.width;
     const uint64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += kPrivThreads) {
-        const u64 x = (u64)ld_nc(keys + i);
+    auto item = [&](u64 x) {
 #pragma unroll 1
         for (uint32_t f = 0; f < sp.families; ++f) {
             if constexpr ((MODE == M61_K32 || MODE == M61_K64) && K > 0 && SPL == SPC_POW2) {
@@ -1158,7 +1157,18 @@ __global__ void __launch_bounds__(kPrivThreads, 1)
                 byte_add(pwords, l2, row * width + idx, neg ? -1 : 1);
             }
         }
+    };
+    // four keys per thread in flight (the loop is otherwise load-latency bound)
+    constexpr int kU = 4;
+    uint64_t i = lo + threadIdx.x;
+    for (; i + (kU - 1) * kPrivThreads < hi; i += kU * kPrivThreads) {
+        u64 xs[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) xs[u] = (u64)ld_nc(keys + i + u * kPrivThreads);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) item(xs[u]);
     }
+    for (; i < hi; i += kPrivThreads) item((u64)ld_nc(keys + i));
     __syncthreads();
     unsigned merged = 0;
     for (u32 c = threadIdx.x; c < ncells; c += kPrivThreads) {

@@ -1158,8 +1158,8 @@ __global__ void __launch_bounds__(kPrivThreads, 1)
             }
         }
     };
-    // four keys per thread in flight (the loop is otherwise load-latency bound)
-    constexpr int kU = 4;
+    // eight keys per thread in flight (the loop is otherwise load-latency bound)
+    constexpr int kU = 8;
     uint64_t i = lo + threadIdx.x;
     for (; i + (kU - 1) * kPrivThreads < hi; i += kU * kPrivThreads) {
         u64 xs[kU];

@@ -175,7 +175,7 @@ __device__ __forceinline__ void small_vec(const SketchParams& sp, const u64* c, 
 }
 
 template <int K, int WK, int STRAT>
-__global__ void __launch_bounds__(kSmallThreads) cs_small_k32_kernel(const SketchParams sp,
+__global__ void __launch_bounds__(kSmallThreads, 1) cs_small_k32_kernel(const SketchParams sp,
                                                                       const u32* __restrict__ keys,
                                                                       const void* __restrict__ w, uint64_t n,
                                                                       i64* __restrict__ table) {
@@ -197,6 +197,19 @@ __global__ void __launch_bounds__(kSmallThreads) cs_small_k32_kernel(const Sketc
     const uint64_t nv = n / 4, stride = (uint64_t)gridDim.x * kSmallThreads;
     const int4 ones = make_int4(1, 1, 1, 1);
     uint64_t i = (uint64_t)blockIdx.x * kSmallThreads + threadIdx.x;
+    // four vectors (16 keys) per lane in flight: the loop is otherwise bound by
+    // the load latency
+    for (; i + 3 * stride < nv; i += 4 * stride) {
+        uint4 kv[4];
+        int4 wv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            kv[u] = ld_stream(k4 + i + u * stride);
+            wv[u] = WK == W_NONE ? ones : ld_stream(w4 + i + u * stride);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) small_vec<K, WK, STRAT>(sp, c, kv[u], wv[u], smem);
+    }
     for (; i + stride < nv; i += 2 * stride) {
         const uint4 ka = ld_stream(k4 + i), kb = ld_stream(k4 + i + stride);
         const int4 wa = WK == W_NONE ? ones : ld_stream(w4 + i);
@@ -361,8 +374,8 @@ cudaError_t launch_small_k32(const SketchParams& sp, const void* keys, const voi
     // one 1024-thread CTA per SM (two when the batch is large): the merge costs
     // one red.global per cell per CTA
     const uint64_t nv = n / 4;
-    uint64_t grid = (nv + 2 * kSmallThreads - 1) / (2 * kSmallThreads);
-    const uint64_t cap = (uint64_t)sm_count() * (n >= (1ull << 22) ? 2 : 1);
+    uint64_t grid = (nv + 4 * kSmallThreads - 1) / (4 * kSmallThreads);
+    const uint64_t cap = (uint64_t)sm_count();
     if (grid > cap) grid = cap;
     if (grid == 0) grid = 1;
     fn<<<(unsigned)grid, kSmallThreads, smem, s>>>(sp, (const u32*)keys, w, n, table);

@@ -435,7 +435,7 @@ def main():
             prev_ms = cur_ms
         barrier_sync()
         t0 = time.perf_counter()
-        e2e_steps = max(1, min(args.steps, 5))
+        e2e_steps = max(1, min(args.steps, 10))
         step_ms = []
         b0 = sk.h2d_bytes()
         for _ in range(e2e_steps):

@@ -2,7 +2,7 @@
 #
 #   make            -> paper_2008_08654_b200/libmersenne_b200.so + oracle/ (+ oracle/_ref if the
 #                      reference sources are present)
-#   make lib        -> the product library only
+#   make lib        -> the product library (+ the bench harness library)
 #   make cpptest    -> tests/cpp/test_host_api (C++ host-API tests, run by pytest -m gpu)
 PKG      := paper_2008_08654_b200
 CUDA     ?= /usr/local/cuda
@@ -13,18 +13,25 @@ CXXFLAGS := -O3 -g -std=c++20 -fPIC -Wall -Wextra -fopenmp -I$(CUDA)/include
 BUILD    := build
 
 CU_SRCS  := $(wildcard $(PKG)/csrc/*.cu)
+H_SRCS   := $(wildcard $(PKG)/harness/*.cu)
 CPP_SRCS := $(wildcard $(PKG)/host/*.cpp)
-HDRS     := $(wildcard $(PKG)/csrc/*.h $(PKG)/csrc/*.cuh include/*.h include/mersenne_b200/*.hpp)
+HDRS     := $(wildcard $(PKG)/csrc/*.h $(PKG)/csrc/*.cuh $(PKG)/harness/*.h include/*.h include/mersenne_b200/*.hpp)
 CU_OBJS  := $(patsubst $(PKG)/csrc/%.cu,$(BUILD)/%.cu.o,$(CU_SRCS))
 CPP_OBJS := $(patsubst $(PKG)/host/%.cpp,$(BUILD)/%.cpp.o,$(CPP_SRCS))
+H_OBJS   := $(patsubst $(PKG)/harness/%.cu,$(BUILD)/harness_%.cu.o,$(H_SRCS))
 LIB      := $(PKG)/libmersenne_b200.so
+HLIB     := $(PKG)/libmersenne_b200_harness.so
 
 .PHONY: all lib oracle cpptest clean
 all: lib oracle
 
-lib: $(LIB)
+lib: $(LIB) $(HLIB)
 
 $(BUILD)/%.cu.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(BUILD)/harness_%.cu.o: $(PKG)/harness/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
@@ -33,7 +40,11 @@ $(BUILD)/%.cpp.o: $(PKG)/host/%.cpp $(HDRS)
 	g++ $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(CU_OBJS) $(CPP_OBJS)
-	$(NVCC) $(ARCH) -shared -cudart shared -o $@ $^ -Xcompiler -fopenmp -Xlinker -rpath,'$$ORIGIN'
+	$(NVCC) $(ARCH) -shared -cudart shared -o $@ $^ -Xcompiler -fopenmp -ldl -Xlinker -rpath,'$$ORIGIN'
+
+# bench / test harness (generators, probes): a separate library, not the drop-in ABI
+$(HLIB): $(H_OBJS) $(LIB)
+	$(NVCC) $(ARCH) -shared -cudart shared -o $@ $(H_OBJS) -L$(PKG) -lmersenne_b200 -Xlinker -rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle all
@@ -44,5 +55,5 @@ cpptest: $(LIB) tests/cpp/test_host_api.cpp oracle
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle'
 
 clean:
-	rm -rf $(BUILD) $(LIB) tests/cpp/test_host_api
+	rm -rf $(BUILD) $(LIB) $(HLIB) tests/cpp/test_host_api
 	$(MAKE) -C oracle clean

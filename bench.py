@@ -67,6 +67,67 @@ def shard(n, rank, world):
     return n * rank // world, n * (rank + 1) // world
 
 
+class TableMerge:
+    """The N > 1 exchange step: ONE in-place allreduce of the rank-local
+    t x m counter table -- the distributed CountSketch::merge (sketch.cpp:182-193).
+    On GPUs it is the product's own entry, mb200_cs_allreduce, over an NCCL
+    communicator the product library made (mb.NcclComm); the table never leaves HBM.
+    Under gloo (the CPU tests) torch.distributed sums the CPU table instead."""
+
+    def __init__(self, mb, dist, world):
+        self.mb, self.dist, self.world, self.comm = mb, dist, world, None
+        self.kind = "none (one rank)"
+        if world > 1:
+            if dist.get_backend() == "nccl":
+                self.comm = mb.NcclComm.from_process_group()
+                self.kind = "mb200_cs_allreduce (NCCL uint64 sum, in place in HBM)"
+            else:
+                self.kind = f"torch.distributed.all_reduce ({dist.get_backend()}, CPU tables)"
+
+    def table(self, t, stream=None):
+        if self.world == 1:
+            return
+        if self.comm is not None:
+            self.mb.cs_allreduce(t, self.comm, stream)
+        else:
+            self.dist.all_reduce(t)
+
+    def sketch(self, sk):
+        """CountSketch.allreduce: the sketch object's HBM table summed in place."""
+        if self.world == 1:
+            return
+        if self.comm is not None:
+            sk.allreduce(self.comm)
+        else:
+            import torch
+            t = torch.from_numpy(sk.counters())
+            self.dist.all_reduce(t)
+            sk.set_counters(t.numpy())
+
+
+def sketch_step(ops, spec, keys, wts, table, mom, merge, ev=None):
+    """One step of a sharded Count Sketch config on one rank: zero the rank's table,
+    fused hash -> split -> scatter of its shard, merge over the ranks, estimator.
+    `ev` = (start, stop) events around the scatter kernel(s)."""
+    table.zero_()
+    if ev is not None:
+        ev[0].record()
+    ops.cs_update(spec, keys, table, wts)
+    if ev is not None:
+        ev[1].record()
+    merge.table(table)
+    ops.cs_moments(table, spec.rows, spec.width, mom)
+
+
+def e2e_step(sk, h_keys, h_wts, merge, zeros):
+    """The same step through the public host API: counters reset, process() of HOST
+    buffers (H2D inside), merge of the replicas' HBM tables, median F2 read back."""
+    sk.set_counters(zeros)
+    sk.process(h_keys, h_wts)
+    merge.sketch(sk)
+    return sk.second_moment(True)
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -252,6 +313,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    merge = TableMerge(mb, dist, world)
     hbm_peak, peak_kind = load_peaks()
     traffic = load_traffic()
 
@@ -336,15 +398,7 @@ def main():
             for _ in range(args.steps)]
 
     def c5_step(i=None):
-        table.zero_()
-        if i is not None:
-            k_ev[i][0].record()
-        mb.cs_update(spec, keys, table, wts)
-        if i is not None:
-            k_ev[i][1].record()
-        if world > 1:
-            dist.all_reduce(table)
-        mb.cs_moments(table, C5_ROWS, C5_WIDTH, mom)
+        sketch_step(mb, spec, keys, wts, table, mom, merge, None if i is None else k_ev[i])
 
     for _ in range(max(3, args.warmup)):
         c5_step()
@@ -376,6 +430,7 @@ def main():
         "config": {"workload": "config5_countsketch_t5_m65536_zipf1.2", "items": n_total,
                    "rows": C5_ROWS, "width": C5_WIDTH, "prime": "2^61-1", "k": 4, "split": "two-for-one pow2",
                    "weights": "int32 uniform [-100,100]", "parallelism": f"dp{world} (item shards + NCCL allreduce)",
+                   "merge": merge.kind,
                    "l2": "inputs 16 GiB >> 126 MB L2 (no flush needed)"},
         "hashes_per_s": value * C5_ROWS,
         "f2_median": str(f2[0]),
@@ -409,21 +464,18 @@ def main():
         torch.cuda.synchronize()
         sk = mb.CountSketch(C5_ROWS, C5_WIDTH, 61, 32, mb.SPLIT_POW2, S)
         hk_np, hw_np = hk.numpy(), hw.numpy()
+        zeros = np.zeros(C5_ROWS * C5_WIDTH, np.int64)
+        e2e_f2 = []
 
-        def e2e_step():
-            sk.set_counters(np.zeros(C5_ROWS * C5_WIDTH, np.int64))
-            sk.process(hk_np, hw_np)            # H2D of keys + weights inside, pipelined
-            if world > 1:
-                t = torch.from_numpy(sk.counters()).to(dev)
-                dist.all_reduce(t)
-            return sk.second_moment(True)       # D2H of the estimator
+        def one_e2e():
+            e2e_f2.append(e2e_step(sk, hk_np, hw_np, merge, zeros))
 
         # untimed warm-up until two consecutive steps agree within 3% (the first calls
         # size the pinned-copy pipeline; host-side transients settle), at most 8
         prev_ms = None
         for _ in range(8):
             ts = time.perf_counter()
-            e2e_step()
+            one_e2e()
             cur_ms = (time.perf_counter() - ts) * 1e3
             stable = prev_ms is not None and abs(cur_ms - prev_ms) <= 0.03 * prev_ms
             if world > 1:  # every rank leaves together (e2e_step holds a collective)
@@ -440,7 +492,7 @@ def main():
         b0 = sk.h2d_bytes()
         for _ in range(e2e_steps):
             ts = time.perf_counter()
-            e2e_step()
+            one_e2e()
             step_ms.append((time.perf_counter() - ts) * 1e3)
         barrier_sync()
         dt = max_over_ranks(time.perf_counter() - t0)
@@ -448,16 +500,18 @@ def main():
         # chunk fits) plus the counter reset
         h2d = (sk.h2d_bytes() - b0) // e2e_steps + C5_ROWS * C5_WIDTH * 8
         line["e2e"] = {"value": n_total * e2e_steps / dt, "unit": "updates/s",
-                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": C5_ROWS * 32 + (C5_ROWS * C5_WIDTH * 8 if world > 1 else 0),
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": C5_ROWS * 32,
                        "h2d_bytes_api_input": n_local * 8,
                        "h2d_gbs": h2d * e2e_steps / dt / 1e9, "step_ms": step_ms,
-                       "path": "mb200_sketch_process (host buffers, pinned; deltas narrowed to i8 on the host cores) + mb200_sketch_second_moment",
+                       "path": "mb200_sketch_process (host buffers, pinned; deltas narrowed to i8 on the host cores)"
+                               + (" + mb200_sketch_allreduce" if world > 1 else "") + " + mb200_sketch_second_moment",
+                       "f2_median": str(e2e_f2[-1][0]), "f2_matches_device_step": e2e_f2[-1][0] == f2[0],
                        "steps": e2e_steps}
         del sk, hk, hw
 
     # ---------------------------------------------------------- configs 1-4
     if not args.no_extras:
-        line["configs"] = bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ranks)
+        line["configs"] = bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ranks, merge)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference_c5(1 << 23)
@@ -490,7 +544,7 @@ def timed_steps(torch, steps, warmup, fn, flush=None):
     return tot / steps
 
 
-def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ranks):
+def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ranks, merge):
     out = {}
     SK = S ^ mb.SALT_KEYS
     steps = args.steps
@@ -507,22 +561,35 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
     mom = torch.empty((1, 4), dtype=torch.int64, device=dev)
 
     def c1():
+        sketch_step(mb, spec, keys, None, table, mom, merge)
+
+    # a ~50 us step of three launches: replayed as one CUDA graph (launch gaps out).
+    # With N > 1 the graph holds the rank-local part (zero + scatter) and the merge
+    # and estimator follow it eagerly.
+    def c1_local():
         table.zero_()
         mb.cs_update(spec, keys, table)
-        mb.cs_moments(table, 1, 1024, mom)
+        if world == 1:
+            mb.cs_moments(table, 1, 1024, mom)
 
-    # a ~50 us step of three launches: replayed as one CUDA graph (launch gaps out)
     step_fn, graphed = c1, False
     try:
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            c1()
+            c1_local()
         torch.cuda.current_stream().wait_stream(side)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            c1()
-        step_fn, graphed = graph.replay, True
+            c1_local()
+        if world == 1:
+            step_fn = graph.replay
+        else:
+            def step_fn():
+                graph.replay()
+                merge.table(table)
+                mb.cs_moments(table, 1, 1024, mom)
+        graphed = True
     except Exception as exc:  # eager launches when capture is unavailable
         print(f"config 1: graph capture failed ({exc}); eager", file=sys.stderr)
     t = max_over_ranks(timed_steps(torch, steps, args.warmup, step_fn, flush))
@@ -569,11 +636,7 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
     mom = torch.empty((2, 4), dtype=torch.int64, device=dev)
 
     def c4():
-        table.zero_()
-        mb.cs_update(spec, keys, table)
-        if world > 1:
-            dist.all_reduce(table)
-        mb.cs_moments(table, 2, 1 << 16, mom)
+        sketch_step(mb, spec, keys, None, table, mom, merge)
 
     t = max_over_ranks(timed_steps(torch, steps, args.warmup, c4))
     mb.hot_stats(reset=True)

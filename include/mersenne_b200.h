@@ -220,19 +220,33 @@ int mb200_sketch_serialize(mb200_sketch* s, uint8_t* out, uint64_t cap, uint64_t
  * stored seeds, counters uploaded to HBM; invalid_argument on malformed payloads */
 int mb200_sketch_deserialize(const uint8_t* bytes, uint64_t len, mb200_sketch** out);
 
-/* ------------------------------------- workload generators (bench harness) --- */
-int mb200_gen_u32_keys(uint64_t seed, uint64_t start, uint64_t n, uint32_t* d_out, void* stream);
-int mb200_gen_u64_keys(uint64_t seed, uint64_t start, uint64_t n, uint64_t* d_out, void* stream);
-int mb200_gen_below_p61(uint64_t seed, uint64_t start, uint64_t n, uint64_t* d_out,
-                        uint64_t* d_bad, void* stream);
-int mb200_gen_pm_inputs(uint64_t seed, uint64_t c, uint64_t start, uint64_t n, uint64_t* d_out,
-                        uint64_t* d_bad, void* stream);
-int mb200_zipf_table(double alpha, uint32_t T, double universe, uint64_t* h_cdf, double* tail_c1);
-int mb200_gen_zipf_items(uint64_t master_seed, const uint64_t* d_cdf, uint32_t T, double tail_c1,
-                         double universe, uint64_t start, uint64_t n, uint32_t* d_keys,
-                         int32_t* d_weights, void* stream);
+/* ------------------------------------------------------ multi-GPU merge --- */
+/* SURVEY 8b entry 6 / 8e: the per-GPU tables of one logical sketch (item stream
+ * sharded over the ranks) are summed by ONE in-place NCCL allreduce -- the
+ * distributed CountSketch::merge (sketch.cpp:182-193, wrapping u64 add).
+ * NCCL is bound at run time (dlopen "libnccl.so.2"; inside a process that
+ * already loaded NCCL, e.g. PyTorch, that copy is used): every entry returns
+ * MB200_UNSUPPORTED when no NCCL can be loaded.  A communicator is an
+ * ncclComm_t passed as void*: one made here, or any ncclComm_t of the same
+ * NCCL library the caller already owns. */
+#define MB200_NCCL_UNIQUE_ID_BYTES 128
+int mb200_nccl_version(int* version);
+/* ncclGetUniqueId: rank 0 calls it and ships the bytes to the other ranks */
+int mb200_nccl_unique_id(uint8_t out[MB200_NCCL_UNIQUE_ID_BYTES]);
+/* ncclCommInitRank on the CURRENT device (collective: every rank calls it) */
+int mb200_nccl_comm_init(int nranks, const uint8_t id[MB200_NCCL_UNIQUE_ID_BYTES], int rank,
+                         void** comm);
+int mb200_nccl_comm_destroy(void* comm);
+int mb200_nccl_comm_size(void* comm, int* nranks);
+/* In-place sum over the communicator's ranks of `count` counters (t x m of a
+ * sketch), asynchronous on `stream`: every rank ends with the merged table.
+ * Collective: every rank calls it with the same count. */
+int mb200_cs_allreduce(int64_t* d_counters, uint64_t count, void* nccl_comm, void* stream);
+/* the same on a sketch object's HBM table (its own stream; returns when the
+ * merged table is in place) -- CountSketch::allreduce */
+int mb200_sketch_allreduce(mb200_sketch* s, void* nccl_comm);
 
-/* ------------------------------------------------------------- probes --- */
+/* ------------------------------------------------------------- diagnostics --- */
 /* Counters of the heavy-hitter Count Sketch kernels since the last reset (device-
  * wide, synchronizes the device): [0] items, [1] items that missed the shared-
  * memory hot set, [2] hot keys applied (each once per call), [3] hot keys placed in
@@ -249,15 +263,6 @@ int mb200_hot_stats(uint64_t out[8], int reset);
 #define MB200_LARGE_DIRECT 0
 #define MB200_LARGE_BINNED 1
 int mb200_set_large_table_strategy(int strategy, int* previous);
-/* blocks x threads threads each issue 8 x iters independent mad.wide.u32 */
-int mb200_probe_imad(int blocks, int threads, int iters, uint64_t* d_sink, void* stream);
-int mb200_probe_atomics(int mode, int blocks, int threads, int iters, uint64_t* d_buf,
-                        uint64_t span, void* stream);
-/* cluster-of-`cluster` CTAs each owning `words` u32 cells in shared memory:
- * mode 0 random remote-or-local red.shared::cluster, 1 local only, 2 one hot cell */
-int mb200_probe_dsmem(int cluster, int mode, int blocks, int threads, int iters, uint32_t words,
-                      uint64_t* d_out, void* stream);
-
 #ifdef __cplusplus
 }
 #endif

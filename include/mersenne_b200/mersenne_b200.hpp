@@ -158,6 +158,10 @@ public:
     std::vector<i64> point_query_batch(const void* h_keys, int key_width, u64 n) const;
 
     CountSketch& merge(const CountSketch& other);  // requires identical seeds (sketch.cpp:182-193)
+    // merge() across GPUs: the tables of this sketch's replicas on every rank of
+    // `nccl_comm` (an ncclComm_t, e.g. NcclCommunicator::get()) are summed in place
+    // by one NCCL allreduce; every rank ends with the merged table.
+    CountSketch& allreduce(void* nccl_comm);
 
     // MCSK1 wire format (sketch.cpp:195-244), byte-identical to the reference:
     // "MCSK1", u32 b, u32 rows, u64 width, u32 k, u32 splitter, u32 log2(u),
@@ -194,6 +198,26 @@ private:
     void* stream_ = nullptr;  // cudaStream_t owned by the sketch
     struct Staging;
     std::unique_ptr<Staging> staging_;
+};
+
+// One NCCL communicator over the ranks of a job (one GPU per rank), for
+// CountSketch::allreduce.  Rank 0 draws unique_id() and ships its bytes to the
+// other ranks by any side channel; every rank then constructs with them.
+class NcclCommunicator {
+public:
+    using Id = std::array<uint8_t, MB200_NCCL_UNIQUE_ID_BYTES>;
+    static Id unique_id();
+    NcclCommunicator(int nranks, const Id& id, int rank);  // current device; collective
+    NcclCommunicator(const NcclCommunicator&) = delete;
+    NcclCommunicator& operator=(const NcclCommunicator&) = delete;
+    ~NcclCommunicator();
+    void* get() const { return comm_; }
+    int size() const { return nranks_; }
+    int rank() const { return rank_; }
+
+private:
+    void* comm_ = nullptr;
+    int nranks_, rank_;
 };
 
 // Host threads CountSketch::process_batch uses to pack and check its inputs

@@ -18,7 +18,7 @@ import numpy as np
 from ._lib import (  # noqa: F401
     KEY_U32, KEY_U64, LIB_PATH, MAP_EXACT_DIV, MAP_MERSENNE, MAP_POW2, SIGNATURES, SPLIT_MERSENNE_ARB, SPLIT_POW2, SPLIT_TWO_FOR_ONE,
     SPLIT_UNIFORM_ARB, W_I32, W_I64, W_NONE, CudaError, DomainError, InvalidArgument, LogicError,
-    SketchDesc, Unsupported, check, lib,
+    SketchDesc, Unsupported, check, harness, lib,
 )
 
 MASK64 = (1 << 64) - 1
@@ -304,18 +304,83 @@ def cs_point_query(spec: SketchSpec, counters, keys, out=None, stream=None):
     return out
 
 
+# ------------------------------------------------------------------ multi-GPU merge
+def nccl_version() -> int:
+    v = C.c_int()
+    check(lib.mb200_nccl_version(C.byref(v)))
+    return v.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib.mb200_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class NcclComm:
+    """One NCCL communicator over the ranks of a job (one GPU per rank), made by the
+    product library (mb200_nccl_comm_init on the current device).  ``cs_allreduce`` /
+    ``CountSketch.allreduce`` sum the rank-local tables through it."""
+
+    def __init__(self, nranks: int, uid: bytes, rank: int):
+        if len(uid) != 128:
+            raise InvalidArgument("NCCL unique id must be 128 bytes")
+        h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        check(lib.mb200_nccl_comm_init(nranks, buf, rank, C.byref(h)))
+        self._h, self.nranks, self.rank = h, nranks, rank
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "NcclComm":
+        """Rank 0 draws the unique id and torch.distributed (any backend) ships it."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(world, obj[0], rank)
+
+    @property
+    def ptr(self):
+        return self._h
+
+    def size(self) -> int:
+        n = C.c_int()
+        check(lib.mb200_nccl_comm_size(self._h, C.byref(n)))
+        return n.value
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and lib is not None:
+            lib.mb200_nccl_comm_destroy(h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter teardown
+            pass
+
+
+def cs_allreduce(counters, comm: NcclComm, stream=None):
+    """In-place NCCL sum of the rank-local tables (distributed CountSketch::merge,
+    sketch.cpp:182-193); asynchronous on `stream`."""
+    check(lib.mb200_cs_allreduce(_dptr(counters), counters.numel(), comm.ptr, _stream(stream)))
+    return counters
+
+
 # ------------------------------------------------------------------ generators
 def gen_u32_keys(seed: int, start: int, n: int, out=None, stream=None):
     torch = _torch()
     out = torch.empty(n, dtype=torch.int32, device="cuda") if out is None else out
-    check(lib.mb200_gen_u32_keys(seed & MASK64, start, n, _dptr(out), _stream(stream)))
+    check(harness().mb200_gen_u32_keys(seed & MASK64, start, n, _dptr(out), _stream(stream)))
     return out
 
 
 def gen_u64_keys(seed: int, start: int, n: int, out=None, stream=None):
     torch = _torch()
     out = torch.empty(n, dtype=torch.int64, device="cuda") if out is None else out
-    check(lib.mb200_gen_u64_keys(seed & MASK64, start, n, _dptr(out), _stream(stream)))
+    check(harness().mb200_gen_u64_keys(seed & MASK64, start, n, _dptr(out), _stream(stream)))
     return out
 
 
@@ -323,7 +388,7 @@ def gen_below_p61(seed: int, start: int, n: int, out=None, bad=None, stream=None
     torch = _torch()
     out = torch.empty(n, dtype=torch.int64, device="cuda") if out is None else out
     bad = torch.zeros(1, dtype=torch.int64, device="cuda") if bad is None else bad
-    check(lib.mb200_gen_below_p61(seed & MASK64, start, n, _dptr(out), _dptr(bad), _stream(stream)))
+    check(harness().mb200_gen_below_p61(seed & MASK64, start, n, _dptr(out), _dptr(bad), _stream(stream)))
     return out, bad
 
 
@@ -331,7 +396,7 @@ def gen_pm_inputs(seed: int, c: int, start: int, n: int, out=None, bad=None, str
     torch = _torch()
     out = torch.empty((n, 2), dtype=torch.int64, device="cuda") if out is None else out
     bad = torch.zeros(1, dtype=torch.int64, device="cuda") if bad is None else bad
-    check(lib.mb200_gen_pm_inputs(seed & MASK64, c, start, n, _dptr(out), _dptr(bad),
+    check(harness().mb200_gen_pm_inputs(seed & MASK64, c, start, n, _dptr(out), _dptr(bad),
                                   _stream(stream)))
     return out, bad
 
@@ -339,7 +404,7 @@ def gen_pm_inputs(seed: int, c: int, start: int, n: int, out=None, bad=None, str
 def zipf_table(alpha: float = 1.2, T: int = 65536, universe: float = 2.0 ** 32):
     cdf = np.zeros(T, np.uint64)
     c1 = C.c_double()
-    check(lib.mb200_zipf_table(alpha, T, universe, _p(cdf), C.byref(c1)))
+    check(harness().mb200_zipf_table(alpha, T, universe, _p(cdf), C.byref(c1)))
     return cdf, c1.value
 
 
@@ -358,22 +423,22 @@ class ZipfStream:
         torch = _torch()
         keys = torch.empty(n, dtype=torch.int32, device="cuda") if keys is None else keys
         weights = torch.empty(n, dtype=torch.int32, device="cuda") if weights is None else weights
-        check(lib.mb200_gen_zipf_items(self.master, _dptr(self.cdf), self.T, self.c1, self.universe,
+        check(harness().mb200_gen_zipf_items(self.master, _dptr(self.cdf), self.T, self.c1, self.universe,
                                        start, n, _dptr(keys), _dptr(weights), _stream(stream)))
         return keys, weights
 
 
 def probe_imad(blocks: int, threads: int, iters: int, sink, stream=None):
-    check(lib.mb200_probe_imad(blocks, threads, iters, _dptr(sink), _stream(stream)))
+    check(harness().mb200_probe_imad(blocks, threads, iters, _dptr(sink), _stream(stream)))
 
 
 def probe_atomics(mode: int, blocks: int, threads: int, iters: int, buf, span: int, stream=None):
-    check(lib.mb200_probe_atomics(mode, blocks, threads, iters, _dptr(buf), span, _stream(stream)))
+    check(harness().mb200_probe_atomics(mode, blocks, threads, iters, _dptr(buf), span, _stream(stream)))
 
 
 def probe_dsmem(cluster: int, mode: int, blocks: int, threads: int, iters: int, words: int, out,
                 stream=None):
-    check(lib.mb200_probe_dsmem(cluster, mode, blocks, threads, iters, words, _dptr(out), _stream(stream)))
+    check(harness().mb200_probe_dsmem(cluster, mode, blocks, threads, iters, words, _dptr(out), _stream(stream)))
 
 
 def hot_stats(reset: bool = False) -> dict:
@@ -490,6 +555,11 @@ class CountSketch:
 
     def merge(self, other: "CountSketch"):
         check(lib.mb200_sketch_merge(self._h, other._h))
+        return self
+
+    def allreduce(self, comm: "NcclComm"):
+        """merge() across the ranks of `comm`: the replicas' HBM tables are summed in place."""
+        check(lib.mb200_sketch_allreduce(self._h, comm.ptr))
         return self
 
     def counters(self) -> np.ndarray:

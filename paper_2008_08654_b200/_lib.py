@@ -11,6 +11,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmersenne_b200.so")
+HARNESS_PATH = os.path.join(HERE, "libmersenne_b200_harness.so")
 
 MB200_OK = 0
 MB200_INVALID_ARGUMENT = 1
@@ -109,6 +110,20 @@ SIGNATURES = [
     ("mb200_sketch_coeffs", I, [P, P, P]),
     ("mb200_sketch_serialize", I, [P, P, u64, P]),
     ("mb200_sketch_deserialize", I, [P, u64, P]),
+    ("mb200_nccl_version", I, [P]),
+    ("mb200_nccl_unique_id", I, [P]),
+    ("mb200_nccl_comm_init", I, [I, P, I, P]),
+    ("mb200_nccl_comm_destroy", I, [P]),
+    ("mb200_nccl_comm_size", I, [P, P]),
+    ("mb200_cs_allreduce", I, [P, u64, P, P]),
+    ("mb200_sketch_allreduce", I, [P, P]),
+    ("mb200_hot_stats", I, [P, I]),
+    ("mb200_set_large_table_strategy", I, [I, P]),
+]
+
+
+# bench / test harness library (include/mersenne_b200_harness.h): not the drop-in ABI
+HARNESS_SIGNATURES = [
     ("mb200_gen_u32_keys", I, [u64, u64, u64, P, P]),
     ("mb200_gen_u64_keys", I, [u64, u64, u64, P, P]),
     ("mb200_gen_below_p61", I, [u64, u64, u64, P, P, P]),
@@ -118,9 +133,15 @@ SIGNATURES = [
     ("mb200_probe_imad", I, [I, I, I, P, P]),
     ("mb200_probe_atomics", I, [I, I, I, I, P, u64, P]),
     ("mb200_probe_dsmem", I, [I, I, I, I, I, u32, P, P]),
-    ("mb200_hot_stats", I, [P, I]),
-    ("mb200_set_large_table_strategy", I, [I, P]),
 ]
+
+
+def _bind(lib, sigs):
+    for name, res, args in sigs:
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
 
 
 def _load():
@@ -128,15 +149,21 @@ def _load():
         raise ImportError(
             f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
             "or `make lib` (the B200 path has no CPU fallback)")
-    lib = C.CDLL(LIB_PATH)
-    for name, res, args in SIGNATURES:
-        f = getattr(lib, name)
-        f.restype = res
-        f.argtypes = args
-    return lib
+    return _bind(C.CDLL(LIB_PATH), SIGNATURES)
 
 
 lib = _load()
+_harness = None
+
+
+def harness():
+    """The bench harness library (generators, probes), loaded on first use."""
+    global _harness
+    if _harness is None:
+        if not os.path.exists(HARNESS_PATH):
+            raise ImportError(f"{HARNESS_PATH} is not built: run `make lib`")
+        _harness = _bind(C.CDLL(HARNESS_PATH), HARNESS_SIGNATURES)
+    return _harness
 
 
 def check(status: int) -> None:

@@ -5,8 +5,8 @@
 // rank and is bit-identical to the sequential stream.  Streams follow the
 // reference benchmark's convention of salting the seed for keys
 // (bench.cpp:23, kKeyStreamSalt).  DESIGN.md "Inputs" defines each stream.
-#include "mb200_device.cuh"
-#include "mb200_internal.h"
+#include "../csrc/mb200_device.cuh"
+#include "harness_internal.h"
 
 namespace mb200 {
 

@@ -4,9 +4,9 @@
 // atomic throughputs that decide the Count Sketch privatisation strategy.
 #include <cooperative_groups.h>
 
-#include "mb200_device.cuh"
-#include "mb200_internal.h"
-#include "mb200_mem.cuh"
+#include "../csrc/mb200_device.cuh"
+#include "harness_internal.h"
+#include "../csrc/mb200_mem.cuh"
 
 namespace mb200 {
 

@@ -129,6 +129,11 @@ int mb200_sketch_merge(mb200_sketch* dst, const mb200_sketch* src) {
     return guarded([&] { dst->sk.merge(src->sk); });
 }
 
+int mb200_sketch_allreduce(mb200_sketch* s, void* nccl_comm) {
+    if (!s) return mb200::fail(MB200_INVALID_ARGUMENT, "null sketch");
+    return guarded([&] { s->sk.allreduce(nccl_comm); });
+}
+
 int mb200_sketch_counters(mb200_sketch* s, int64_t* h_out) {
     if (!s) return mb200::fail(MB200_INVALID_ARGUMENT, "null sketch");
     return guarded([&] {

@@ -547,6 +547,25 @@ CountSketch& CountSketch::merge(const CountSketch& other) {  // sketch.cpp:182-1
     return *this;
 }
 
+CountSketch& CountSketch::allreduce(void* nccl_comm) {
+    cudaStream_t s = (cudaStream_t)stream_;
+    throw_status(mb200_cs_allreduce(d_counters_, u64(rows_) * width_, nccl_comm, s));
+    synchronize();
+    return *this;
+}
+
+NcclCommunicator::Id NcclCommunicator::unique_id() {
+    Id id{};
+    throw_status(mb200_nccl_unique_id(id.data()));
+    return id;
+}
+
+NcclCommunicator::NcclCommunicator(int nranks, const Id& id, int rank) : nranks_(nranks), rank_(rank) {
+    throw_status(mb200_nccl_comm_init(nranks, id.data(), rank, &comm_));
+}
+
+NcclCommunicator::~NcclCommunicator() { mb200_nccl_comm_destroy(comm_); }
+
 namespace {
 void put_u32(std::vector<uint8_t>& out, uint32_t v) {
     for (int i = 0; i < 4; ++i) out.push_back(uint8_t(v >> (8 * i)));

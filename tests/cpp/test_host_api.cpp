@@ -220,12 +220,34 @@ static void test_sketch() {  // test_sketch.cpp
     }
 }
 
+static void test_allreduce() {  // SURVEY 8b entry 6: CountSketch::allreduce over NCCL
+    MersenneModulus m61(61, true);
+    NcclCommunicator comm(1, NcclCommunicator::unique_id(), 0);  // one GPU: a one-rank job
+    CHECK(comm.size() == 1 && comm.get() != nullptr);
+    CountSketch a(5, 4096, m61, u128(1) << 32, Splitter::Pow2, 7);
+    CountSketch b(5, 4096, m61, u128(1) << 32, Splitter::Pow2, 7);
+    std::vector<uint32_t> keys(1 << 16);
+    std::vector<int32_t> w(keys.size());
+    for (size_t i = 0; i < keys.size(); ++i) {
+        keys[i] = uint32_t(i * 2654435761u);
+        w[i] = int32_t(i % 201) - 100;
+    }
+    a.process_batch(keys.data(), 32, w.data(), MB200_W_I32, keys.size() / 2);
+    b.process_batch(keys.data() + keys.size() / 2, 32, w.data() + keys.size() / 2, MB200_W_I32, keys.size() / 2);
+    a.merge(b);                                  // the single-process merge
+    const std::vector<int64_t> merged = a.counters();
+    a.allreduce(comm.get());                     // one rank: the sum over ranks is the table itself
+    CHECK(a.counters() == merged);
+    CHECK_THROWS_AS(a.allreduce(nullptr), std::invalid_argument);
+}
+
 int main() {
     try {
         test_field();
         test_polyhash();
         test_bucketing();
         test_sketch();
+        test_allreduce();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "unexpected exception: %s\n", e.what());
         return 2;

@@ -31,6 +31,26 @@ def test_library_exports_every_declared_symbol(mb):
     assert sorted(n for n, _, _ in mb.SIGNATURES) == syms
 
 
+def test_harness_library_exports_its_header(mb):
+    """Generators and probes live in a separate harness library, outside the drop-in ABI."""
+    with open(os.path.join(ROOT, "include", "mersenne_b200_harness.h")) as f:
+        syms = sorted(set(re.findall(r"\b(mb200_[a-z0-9_]+)\s*\(", f.read())))
+    h = C.CDLL(mb._lib.HARNESS_PATH)
+    assert all(hasattr(h, s) for s in syms)
+    assert sorted(n for n, _, _ in mb._lib.HARNESS_SIGNATURES) == syms
+    assert not set(syms) & set(header_symbols())
+    prod = C.CDLL(mb.LIB_PATH)
+    assert not any(hasattr(prod, s) for s in syms), "harness entries leaked into the product library"
+
+
+def test_nccl_entries_validate_without_gpu(mb):
+    """The multi-GPU merge entry rejects a null communicator before touching NCCL state."""
+    import numpy as np
+    with pytest.raises(mb.InvalidArgument, match="null communicator"):
+        mb.check(mb.lib.mb200_cs_allreduce(None, 8, None, None))
+    assert len(mb.nccl_unique_id()) == 128  # libnccl.so.2 resolved at run time
+
+
 def test_abi_version(mb):
     assert mb.lib.mb200_abi_version() == 1
 

@@ -674,8 +674,43 @@ def test_count_sketch_injected_families(cuda, mb):
     sk = mb.CountSketch.from_families(4, mb.SPLIT_POW2, 5, 4, [[1, 2, 3, 4]])
     with pytest.raises(mb.LogicError):
         sk.seeds()
-    sk.process(np.array([1, 3, 7], np.uint64), np.array([2, -1, 3], np.int64))
-    assert sk.counters().sum() != 0 or True
+    keys, deltas = np.array([1, 3, 7], np.uint64), np.array([2, -1, 3], np.int64)
+    sk.process(keys, deltas)
+    exp = orc_cs(mb, [[1, 2, 3, 4]], keys, deltas)
+    assert (sk.counters() == exp).all() and exp.any()
+
+
+def orc_cs(mb, fams, keys, deltas):
+    from oracle_bind import oracle
+
+    return oracle().cs_process(1, 4, 5, fams, 4, mb.SPLIT_POW2, keys, deltas)
+
+
+# ---------------------------------------------------------------- multi-GPU merge
+def test_nccl_allreduce_one_rank(cuda, mb, orc):
+    """mb200_cs_allreduce over a one-rank communicator made by the product: the merge
+    of one table is that table (N > 1 is covered by the gloo tests of bench's step
+    logic; one box has one GPU).  Exercises the dlopen'd NCCL, the comm lifecycle
+    and the uint64 in-place reduction on a table holding wrap-around values."""
+    import torch
+
+    comm = mb.NcclComm(1, mb.nccl_unique_id(), 0)
+    assert comm.size() == 1 and mb.nccl_version() >= 21800
+    vals = np.array([0, 1, -1, 2**63 - 1, -(2**63), 12345, -987654321] * 1000, np.int64)
+    t = torch.from_numpy(vals.copy()).cuda()
+    mb.cs_allreduce(t, comm)
+    torch.cuda.synchronize()
+    assert (t.cpu().numpy() == vals).all()
+    # the object path: CountSketch.allreduce leaves the (one-rank) merged table in HBM
+    sk = mb.CountSketch(5, 1 << 10, 61, 32, mb.SPLIT_POW2, 1)
+    keys, w = orc.gen_zipf_items(1, 0, 50_000)
+    sk.process(keys, w)
+    before = sk.counters()
+    sk.allreduce(comm)
+    assert (sk.counters() == before).all()
+    fams = [orc.coeffs(61, 4, s) for s in orc.row_seeds(1, 5)]
+    assert (before == orc.cs_process(5, 1 << 10, 61, fams, 32, 0, keys, w)).all()
+    comm.close()
 
 
 # ---------------------------------------------------------------- generators

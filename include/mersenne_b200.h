@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define MB200_ABI_VERSION 1
+#define MB200_ABI_VERSION 2
 
 #define MB200_OK 0
 #define MB200_INVALID_ARGUMENT 1 /* std::invalid_argument (construction-time checks) */
@@ -60,8 +60,9 @@ int mb200_device_count(void);
 /* MersenneModulus(b, require_prime) validation: field.cpp:197-206 */
 int mb200_mersenne_modulus_check(unsigned b, int require_prime);
 /* PseudoMersenneModulus(b, c, m_iters) ctor: field.cpp:224-244 (default
- * iteration count field.cpp:158-171, domain threshold :176-193).  c < 2^64. */
-int mb200_pm_modulus(unsigned b, uint64_t c, unsigned m_iters, unsigned* iterations,
+ * iteration count field.cpp:156-171, domain threshold :173-193) for any u128
+ * c = (c_hi << 64) | c_lo; max_input receives the 256-bit admissible maximum. */
+int mb200_pm_modulus(unsigned b, uint64_t c_lo, uint64_t c_hi, unsigned m_iters, unsigned* iterations,
                      uint64_t max_input[4]);
 
 /* ------------------------------------------------------------- hashing --- */
@@ -98,6 +99,21 @@ int mb200_hash89(const uint64_t* d_keys, uint64_t n, const uint64_t* coeffs_lo,
  * quotient >= 2^64 (possible only for v >= 2^64 p). */
 int mb200_pm_divmod(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, unsigned m_iters,
                     uint64_t* d_q, uint64_t* d_r, uint64_t* d_overflow, void* stream);
+
+/* pseudo_mersenne_div alone (field.cpp:260-265): quotients only (same rules as
+ * mb200_pm_divmod, which also accepts d_r == NULL) */
+int mb200_pm_div(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, unsigned m_iters,
+                 uint64_t* d_q, uint64_t* d_overflow, void* stream);
+/* pseudo_mersenne_mod alone (field.cpp:267-273): r = (v + z c) & (2^b - 1) for
+ * given quotients z (u64); b <= 64 */
+int mb200_pm_mod(const uint64_t* d_v, const uint64_t* d_z, uint64_t n, unsigned b, uint64_t c,
+                 uint64_t* d_r, void* stream);
+/* mersenne_divmod, Alg 3 (field.cpp:208-222) for p = 2^b - 1, 2 <= b <= 63:
+ * branch-free quotient and remainder of every v < 2^(2b) (u128 (lo, hi) pairs);
+ * any larger input raises domain_error "input exceeds 2^(2b)" before any output
+ * is written (synchronizes `stream`).  b in [64, 127]: MB200_UNSUPPORTED. */
+int mb200_mersenne_divmod(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t* d_q, uint64_t* d_r,
+                          void* stream);
 
 /* ------------------------------------------------------------- bucketing --- */
 /* Bucket maps of bucketing.hpp:31-58 on device u64 arrays (b <= 64):
@@ -137,6 +153,18 @@ int mb200_bucket_map(int kind, const uint64_t* d_v, uint64_t n, unsigned b, uint
 int mb200_enum_moment_sums(unsigned b, uint64_t key_domain, uint64_t buckets, int splitter,
                            const uint64_t* keys, const int64_t* deltas, uint64_t n, uint64_t out[5],
                            void* stream);
+
+/* ------------------------------------------------------------ splitters --- */
+/* The two-for-one bucket/sign split on a batch of u64 hash values (b <= 64):
+ *   MB200_SPLIT_POW2         split_pow2(h, b, l)          sketch.cpp:13-19   (l_or_r = l < b)
+ *   MB200_SPLIT_UNIFORM_ARB  split_arb_uniform(h, b, r)   sketch.cpp:21-29   (1 <= r <= 2^(b-1))
+ *   MB200_SPLIT_MERSENNE_ARB split_arb_mersenne(h, b, r)  sketch.cpp:31-34
+ * d_index: u64 index, d_sign: +1 / -1.  Hash values outside the splitter's domain
+ * (h >= 2^b; h >= 2^b - 1 for the Mersenne splitter; the reference asserts) are
+ * counted into *d_out_of_domain (nullable, accumulated), or, when it is NULL, by a
+ * synchronizing read-back returning MB200_DOMAIN_ERROR. */
+int mb200_split_batch(int splitter, const uint64_t* d_h, uint64_t n, unsigned b, uint64_t l_or_r,
+                      uint64_t* d_index, int32_t* d_sign, uint64_t* d_out_of_domain, void* stream);
 
 /* --------------------------------------------------------- count sketch --- */
 typedef struct {

@@ -38,28 +38,71 @@ private:
     bool prime_;
 };
 
-// field.hpp:38-63 (c < 2^64 on this path)
+// field.hpp:11: arithmetic backend.  On the GPU every engine computes the same
+// values (the kernels are fixed-limb); the choice is validated and kept for parity.
+enum class Engine { Auto, Native, Generic };
+
+// 256-bit little-endian value: the role of the reference's UWide (uwide.hpp) at
+// this API's single-value entries.  The GPU batches take u128 (lo, hi) pairs.
+struct UWide {
+    std::array<u64, 4> limb{};
+    UWide() = default;
+    explicit UWide(u64 v) : limb{v, 0, 0, 0} {}
+    static UWide of_u128(u128 v) {
+        UWide w;
+        w.limb = {u64(v), u64(v >> 64), 0, 0};
+        return w;
+    }
+    u128 low_u128() const { return (u128(limb[1]) << 64) | limb[0]; }
+    bool fits_u128() const { return limb[2] == 0 && limb[3] == 0; }
+    u64 operator[](size_t i) const { return limb[i]; }
+    friend bool operator==(const UWide&, const UWide&) = default;
+};
+
+struct DivMod {  // field.hpp:13-16
+    UWide quotient;
+    UWide remainder;
+};
+
+// field.hpp:38-63: modulus 2^b - c, iteration count and admissible maximum
+// computed on the host for any u128 c (field.cpp:224-244).  The GPU batches
+// divide for b <= 64 (c < 2^(b-1) < 2^64); wider moduli are validated and
+// described here but their division raises runtime_error (MB200_UNSUPPORTED).
 class PseudoMersenneModulus {
 public:
-    PseudoMersenneModulus(unsigned b, u64 c, unsigned m_iters = 0);
+    PseudoMersenneModulus(unsigned b, u128 c, unsigned m_iters = 0, Engine engine = Engine::Auto);
     unsigned b() const { return b_; }
-    u64 c() const { return c_; }
+    u128 c() const { return c_; }
     u128 p() const { return (u128(1) << b_) - c_; }
     unsigned iterations() const { return m_; }
-    const std::array<u64, 4>& max_input() const { return max_input_; }
+    Engine engine() const { return engine_; }
+    const UWide& max_input() const { return max_input_; }
 
     // pseudo_mersenne_div + pseudo_mersenne_mod over device arrays (field.cpp:260-273):
-    // d_v holds n u128 as (lo, hi) pairs; d_q, d_r receive n u64 each.
+    // d_v holds n u128 as (lo, hi) pairs; d_q, d_r receive n u64 each (d_r may be null).
     void divmod_device(const u64* d_v, u64 n, u64* d_q, u64* d_r, void* stream = nullptr) const;
     // host-buffer convenience: copies in, divides, copies out
     void divmod(const u64* h_v, u64 n, u64* h_q, u64* h_r) const;
 
 private:
     unsigned b_;
-    u64 c_;
+    u128 c_;
     unsigned m_;
-    std::array<u64, 4> max_input_;
+    Engine engine_;
+    UWide max_input_;
 };
+
+// field.hpp:76-82 -- the reference's free functions.  Single values launch a
+// one-element GPU batch (API parity); the *_device forms are the batch path.
+DivMod mersenne_divmod(const UWide& v, const MersenneModulus& mod);            // Alg 3, b <= 63
+UWide pseudo_mersenne_div(const UWide& v, const PseudoMersenneModulus& mod);   // Alg 4
+UWide pseudo_mersenne_mod(const UWide& v, const UWide& z, const PseudoMersenneModulus& mod);  // Alg 5
+void mersenne_divmod_device(const u64* d_v, u64 n, const MersenneModulus& mod, u64* d_q, u64* d_r,
+                            void* stream = nullptr);
+void pseudo_mersenne_div_device(const u64* d_v, u64 n, const PseudoMersenneModulus& mod, u64* d_q,
+                                void* stream = nullptr);
+void pseudo_mersenne_mod_device(const u64* d_v, const u64* d_z, u64 n, const PseudoMersenneModulus& mod,
+                                u64* d_r, void* stream = nullptr);
 
 // bucketing.hpp:31-58 -- bucket maps over device u64 arrays (b <= 64)
 // map_pow2: floor(v r / 2^b), v < 2^b;  map_mersenne: floor((v+1) r / 2^b), v < 2^b - 1
@@ -121,8 +164,14 @@ struct SignIndexPair {
     int sign;
     friend bool operator==(const SignIndexPair&, const SignIndexPair&) = default;
 };
-// sketch.cpp:13-19 (host helper, the kernels apply the same rule in registers)
-SignIndexPair split_pow2(u128 h, unsigned b, unsigned l);
+// sketch.hpp:17-30 (host helpers; the kernels apply the same rules in registers)
+SignIndexPair split_pow2(u128 h, unsigned b, unsigned l);            // sketch.cpp:13-19
+SignIndexPair split_arb_uniform(u128 h, unsigned b, u128 r);         // sketch.cpp:21-29
+SignIndexPair split_arb_mersenne(u128 h, unsigned b, u128 r);        // sketch.cpp:31-34
+// the same three rules over a device batch of u64 hash values (b <= 64):
+// l_or_r = l for Pow2, r for the arbitrary-width splitters; d_sign gets +1 / -1
+void split_device(Splitter splitter, const u64* d_h, u64 n, unsigned b, u64 l_or_r, u64* d_index, int32_t* d_sign,
+                  void* stream = nullptr);
 
 // sketch.hpp:40-92 with counters resident in HBM of the current device
 class CountSketch {
@@ -131,8 +180,8 @@ public:
                 u64 seed, unsigned independence = 4);
     // Injected families: one per row (or one per two rows for Splitter::TwoForOne).
     CountSketch(u64 width, Splitter splitter, std::vector<PolyHashFamily> families, unsigned rows = 0);
-    CountSketch(const CountSketch&) = delete;
-    CountSketch& operator=(const CountSketch&) = delete;
+    CountSketch(const CountSketch& other);             // value semantics: own HBM table, copied D2D
+    CountSketch& operator=(const CountSketch& other);
     CountSketch(CountSketch&&) noexcept;
     ~CountSketch();
 
@@ -178,6 +227,9 @@ public:
     const std::vector<u64>& seeds() const { return seeds_; }
     const std::vector<PolyHashFamily>& families() const { return families_; }
     std::vector<i64> counters() const;         // D2H copy (row-major, sketch.hpp:75)
+    i64 counter(unsigned row, u64 index) const;  // sketch.hpp:76 (one D2H read)
+    // sketch.hpp:78-82: geometry, seeds and counters
+    friend bool operator==(const CountSketch& a, const CountSketch& b);
     void set_counters(const std::vector<i64>& c);
     i64* device_counters() { return d_counters_; }
     const i64* device_counters() const { return d_counters_; }

@@ -111,11 +111,12 @@ int ref_mersenne_divmod(unsigned b, uint64_t v_lo, uint64_t v_hi, uint64_t* q_lo
     }
 }
 
-// PseudoMersenneModulus(b, c, m_iters, engine): returns iterations, 0 on invalid_argument
-unsigned ref_pm_setup(unsigned b, uint64_t c, unsigned m_iters, int engine,
+// PseudoMersenneModulus(b, c, m_iters, engine) for u128 c = (c_hi << 64) | c_lo:
+// returns iterations, 0 on invalid_argument
+unsigned ref_pm_setup(unsigned b, uint64_t c_lo, uint64_t c_hi, unsigned m_iters, int engine,
                       uint64_t max_input[4]) {
     try {
-        PseudoMersenneModulus m(b, c, m_iters, Engine(engine));
+        PseudoMersenneModulus m(b, mk(c_lo, c_hi), m_iters, Engine(engine));
         for (int i = 0; i < 4; ++i) max_input[i] = m.max_input().limb[i];
         return m.iterations();
     } catch (const std::invalid_argument&) {
@@ -307,6 +308,41 @@ uint64_t ref_cs_serialize(unsigned rows, uint64_t width, unsigned b, unsigned ke
     auto bytes = sk.serialize();
     if (bytes.size() <= cap) std::memcpy(out, bytes.data(), bytes.size());
     return bytes.size();
+}
+
+// Resume a serialized sketch in the reference (sketch.cpp:213-244): deserialize the
+// MCSK1 bytes, process (keys, w) serially, serialize again.  Returns the new size
+// (bytes written only when cap suffices); 0 when deserialize throws.
+uint64_t ref_cs_resume(const uint8_t* bytes, uint64_t len, const uint64_t* keys, const int64_t* w,
+                       uint64_t n, uint8_t* out, uint64_t cap, uint64_t* f2_lo, uint64_t* f2_hi) {
+    try {
+        CountSketch sk = CountSketch::deserialize(std::vector<uint8_t>(bytes, bytes + len));
+        for (uint64_t i = 0; i < n; ++i) sk.process(keys[i], w ? w[i] : 1);
+        const auto m = sk.second_moment(true);
+        *f2_lo = uint64_t(m.value);
+        *f2_hi = uint64_t(m.value >> 64);
+        auto b = sk.serialize();
+        if (b.size() <= cap) std::memcpy(out, b.data(), b.size());
+        return b.size();
+    } catch (const std::invalid_argument&) {
+        return 0;
+    }
+}
+
+// Config 4's two-for-one table from the reference's own pieces: the
+// 89-bit PolyHashFamily::operator() and split_pow2 applied to the two substrings
+// (row 0: split_pow2(h, 89, 16); row 1: split_pow2((h >> 16) & (2^72 - 1), 72, 16)),
+// unit deltas, wrapping adds like CountSketch::process.  Serial.
+void ref_two_for_one_run(const uint64_t* clo, const uint64_t* chi, unsigned k, const uint64_t* keys, uint64_t n,
+                         int64_t* table) {
+    const PolyHashFamily fam(MersenneModulus(89, true), coeff_vec(clo, chi, k), u128(1) << 64);
+    for (uint64_t i = 0; i < n; ++i) {
+        const u128 h = fam(keys[i]);
+        const auto a = split_pow2(h, 89, 16);
+        const auto b = split_pow2((h >> 16) & ((u128(1) << 72) - 1), 72, 16);
+        table[size_t(a.index)] = int64_t(uint64_t(table[size_t(a.index)]) + uint64_t(int64_t(a.sign)));
+        table[65536 + size_t(b.index)] = int64_t(uint64_t(table[65536 + size_t(b.index)]) + uint64_t(int64_t(b.sign)));
+    }
 }
 
 // The reference's own benchmark loops (bench.cpp:96-189): median of 5 after 3 warm-ups.

@@ -42,7 +42,7 @@ def pm_modulus(b: int, c: int, m_iters: int = 0):
     """PseudoMersenneModulus(b, c, m_iters) -> (iterations, max_input)."""
     m = C.c_uint()
     mx = np.zeros(4, np.uint64)
-    check(lib.mb200_pm_modulus(b, c, m_iters, C.byref(m), _p(mx)))
+    check(lib.mb200_pm_modulus(b, c & MASK64, c >> 64, m_iters, C.byref(m), _p(mx)))
     return m.value, sum(int(v) << (64 * i) for i, v in enumerate(mx))
 
 
@@ -147,6 +147,53 @@ def pm_divmod(v, b: int, c: int, m_iters: int = 0, q=None, r=None, overflow=None
     check(lib.mb200_pm_divmod(_dptr(v), n, b, c, m_iters, _dptr(q), _dptr(r), _dptr(overflow),
                               _stream(stream)))
     return q, r
+
+
+def pm_div(v, b: int, c: int, m_iters: int = 0, q=None, overflow=None, stream=None):
+    """pseudo_mersenne_div (field.cpp:260-265) alone: quotients of (n, 2) u128 inputs."""
+    torch = _torch()
+    n = v.numel() // 2
+    if q is None:
+        q = torch.empty(n, dtype=torch.int64, device=v.device)
+    check(lib.mb200_pm_div(_dptr(v), n, b, c, m_iters, _dptr(q), _dptr(overflow), _stream(stream)))
+    return q
+
+
+def pm_mod(v, z, b: int, c: int, r=None, stream=None):
+    """pseudo_mersenne_mod (field.cpp:267-273): (v + z c) & (2^b - 1) for given quotients z."""
+    torch = _torch()
+    n = v.numel() // 2
+    if r is None:
+        r = torch.empty(n, dtype=torch.int64, device=v.device)
+    check(lib.mb200_pm_mod(_dptr(v), _dptr(z), n, b, c, _dptr(r), _stream(stream)))
+    return r
+
+
+def mersenne_divmod(v, b: int, q=None, r=None, stream=None):
+    """mersenne_divmod, Alg 3 (field.cpp:208-222), over (n, 2) u128 inputs < 2^(2b)."""
+    torch = _torch()
+    n = v.numel() // 2
+    if q is None:
+        q = torch.empty(n, dtype=torch.int64, device=v.device)
+    if r is None:
+        r = torch.empty(n, dtype=torch.int64, device=v.device)
+    check(lib.mb200_mersenne_divmod(_dptr(v), n, b, _dptr(q), _dptr(r), _stream(stream)))
+    return q, r
+
+
+def split_batch(splitter: int, h, b: int, l_or_r: int, index=None, sign=None, out_of_domain=None,
+                stream=None):
+    """split_pow2 / split_arb_uniform / split_arb_mersenne (sketch.cpp:13-34) of a device
+    batch of u64 hash values; returns (index int64, sign int32 of +1/-1)."""
+    torch = _torch()
+    n = h.numel()
+    if index is None:
+        index = torch.empty(n, dtype=torch.int64, device=h.device)
+    if sign is None:
+        sign = torch.empty(n, dtype=torch.int32, device=h.device)
+    check(lib.mb200_split_batch(splitter, _dptr(h), n, b, l_or_r, _dptr(index), _dptr(sign),
+                                _dptr(out_of_domain), _stream(stream)))
+    return index, sign
 
 
 def exact_division_iterations(b: int, c: int, r: int) -> int:

@@ -77,12 +77,16 @@ SIGNATURES = [
     ("mb200_abi_version", I, []),
     ("mb200_device_count", I, []),
     ("mb200_mersenne_modulus_check", I, [U, I]),
-    ("mb200_pm_modulus", I, [U, u64, U, P, P]),
+    ("mb200_pm_modulus", I, [U, u64, u64, U, P, P]),
     ("mb200_draw_coeffs", I, [U, U, u64, P, P]),
     ("mb200_row_seeds", I, [u64, U, P]),
     ("mb200_hash61", I, [P, I, u64, U, P, U, U, P, P]),
     ("mb200_hash89", I, [P, u64, P, P, U, U, P, P, P]),
     ("mb200_pm_divmod", I, [P, u64, U, u64, U, P, P, P, P]),
+    ("mb200_pm_div", I, [P, u64, U, u64, U, P, P, P]),
+    ("mb200_pm_mod", I, [P, P, u64, U, u64, P, P]),
+    ("mb200_mersenne_divmod", I, [P, u64, U, P, P, P]),
+    ("mb200_split_batch", I, [I, P, u64, U, u64, P, P, P, P]),
     ("mb200_exact_division_iterations", I, [U, u64, u64, P]),
     ("mb200_bucket_map", I, [I, P, u64, U, u64, u64, P, P, P]),
     ("mb200_enum_moment_sums", I, [U, u64, u64, I, P, P, u64, P, P]),

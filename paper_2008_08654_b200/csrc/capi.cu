@@ -223,9 +223,9 @@ int mb200_pm_divmod(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, uns
     }
     unsigned m = 0;
     uint64_t max_input[4];
-    if (int rc = mb200_pm_modulus(b, c, m_iters, &m, max_input)) return rc;
+    if (int rc = mb200_pm_modulus(b, c, 0, m_iters, &m, max_input)) return rc;
     if (n == 0) return MB200_OK;
-    if (!d_v || !d_q || !d_r) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    if (!d_v || !d_q) return fail(MB200_INVALID_ARGUMENT, "null buffer");  // d_r null: quotient only
     cudaStream_t s = (cudaStream_t)stream;
     if (max_input[2] == 0 && max_input[3] == 0) {  // domain narrower than u128: check
         unsigned long long bad = 0;
@@ -248,6 +248,86 @@ int mb200_pm_divmod(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, uns
     e = launch_pm_divmod(d_v, n, b, c, m, d_q, d_r, flags, s);
     if (scratch) cudaFreeAsync(scratch, s);
     return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_pm_divmod");
+}
+
+int mb200_pm_div(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, unsigned m_iters, uint64_t* d_q,
+                 uint64_t* d_overflow, void* stream) {
+    if (!d_q && n) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    return mb200_pm_divmod(d_v, n, b, c, m_iters, d_q, nullptr, d_overflow, stream);
+}
+
+int mb200_pm_mod(const uint64_t* d_v, const uint64_t* d_z, uint64_t n, unsigned b, uint64_t c, uint64_t* d_r,
+                 void* stream) {
+    if (b < 2 || b > 64) {
+        if (b >= 2 && b <= 127) return fail(MB200_UNSUPPORTED, "GPU division supports b <= 64");
+        return fail(MB200_INVALID_ARGUMENT, "width must be in [2, 127]");
+    }
+    if (int rc = mb200_pm_modulus(b, c, 0, 1, nullptr, nullptr)) return rc;  // validates (b, c) only
+    if (n == 0) return MB200_OK;
+    if (!d_v || !d_z || !d_r) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaError_t e = launch_pm_mod(d_v, d_z, n, b, c, d_r, (cudaStream_t)stream);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_pm_mod");
+}
+
+int mb200_mersenne_divmod(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t* d_q, uint64_t* d_r,
+                          void* stream) {
+    if (b < 2 || b > 127) return fail(MB200_INVALID_ARGUMENT, "exponent must be in [2, 127]");  // field.cpp:198
+    if (b > 63) return fail(MB200_UNSUPPORTED, "GPU Mersenne divmod supports b <= 63");
+    if (n == 0) return MB200_OK;
+    if (!d_v || !d_q || !d_r) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    // v < 2^(2b), else domain_error (field.cpp:209-210); checked before any output
+    const uint64_t max_lo = b >= 32 ? ~0ull : (1ull << (2 * b)) - 1;
+    const uint64_t max_hi = b >= 32 ? (b == 64 ? ~0ull : (1ull << (2 * b - 64)) - 1) : 0;
+    unsigned long long bad = 0;
+    int rc = count_on_device(
+        [&](unsigned long long* d, cudaStream_t st) { return launch_count_above(d_v, n, max_lo, max_hi, d, st); }, s,
+        &bad);
+    if (rc) return rc;
+    if (bad) return fail(MB200_DOMAIN_ERROR, "input exceeds 2^(2b)");
+    // Alg 3 is Alg 4 + 5 at c = 1, m = 2: z = ((v+1) >> b + v + 1) >> b, y = (v + z) & p
+    unsigned long long* flags = nullptr;
+    cudaError_t e = cudaMallocAsync(&flags, sizeof(*flags), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    e = launch_pm_divmod(d_v, n, b, 1, 2, d_q, d_r, flags, s);
+    cudaFreeAsync(flags, s);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_mersenne_divmod");
+}
+
+int mb200_split_batch(int splitter, const uint64_t* d_h, uint64_t n, unsigned b, uint64_t l_or_r, uint64_t* d_index,
+                      int32_t* d_sign, uint64_t* d_out_of_domain, void* stream) {
+    if (b < 2 || b > 127) return fail(MB200_INVALID_ARGUMENT, "exponent must be in [2, 127]");
+    if (b > 64) return fail(MB200_UNSUPPORTED, "GPU splitters take hash values of b <= 64 bits");
+    SketchParams sp{};
+    sp.b = b;
+    sp.splitter = (uint32_t)splitter;
+    sp.families = sp.rows = 1;
+    if (splitter == MB200_SPLIT_POW2) {  // sketch.cpp:14: l < b
+        if (l_or_r >= b) return fail(MB200_INVALID_ARGUMENT, "split_pow2 needs l < b");
+        sp.lw = (uint32_t)l_or_r;
+        sp.width = 1ull << l_or_r;
+    } else if (splitter == MB200_SPLIT_UNIFORM_ARB || splitter == MB200_SPLIT_MERSENNE_ARB) {
+        if (l_or_r < 1 || l_or_r > (1ull << (b - 1)))  // sketch.cpp:24
+            return fail(MB200_INVALID_ARGUMENT, "bucket count must be in [1, 2^(b-1)]");
+        sp.width = l_or_r;
+    } else {
+        return fail(MB200_INVALID_ARGUMENT, "unknown splitter");
+    }
+    if (n == 0) return MB200_OK;
+    if (!d_h || !d_index || !d_sign) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (d_out_of_domain) {
+        cudaError_t e = launch_split_batch(sp, d_h, n, d_index, d_sign,
+                                           reinterpret_cast<unsigned long long*>(d_out_of_domain), s);
+        return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_split_batch");
+    }
+    unsigned long long bad = 0;
+    int rc = count_on_device(
+        [&](unsigned long long* d, cudaStream_t st) { return launch_split_batch(sp, d_h, n, d_index, d_sign, d, st); },
+        s, &bad);
+    if (rc) return rc;
+    if (bad) return fail(MB200_DOMAIN_ERROR, "hash value outside the splitter's domain");
+    return MB200_OK;
 }
 
 int mb200_bucket_map(int kind, const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, uint64_t r,

@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kThreads) pm_divmod_kernel(const u64* __restri
             divmod_one<B, M>(a[u].x, a[u].y, b, c, m, q0, r0, overflow);
             divmod_one<B, M>(bb[u].x, bb[u].y, b, c, m, q1, r1, overflow);
             st_stream(q2 + i + u * stride, make_ulonglong2(q0, q1));
-            st_stream(r2 + i + u * stride, make_ulonglong2(r0, r1));
+            if (r2) st_stream(r2 + i + u * stride, make_ulonglong2(r0, r1));  // null: quotient only
         }
     }
     for (; i < npairs; i += stride) {
@@ -112,13 +112,13 @@ __global__ void __launch_bounds__(kThreads) pm_divmod_kernel(const u64* __restri
         divmod_one<B, M>(a.x, a.y, b, c, m, q0, r0, overflow);
         divmod_one<B, M>(bb.x, bb.y, b, c, m, q1, r1, overflow);
         st_stream(q2 + i, make_ulonglong2(q0, q1));
-        st_stream(r2 + i, make_ulonglong2(r0, r1));
+        if (r2) st_stream(r2 + i, make_ulonglong2(r0, r1));
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         u64 q0, r0;
         divmod_one<B, M>(v[2 * (n - 1)], v[2 * (n - 1) + 1], b, c, m, q0, r0, overflow);
         q[n - 1] = q0;
-        r[n - 1] = r0;
+        if (r) r[n - 1] = r0;
     }
     if (__any_sync(0xffffffffu, overflow) && (threadIdx.x & 31) == 0) atomicAdd(flags, 1ull);
 }
@@ -129,9 +129,23 @@ __global__ void __launch_bounds__(kThreads) pm_divmod_scalar(const u64* __restri
                                                              unsigned long long* flags) {
     unsigned overflow = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        divmod_one<B, M>(v[2 * i], v[2 * i + 1], b, c, m, q[i], r[i], overflow);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        u64 q0, r0;
+        divmod_one<B, M>(v[2 * i], v[2 * i + 1], b, c, m, q0, r0, overflow);
+        q[i] = q0;
+        if (r) r[i] = r0;
+    }
     if (__any_sync(0xffffffffu, overflow) && (threadIdx.x & 31) == 0) atomicAdd(flags, 1ull);
+}
+
+// Alg 5 alone (pseudo_mersenne_mod, field.cpp:267-273) from a given quotient:
+// r = (v + z c) & (2^b - 1); b <= 64 keeps only the low 64 bits of v + z c.
+__global__ void __launch_bounds__(kThreads) pm_mod_kernel(const u64* __restrict__ v, const u64* __restrict__ z,
+                                                          uint64_t n, u32 b, u64 c, u64* __restrict__ r) {
+    const u64 mask = b == 64 ? ~0ull : ((1ull << b) - 1);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        r[i] = (__ldg(v + 2 * i) + __ldg(z + i) * c) & mask;
 }
 
 __global__ void count_above_kernel(const u64* __restrict__ v, uint64_t n, u64 max_lo, u64 max_hi,
@@ -222,7 +236,7 @@ int grid_for(uint64_t items, int per_sm) {
 cudaError_t launch_pm_divmod(const uint64_t* v, uint64_t n, uint32_t b, uint64_t c, uint32_t iters, uint64_t* q,
                              uint64_t* r, unsigned long long* d_flags, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const bool vec = (((uintptr_t)v | (uintptr_t)q | (uintptr_t)r) & 15) == 0;
+    const bool vec = (((uintptr_t)v | (uintptr_t)q | (uintptr_t)r) & 15) == 0;  // r may be null
     if (!vec) {
         const int g = grid_for(n, 8);
         if (b == 64) pm_divmod_scalar<64, 0><<<g, kThreads, 0, s>>>(v, n, b, c, iters, q, r, d_flags);
@@ -259,6 +273,13 @@ cudaError_t launch_bucket_map(int kind, const uint64_t* v, uint64_t n, uint32_t 
     else if (b == 64 && m == 3) bucket_launch<2, 64, 3>(vec, v, n, b, c, m, r, bound, out, d_flags, s);
     else if (b == 64) bucket_launch<2, 64, 0>(vec, v, n, b, c, m, r, bound, out, d_flags, s);
     else bucket_launch<2, 0, 0>(vec, v, n, b, c, m, r, bound, out, d_flags, s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pm_mod(const uint64_t* v, const uint64_t* z, uint64_t n, uint32_t b, uint64_t c, uint64_t* r,
+                          cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    pm_mod_kernel<<<grid_for(n, 8), kThreads, 0, s>>>(v, z, n, b, c, r);
     return cudaGetLastError();
 }
 

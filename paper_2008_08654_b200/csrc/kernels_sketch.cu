@@ -510,6 +510,37 @@ cudaError_t launch_cs_point_query(const SketchParams& sp, const int64_t* table, 
     return cudaGetLastError();
 }
 
+// ---- batched splitters (sketch.cpp:13-34) ---------------------------------------
+// The rule every sketch kernel applies in registers (split_small), exposed on a
+// batch of u64 hash values: index into d_index, sign (+1 / -1) into d_sign.
+__global__ void split_batch_kernel(const SketchParams sp, const u64* __restrict__ h, uint64_t n,
+                                   u64* __restrict__ index, int32_t* __restrict__ sign,
+                                   unsigned long long* flags) {
+    // domain: h < 2^b (h < 2^b - 1 for the Mersenne splitter, sketch.cpp:32)
+    const u64 top = sp.b == 64 ? ~0ull : ((1ull << sp.b) - 1);
+    const u64 last = sp.splitter == SPLIT_MERSENNE_ARB ? top - 1 : top;
+    unsigned bad = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const u64 x = ld_nc(h + i);
+        bad += x > last;
+        bool neg;
+        index[i] = split_small(sp, x, 0, neg);
+        sign[i] = neg ? -1 : 1;
+    }
+    bad = __reduce_add_sync(0xffffffffu, bad);
+    if (bad && (threadIdx.x & 31) == 0) atomicAdd(flags, (unsigned long long)bad);
+}
+
+cudaError_t launch_split_batch(const SketchParams& sp, const uint64_t* h, uint64_t n, uint64_t* index,
+                               int32_t* sign, unsigned long long* d_flags, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    uint64_t grid = (n + 255) / 256;
+    if (grid > (uint64_t)sm_count() * 8) grid = (uint64_t)sm_count() * 8;
+    split_batch_kernel<<<(unsigned)grid, 256, 0, s>>>(sp, h, n, index, sign, d_flags);
+    return cudaGetLastError();
+}
+
 // ---- delta widening (host API transport) --------------------------------------
 // mb200_sketch_process ships deltas over PCIe in the narrowest of i8 / i16 that
 // holds every delta of a chunk; this sign-extends them back to the API's weight

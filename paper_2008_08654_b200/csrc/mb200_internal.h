@@ -65,12 +65,20 @@ int set_large_table_strategy(int s);  // returns the previous strategy, -1 if in
 cudaError_t launch_cs_moments(const int64_t* table, uint32_t rows, uint64_t width, uint64_t* out,
                               cudaStream_t s);
 cudaError_t launch_cs_merge(int64_t* dst, const int64_t* src, uint64_t count, cudaStream_t s);
+// split_pow2 / split_arb_uniform / split_arb_mersenne (sketch.cpp:13-34) of u64 hash
+// values (sp carries b, splitter and width = 2^l or r); hashes outside the
+// splitter's domain are counted into *d_flags
+cudaError_t launch_split_batch(const SketchParams& sp, const uint64_t* h, uint64_t n, uint64_t* index,
+                               int32_t* sign, unsigned long long* d_flags, cudaStream_t s);
 cudaError_t launch_cs_point_query(const SketchParams& sp, const int64_t* table, const void* keys,
                                   int key_width, uint64_t n, int64_t* out, cudaStream_t s);
 
 // division (kernels_divmod.cu)
 cudaError_t launch_pm_divmod(const uint64_t* v, uint64_t n, uint32_t b, uint64_t c, uint32_t iters,
                              uint64_t* q, uint64_t* r, unsigned long long* d_flags, cudaStream_t s);
+// Alg 5 from given quotients z (u64): r = (v + z c) mod 2^b
+cudaError_t launch_pm_mod(const uint64_t* v, const uint64_t* z, uint64_t n, uint32_t b, uint64_t c, uint64_t* r,
+                          cudaStream_t s);
 cudaError_t launch_count_above(const uint64_t* v, uint64_t n, uint64_t max_lo, uint64_t max_hi,
                                unsigned long long* d_count, cudaStream_t s);
 // bucket maps: kind 0 map_pow2, 1 map_mersenne, 2 exact division (m iterations);

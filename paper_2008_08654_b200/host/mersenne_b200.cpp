@@ -60,18 +60,99 @@ MersenneModulus::MersenneModulus(unsigned b, bool require_prime) : b_(b) {
     if (require_prime && !prime_) throw std::invalid_argument("2^b - 1 is not prime for this exponent");
 }
 
-PseudoMersenneModulus::PseudoMersenneModulus(unsigned b, u64 c, unsigned m_iters) : b_(b), c_(c) {
-    throw_status(mb200_pm_modulus(b, c, m_iters, &m_, max_input_.data()));
+PseudoMersenneModulus::PseudoMersenneModulus(unsigned b, u128 c, unsigned m_iters, Engine engine)
+    : b_(b), c_(c), engine_(engine) {
+    unsigned m = 0;
+    std::array<u64, 4> mx{};
+    throw_status(mb200_pm_modulus(b, u64(c), u64(c >> 64), m_iters, &m, mx.data()));  // field.cpp:225-228, 242-243
+    switch (engine) {  // field.cpp:229-241
+        case Engine::Auto: engine_ = b <= 61 ? Engine::Native : Engine::Generic; break;
+        case Engine::Native:
+            if (b > 61) throw std::invalid_argument("native engine requires b <= 61");
+            break;
+        case Engine::Generic: break;
+    }
+    m_ = m;
+    max_input_.limb = mx;
 }
 
+namespace {
+// the GPU division path covers b <= 64 (then c < 2^63)
+void require_gpu_division(const PseudoMersenneModulus& mod) {
+    if (mod.b() > 64) throw_status(mb200_pm_div(nullptr, 0, mod.b(), 0, 0, nullptr, nullptr, nullptr));
+}
+}  // namespace
+
 void PseudoMersenneModulus::divmod_device(const u64* d_v, u64 n, u64* d_q, u64* d_r, void* stream) const {
+    require_gpu_division(*this);
     DevBuf<u64> ovf(1);
     cuda_check(cudaMemsetAsync(ovf.p, 0, sizeof(u64), (cudaStream_t)stream), "memset");
-    throw_status(mb200_pm_divmod(d_v, n, b_, c_, m_, d_q, d_r, ovf.p, stream));
+    throw_status(mb200_pm_divmod(d_v, n, b_, u64(c_), m_, d_q, d_r, ovf.p, stream));
     u64 o = 0;
     cuda_check(cudaMemcpyAsync(&o, ovf.p, sizeof(u64), cudaMemcpyDeviceToHost, (cudaStream_t)stream), "copy");
     cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "sync");
     if (o) throw std::domain_error("quotient exceeds 64 bits");
+}
+
+void mersenne_divmod_device(const u64* d_v, u64 n, const MersenneModulus& mod, u64* d_q, u64* d_r, void* stream) {
+    throw_status(mb200_mersenne_divmod(d_v, n, mod.b(), d_q, d_r, stream));
+}
+
+void pseudo_mersenne_div_device(const u64* d_v, u64 n, const PseudoMersenneModulus& mod, u64* d_q, void* stream) {
+    mod.divmod_device(d_v, n, d_q, nullptr, stream);
+}
+
+void pseudo_mersenne_mod_device(const u64* d_v, const u64* d_z, u64 n, const PseudoMersenneModulus& mod, u64* d_r,
+                                void* stream) {
+    require_gpu_division(mod);
+    throw_status(mb200_pm_mod(d_v, d_z, n, mod.b(), u64(mod.c()), d_r, stream));
+}
+
+namespace {
+bool wide_greater(const UWide& a, const UWide& b) {
+    for (int i = 3; i >= 0; --i)
+        if (a.limb[i] != b.limb[i]) return a.limb[i] > b.limb[i];
+    return false;
+}
+// one u128 value to the device as a (lo, hi) pair, `outs` u64 results back
+template <typename F>
+std::vector<u64> one_value(const UWide& v, int outs, F&& launch) {
+    DevBuf<u64> d(2 + 2 * size_t(outs));
+    const u64 in[2] = {v.limb[0], v.limb[1]};
+    cuda_check(cudaMemcpy(d.p, in, sizeof in, cudaMemcpyHostToDevice), "H2D");
+    launch(d.p, d.p + 2);
+    std::vector<u64> out(static_cast<size_t>(outs));
+    cuda_check(cudaMemcpy(out.data(), d.p + 2, out.size() * sizeof(u64), cudaMemcpyDeviceToHost), "D2H");
+    return out;
+}
+}  // namespace
+
+DivMod mersenne_divmod(const UWide& v, const MersenneModulus& mod) {  // field.cpp:208-222
+    const unsigned b = mod.b();
+    const bool fits = v.fits_u128() && (2 * b >= 128 || (v.low_u128() >> (2 * b)) == 0);
+    if (!fits) throw std::domain_error("input exceeds 2^(2b)");
+    const auto qr = one_value(v, 2, [&](const u64* dv, u64* out) { mersenne_divmod_device(dv, 1, mod, out, out + 1); });
+    return {UWide(qr[0]), UWide(qr[1])};
+}
+
+UWide pseudo_mersenne_div(const UWide& v, const PseudoMersenneModulus& mod) {  // field.cpp:260-265
+    if (wide_greater(v, mod.max_input())) throw std::domain_error("input exceeds division domain for m iterations");
+    require_gpu_division(mod);
+    if (!v.fits_u128()) throw std::runtime_error("GPU division takes dividends below 2^128");
+    const auto q = one_value(v, 1, [&](const u64* dv, u64* out) { pseudo_mersenne_div_device(dv, 1, mod, out); });
+    return UWide(q[0]);
+}
+
+UWide pseudo_mersenne_mod(const UWide& v, const UWide& z, const PseudoMersenneModulus& mod) {  // field.cpp:267-273
+    require_gpu_division(mod);
+    // (v + z c) mod 2^b with b <= 64 depends on the low words only
+    DevBuf<u64> d(4);
+    const u64 in[3] = {v.limb[0], v.limb[1], z.limb[0]};
+    cuda_check(cudaMemcpy(d.p, in, sizeof in, cudaMemcpyHostToDevice), "H2D");
+    pseudo_mersenne_mod_device(d.p, d.p + 2, 1, mod, d.p + 3);
+    u64 r = 0;
+    cuda_check(cudaMemcpy(&r, d.p + 3, sizeof r, cudaMemcpyDeviceToHost), "D2H");
+    return UWide(r);
 }
 
 void PseudoMersenneModulus::divmod(const u64* h_v, u64 n, u64* h_q, u64* h_r) const {
@@ -95,7 +176,8 @@ void map_mersenne_device(const u64* d_v, u64 n, unsigned b, u64 r, u64* d_out, v
 namespace {
 PseudoMersenneModulus exact_divider(const PseudoMersenneModulus& mod, u64 r) {
     unsigned m = 0;
-    throw_status(mb200_exact_division_iterations(mod.b(), mod.c(), r, &m));
+    if (mod.b() > 64) throw_status(mb200_bucket_map(MB200_MAP_EXACT_DIV, nullptr, 0, mod.b(), 0, r, nullptr, nullptr, nullptr));
+    throw_status(mb200_exact_division_iterations(mod.b(), u64(mod.c()), r, &m));
     return PseudoMersenneModulus(mod.b(), mod.c(), m);
 }
 }  // namespace
@@ -104,7 +186,7 @@ ExactDivisionMap::ExactDivisionMap(const PseudoMersenneModulus& mod, u64 r)
     : divider_(exact_divider(mod, r)), r_(r) {}
 
 void ExactDivisionMap::map_device(const u64* d_v, u64 n, u64* d_out, void* stream) const {
-    throw_status(mb200_bucket_map(MB200_MAP_EXACT_DIV, d_v, n, divider_.b(), divider_.c(), r_, d_out, nullptr,
+    throw_status(mb200_bucket_map(MB200_MAP_EXACT_DIV, d_v, n, divider_.b(), u64(divider_.c()), r_, d_out, nullptr,
                                   stream));
 }
 
@@ -192,6 +274,35 @@ SignIndexPair split_pow2(u128 h, unsigned b, unsigned l) {
     const u128 i = h & ((u128(1) << l) - 1);
     const int a = int(h >> (b - 1));
     return {i, 1 - 2 * a};
+}
+
+namespace {
+// floor(j r / 2^s) for j, r < 2^127 (map_pow2, bucketing.cpp:61-66): the 254-bit
+// product from four 64 x 64 partial products
+u128 mul_shift(u128 j, u128 r, unsigned s) {
+    const u64 j0 = u64(j), j1 = u64(j >> 64), r0 = u64(r), r1 = u64(r >> 64);
+    const u128 p00 = u128(j0) * r0, p01 = u128(j0) * r1, p10 = u128(j1) * r0, p11 = u128(j1) * r1;
+    const u128 mid = (p00 >> 64) + u64(p01) + u64(p10);
+    const u128 lo = (mid << 64) | u64(p00);
+    const u128 hi = p11 + (p01 >> 64) + (p10 >> 64) + (mid >> 64);
+    if (s == 0) return lo;
+    if (s >= 128) return hi >> (s - 128);
+    return (hi << (128 - s)) | (lo >> s);
+}
+}  // namespace
+
+SignIndexPair split_arb_uniform(u128 h, unsigned b, u128 r) {
+    const unsigned s = b - 1;
+    const u128 j = h & ((u128(1) << s) - 1);  // low b-1 bits
+    const int a = int(h >> s);                // top bit: set -> +1
+    return {mul_shift(j, r, s), 2 * a - 1};
+}
+
+SignIndexPair split_arb_mersenne(u128 h, unsigned b, u128 r) { return split_arb_uniform(h + 1, b, r); }
+
+void split_device(Splitter splitter, const u64* d_h, u64 n, unsigned b, u64 l_or_r, u64* d_index, int32_t* d_sign,
+                  void* stream) {
+    throw_status(mb200_split_batch(int(splitter), d_h, n, b, l_or_r, d_index, d_sign, nullptr, stream));
 }
 
 // ----------------------------------------------------------------- sketch --
@@ -311,6 +422,47 @@ CountSketch::CountSketch(CountSketch&& o) noexcept
       stream_(o.stream_), staging_(std::move(o.staging_)) {
     o.d_counters_ = nullptr;
     o.stream_ = nullptr;
+}
+
+CountSketch::CountSketch(const CountSketch& o)
+    : rows_(o.rows_), width_(o.width_), splitter_(o.splitter_), families_(o.families_), seeds_(o.seeds_) {
+    init_device();
+    o.synchronize();
+    cuda_check(cudaMemcpyAsync(d_counters_, o.d_counters_, size_t(rows_) * width_ * sizeof(i64),
+                               cudaMemcpyDeviceToDevice, (cudaStream_t)stream_),
+               "D2D");
+    synchronize();
+}
+
+CountSketch& CountSketch::operator=(const CountSketch& o) {
+    if (this != &o) {
+        CountSketch tmp(o);
+        std::swap(rows_, tmp.rows_);
+        std::swap(width_, tmp.width_);
+        std::swap(splitter_, tmp.splitter_);
+        std::swap(families_, tmp.families_);
+        std::swap(seeds_, tmp.seeds_);
+        std::swap(d_counters_, tmp.d_counters_);
+        std::swap(stream_, tmp.stream_);
+        std::swap(staging_, tmp.staging_);
+    }
+    return *this;
+}
+
+i64 CountSketch::counter(unsigned row, u64 index) const {
+    if (row >= rows_ || index >= width_) throw std::out_of_range("counter index out of range");
+    i64 v = 0;
+    cudaStream_t s = (cudaStream_t)stream_;
+    cuda_check(cudaMemcpyAsync(&v, d_counters_ + size_t(row) * width_ + index, sizeof v, cudaMemcpyDeviceToHost, s),
+               "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    return v;
+}
+
+bool operator==(const CountSketch& a, const CountSketch& b) {  // sketch.hpp:78-82
+    return a.width_ == b.width_ && a.splitter_ == b.splitter_ && a.seeds_ == b.seeds_ && a.rows_ == b.rows_ &&
+           a.modulus().b() == b.modulus().b() && a.key_domain() == b.key_domain() &&
+           a.independence() == b.independence() && a.counters() == b.counters();
 }
 
 CountSketch::~CountSketch() {

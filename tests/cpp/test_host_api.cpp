@@ -52,7 +52,7 @@ static void test_field() {  // test_field.cpp:56-158
     CHECK_THROWS_AS(PseudoMersenneModulus(4, 8), std::invalid_argument);
     CHECK_THROWS_AS(PseudoMersenneModulus(4, 0), std::invalid_argument);
     PseudoMersenneModulus m(4, 3, 2);
-    CHECK(m.p() == 13 && m.iterations() == 2 && m.max_input()[0] == 69);
+    CHECK(m.p() == 13 && m.iterations() == 2 && m.max_input()[0] == 69 && m.max_input() == UWide(69));
     u64 v[4] = {27, 0, 69, 0}, q[2], r[2];
     m.divmod(v, 2, q, r);
     CHECK(q[0] == 2 && r[0] == 1 && q[1] == 5 && r[1] == 4);
@@ -220,6 +220,101 @@ static void test_sketch() {  // test_sketch.cpp
     }
 }
 
+static void test_reference_free_functions() {  // test_field.cpp:104-158, 250-277; test_sketch.cpp:14-52
+    // mersenne_divmod (Alg 3)
+    MersenneModulus m3(3);
+    DivMod d = mersenne_divmod(UWide(30), m3);
+    CHECK(d.quotient == UWide(4) && d.remainder == UWide(2));
+    d = mersenne_divmod(UWide(63), m3);
+    CHECK(d.quotient == UWide(9) && d.remainder == UWide(0));
+    CHECK_THROWS_AS(mersenne_divmod(UWide(64), m3), std::domain_error);
+    bool exact = true;
+    for (u64 v = 0; v < 64; ++v) {
+        const DivMod e = mersenne_divmod(UWide(v), m3);
+        exact &= e.quotient == UWide(v / 7) && e.remainder == UWide(v % 7);
+    }
+    CHECK(exact);
+    // pseudo_mersenne_div / pseudo_mersenne_mod (Alg 4, 5)
+    PseudoMersenneModulus m(4, 3, 2);
+    CHECK(pseudo_mersenne_div(UWide(27), m) == UWide(2));
+    CHECK(pseudo_mersenne_div(UWide(69), m) == UWide(5));
+    CHECK_THROWS_AS(pseudo_mersenne_div(UWide(70), m), std::domain_error);
+    CHECK(pseudo_mersenne_mod(UWide(27), UWide(2), m) == UWide(1));
+    CHECK(pseudo_mersenne_mod(UWide(0), UWide(0), m) == UWide(0));
+    PseudoMersenneModulus m31(3, 1);
+    CHECK(pseudo_mersenne_div(UWide(30), m31) == mersenne_divmod(UWide(30), m3).quotient);
+    CHECK(pseudo_mersenne_mod(UWide(48), UWide(6), m31) == UWide(6));
+    // Engine selection and u128 offsets (field.cpp:224-244)
+    CHECK(PseudoMersenneModulus(89, 1).engine() == Engine::Generic);
+    CHECK(PseudoMersenneModulus(61, 1).engine() == Engine::Native);
+    CHECK(PseudoMersenneModulus(13, 5, 0, Engine::Generic).engine() == Engine::Generic);
+    CHECK_THROWS_AS(PseudoMersenneModulus(89, 1, 0, Engine::Native), std::invalid_argument);
+    const PseudoMersenneModulus wide(127, (u128(1) << 100) + 12345);
+    CHECK(wide.c() == (u128(1) << 100) + 12345 && wide.iterations() >= 3);
+    CHECK_THROWS_AS(pseudo_mersenne_div(UWide(5), wide), std::runtime_error);  // GPU division: b <= 64
+    CHECK_THROWS_AS(PseudoMersenneModulus(100, u128(1) << 99), std::invalid_argument);
+    // splitters
+    CHECK(split_pow2(0b110, 3, 2) == (SignIndexPair{2, -1}));
+    CHECK(split_arb_uniform(0b1011, 4, 3) == (SignIndexPair{1, +1}));
+    CHECK(split_arb_uniform(0, 4, 3) == (SignIndexPair{0, -1}));
+    CHECK(split_arb_mersenne(3, 3, 3) == (SignIndexPair{0, +1}));
+    CHECK(split_arb_mersenne(6, 3, 3) == (SignIndexPair{2, +1}));
+    int zero_hits = 0;
+    for (u128 h = 0; h < 7; ++h) zero_hits += split_arb_mersenne(h, 3, 3).index == 0;
+    CHECK(zero_hits == 3);
+    // the batched device splitter against the host rule
+    std::vector<u64> hs(4096);
+    for (size_t i = 0; i < hs.size(); ++i) hs[i] = (i * 0x9E3779B97F4A7C15ull) >> 3;  // < 2^61
+    u64* dh = nullptr;
+    u64* di = nullptr;
+    int32_t* ds = nullptr;
+    cudaMalloc(&dh, hs.size() * 8);
+    cudaMalloc(&di, hs.size() * 8);
+    cudaMalloc(&ds, hs.size() * 4);
+    cudaMemcpy(dh, hs.data(), hs.size() * 8, cudaMemcpyHostToDevice);
+    bool same = true;
+    for (Splitter sp : {Splitter::Pow2, Splitter::UniformArb, Splitter::MersenneArb}) {
+        const u64 lr = sp == Splitter::Pow2 ? 16 : 1000003;
+        split_device(sp, dh, hs.size(), 61, lr, di, ds);
+        std::vector<u64> idx(hs.size());
+        std::vector<int32_t> sg(hs.size());
+        cudaMemcpy(idx.data(), di, idx.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(sg.data(), ds, sg.size() * 4, cudaMemcpyDeviceToHost);
+        for (size_t i = 0; i < hs.size(); ++i) {
+            const SignIndexPair e = sp == Splitter::Pow2       ? split_pow2(hs[i], 61, 16)
+                                    : sp == Splitter::UniformArb ? split_arb_uniform(hs[i], 61, lr)
+                                                                 : split_arb_mersenne(hs[i], 61, lr);
+            same &= e.index == idx[i] && e.sign == sg[i];
+        }
+    }
+    CHECK(same);
+    cudaFree(dh);
+    cudaFree(di);
+    cudaFree(ds);
+}
+
+static void test_sketch_value_semantics() {  // sketch.hpp:72-82: counter(), operator==, copies
+    MersenneModulus m61(61, true);
+    CountSketch a(3, 8, m61, u128(1) << 32, Splitter::Pow2, 0xCAFE);
+    a.process(99, 2);
+    a.process(99, 2);
+    CountSketch once(3, 8, m61, u128(1) << 32, Splitter::Pow2, 0xCAFE);
+    once.process(99, 4);
+    CHECK(a == once);  // test_sketch.cpp:56-72
+    CountSketch copy(a);
+    CHECK(copy == a);
+    copy.process(7, 1);
+    CHECK(!(copy == a));  // independent HBM tables
+    const std::vector<int64_t> c = a.counters();
+    bool cells = true;
+    for (unsigned r = 0; r < 3; ++r)
+        for (u64 i = 0; i < 8; ++i) cells &= a.counter(r, i) == c[r * 8 + i];
+    CHECK(cells);
+    CountSketch other(3, 8, m61, u128(1) << 32, Splitter::Pow2, 0xBEEF);
+    other = a;
+    CHECK(other == a && other.seeds() == a.seeds());
+}
+
 static void test_allreduce() {  // SURVEY 8b entry 6: CountSketch::allreduce over NCCL
     MersenneModulus m61(61, true);
     NcclCommunicator comm(1, NcclCommunicator::unique_id(), 0);  // one GPU: a one-rank job
@@ -247,6 +342,8 @@ int main() {
         test_polyhash();
         test_bucketing();
         test_sketch();
+        test_reference_free_functions();
+        test_sketch_value_semantics();
         test_allreduce();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "unexpected exception: %s\n", e.what());

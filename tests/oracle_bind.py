@@ -305,7 +305,9 @@ class Ref:
         _sig(lib, "ref_hash_batch", u64, [U, P, P, U, U, I, P, u64, P, P, I])
         _sig(lib, "ref_hash_full_batch", None, [U, P, U, P, u64, P, I])
         _sig(lib, "ref_mersenne_divmod", I, [U, u64, u64, P, P, P, P])
-        _sig(lib, "ref_pm_setup", U, [U, u64, U, I, P])
+        _sig(lib, "ref_cs_resume", u64, [P, u64, P, P, u64, P, u64, P, P])
+        _sig(lib, "ref_two_for_one_run", None, [P, P, U, P, u64, P])
+        _sig(lib, "ref_pm_setup", U, [U, u64, u64, U, I, P])
         _sig(lib, "ref_pm_divmod_batch", u64, [U, u64, U, P, u64, P, P, I])
         _sig(lib, "ref_pm_divmod", I, [U, u64, U, u64, u64, P, P, P, P])
         _sig(lib, "ref_cch_divmod", None, [U, u64, u64, u64, P, P, P, P])
@@ -359,7 +361,7 @@ class Ref:
 
     def pm_setup(self, b, c, m_iters=0, engine=0):
         mx = np.zeros(4, np.uint64)
-        m = self.lib.ref_pm_setup(b, c, m_iters, engine, ptr(mx))
+        m = self.lib.ref_pm_setup(b, c & (2**64 - 1), c >> 64, m_iters, engine, ptr(mx))
         if m == 0:
             raise ValueError("invalid pseudo-Mersenne modulus")
         return m, sum(int(v) << (64 * i) for i, v in enumerate(mx))
@@ -456,6 +458,28 @@ class Ref:
         n = self.lib.ref_cs_serialize(rows, width, b, key_bits, splitter, seed, ptr(keys), ptr(w),
                                       len(keys), ptr(out), cap)
         return bytes(out[:n])
+
+    def resume(self, payload, keys=None, weights=None):
+        """CountSketch::deserialize(payload), process(keys, weights), serialize -> (bytes, median F2)."""
+        buf = np.frombuffer(payload, np.uint8).copy()
+        keys = np.zeros(0, np.uint64) if keys is None else np.ascontiguousarray(keys, np.uint64)
+        w = None if weights is None else np.ascontiguousarray(weights, np.int64)
+        out = np.zeros(len(buf) + 64, np.uint8)
+        lo, hi = u64(), u64()
+        n = self.lib.ref_cs_resume(ptr(buf), len(buf), ptr(keys), ptr(w), len(keys), ptr(out), len(out),
+                                   C.byref(lo), C.byref(hi))
+        if n == 0:
+            raise ValueError("malformed sketch payload")
+        return bytes(out[:n]), lo.value | (hi.value << 64)
+
+    def two_for_one(self, coeffs89, keys):
+        """Config 4's 2 x 65536 table from the reference's hash + split_pow2."""
+        lo = np.array([c & (2**64 - 1) for c in coeffs89], np.uint64)
+        hi = np.array([c >> 64 for c in coeffs89], np.uint64)
+        keys = np.ascontiguousarray(keys, np.uint64)
+        table = np.zeros(2 * 65536, np.int64)
+        self.lib.ref_two_for_one_run(ptr(lo), ptr(hi), len(coeffs89), ptr(keys), len(keys), ptr(table))
+        return table
 
     def bench_hash(self, b, k, n, seed):
         cs = u64()

@@ -52,7 +52,7 @@ def test_nccl_entries_validate_without_gpu(mb):
 
 
 def test_abi_version(mb):
-    assert mb.lib.mb200_abi_version() == 1
+    assert mb.lib.mb200_abi_version() == 2
 
 
 def test_host_coefficients_match_oracle(mb, orc, golden):
@@ -75,6 +75,33 @@ def test_host_pm_modulus_matches_oracle(mb, orc):
         n = int(rng.integers(0, 6))
         assert mb.pm_modulus(b, c, n) == orc.pm_setup(b, c, n)[:2]
     assert mb.pm_modulus(64, 59) == orc.pm_setup(64, 59)[:2]
+
+
+def _threshold_bigint(b, c, n):
+    """field.cpp:173-193 in Python integers (an independent third statement)."""
+    q = 1 << b
+    d = c ** n if c & (c - 1) == 0 else c * q ** (n - 1)
+    return min((q ** n - d) // c ** (n - 1), (1 << 255) - (1 << 127))
+
+
+def test_host_pm_modulus_matches_reference_wide_c(mb, ref):
+    """PseudoMersenneModulus(b, c, m) setup for u128 c (field.hpp:45) against the compiled
+    reference over 200 random (b, c, m) -- including the default iteration count, which
+    reaches ~2b rounds (~32k-bit intermediates) when c is close to 2^(b-1)."""
+    rng = np.random.default_rng(0x5EED)
+    cases = [(127, (1 << 126) - 1, 0), (127, 1, 0), (89, 1 << 70, 0), (127, (1 << 126) - 3, 0), (65, 2**64 - 1, 0),
+             (2, 1, 0), (3, 3, 0), (128 - 1, 3, 7)]
+    for _ in range(200):
+        b = int(rng.integers(2, 128))
+        c = int.from_bytes(rng.bytes(16), "little") % ((1 << (b - 1)) - 1) + 1
+        if rng.random() < 0.3:
+            c = max(1, (1 << (b - 1)) - 1 - int(rng.integers(0, 1000)))
+        n = int(rng.integers(0, 8)) if rng.random() < 0.5 else 0
+        cases.append((b, c, n))
+    for b, c, n in cases:
+        got = mb.pm_modulus(b, c, n)
+        assert got == ref.pm_setup(b, c, n), (b, c, n)
+        assert got[1] == _threshold_bigint(b, c, got[0]), (b, c, n)
 
 
 def test_host_exact_division_iterations(mb, orc, ref):

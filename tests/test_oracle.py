@@ -398,3 +398,38 @@ def test_enum_moment_mean_is_exact(orc, b, r, splitter):
     f2 = sum(d * d for _, d in stream)
     assert Fraction(sx, p ** 4) == Fraction(f2 * p * p + f1 * f1 - f2, p * p)
     assert sxx >= sx * sx // p ** 4
+
+
+def _digest(a):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_oracle_matches_reference_large_goldens(orc, golden):
+    """The restated oracle reproduces the reference-executed >= 2^22-unit digests
+    (tests/golden/make_golden.py large_prefixes), so the GPU's large-batch kernels and
+    the oracle are pinned to the same reference outputs."""
+    L = golden["large"]
+    S, SK = golden["seed"], golden["key_seed"]
+    fams5 = [orc.coeffs(61, 4, s) for s in orc.row_seeds(S, 5)]
+    for name in ("c5_head", "c5_window"):
+        g = L[name]
+        zk, zw = orc.gen_zipf_items(S, g["start"], g["n"])
+        t = orc.cs_process(5, 65536, 61, fams5, 32, 0, zk, zw)
+        assert _digest(t) == g["sha256"]
+        assert [str(orc.row_moment(t[r * 65536:(r + 1) * 65536], 65536)[0]) for r in range(5)] == g["row_f2"]
+        assert str(orc.second_moment(t, 5, 65536, True)[0]) == g["median_f2"]
+    g = L["c4_head"]
+    t = orc.cs_process(2, 65536, 89, [orc.coeffs(89, 4, S)], 64, 3, orc.gen_u64_keys(SK, 0, g["n"]))
+    assert _digest(t) == g["sha256"]
+    g = L["c1_full"]
+    t = orc.cs_process(1, 1024, 61, [orc.coeffs(61, 4, s) for s in orc.row_seeds(S, 1)], 32, 0,
+                       orc.gen_u32_keys(SK, 0, g["n"]))
+    assert _digest(t) == g["sha256"] and str(orc.row_moment(t, 1024)[0]) == g["f2"]
+    kp = orc.gen_below_p61(SK, 0, L["c2_k4_head"]["n"])
+    for k in (4, 8):
+        assert _digest(orc.hash_full(61, orc.coeffs(61, k, S), kp)) == L[f"c2_k{k}_head"]["sha256"]
+    v = orc.gen_pm_inputs(SK, 59, 0, L["c3_head"]["n"])
+    q, r, _ = orc.pm_divmod_batch(64, 59, v)
+    assert _digest(q) == L["c3_head"]["q_sha256"] and _digest(r) == L["c3_head"]["r_sha256"]

@@ -203,36 +203,114 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ---------------------------------------------------------------- reference arm
-def cpu_reference_c5(sample_items, reps=3, threads=None):
-    """The reference's own CPU path (oracle/_ref = unmodified reference sources):
-    CountSketch(5, 65536, m61, 2^32, Pow2, S)::process over a bounded sample,
-    sharded over host threads + merge() (bit-identical to one serial pass)."""
+# ---------------------------------------------------------------- reference arm / CPU baselines
+def cpu_info():
+    """Host CPU of this run (nproc + lscpu model + threads per core)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "Model name":
+                info["model"] = v
+            elif k == "Thread(s) per core":
+                info["threads_per_core"] = int(v)
+            elif k == "Core(s) per socket":
+                info["cores_per_socket"] = int(v)
+            elif k == "Socket(s)":
+                info["sockets"] = int(v)
+    except Exception:  # noqa: BLE001
+        pass
+    try:
+        info["affinity"] = len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        pass
+    return info
+
+
+def _median_rate(fn, units, reps):
+    """Units per second: median of `reps` timed calls after one warm-up."""
+    fn()
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+    return units / statistics.median(times), statistics.median(times)
+
+
+def cpu_baselines(threads=None, reps=3):
+    """The reference's own CPU path (oracle/_ref = the unmodified reference sources
+    compiled by oracle/Makefile; the oracle port if it is absent) on every config,
+    single-thread and all-core, on bounded samples of each config's own inputs,
+    plus the reference's own benchmark loops (cli::bench_hash / bench_div,
+    bench.cpp:96-189: 3 warm-ups + median of 5).  Reported baselines, not targets."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_bind import oracle, reference
 
-    ref = reference()
-    kind = "reference"
-    if ref is None:
-        ref, kind = None, "port"
-    orc = oracle()
-    keys, w = orc.gen_zipf_items(S, 0, sample_items)
-    threads = threads or (os.cpu_count() or 1)
-    times = []
-    for rep in range(reps + 1):
-        t0 = time.perf_counter()
-        if ref is not None:
-            ref.cs_run(C5_ROWS, C5_WIDTH, 61, 32, 0, S, keys, w, threads=threads)
-        else:
-            fams = [orc.coeffs(61, 4, s) for s in orc.row_seeds(S, C5_ROWS)]
-            orc.cs_process(C5_ROWS, C5_WIDTH, 61, fams, 32, 0, keys, w)
-        dt = time.perf_counter() - t0
-        if rep:
-            times.append(dt)
-    med = statistics.median(times)
-    return {"value": sample_items / med, "unit": "updates/s", "cores": threads, "kind": kind,
-            "sample": f"config 5 prefix of {sample_items} Zipf items (5 rows x 65536), median of {reps} "
-                      f"after 1 warm-up, {threads} threads, shard + merge()"}
+    ref, orc = reference(), oracle()
+    kind = "reference" if ref is not None else "port"
+    allc = threads or (os.cpu_count() or 1)
+    SK = S ^ 0x7B5BAD595E238E31
+    out = {"_cpu": cpu_info()}
+
+    def lines(name, unit, sample, run1, runN, n1, nN, note):
+        ent = {"unit": unit, "kind": kind, "note": note}
+        for tag, fn, n, cores in (("single_thread", run1, n1, 1), ("all_core", runN, nN, allc)):
+            v, sec = _median_rate(fn, n, reps)
+            ent[tag] = {"value": v, "cores": cores, "sample": f"{n} {sample}", "median_s": sec}
+        ent["value"], ent["cores"] = ent["all_core"]["value"], allc
+        ent["sample"] = ent["all_core"]["sample"] + f"; median of {reps} after 1 warm-up"
+        out[name] = ent
+
+    fams5 = [orc.coeffs(61, 4, s) for s in orc.row_seeds(S, 5)]
+    if ref is not None:
+        # config 1: CountSketch(1, 1024)::process over u32 keys (shard + merge() on all cores)
+        k1 = orc.gen_u32_keys(SK, 0, 1 << 23)
+        lines("c1", "updates/s", "config-1 keys", lambda: ref.cs_run(1, 1024, 61, 32, 0, S, k1[:1 << 21]),
+              lambda: ref.cs_run(1, 1024, 61, 32, 0, S, k1, threads=allc), 1 << 21, 1 << 23,
+              "CountSketch::process (sketch.cpp:133-140)")
+        # config 2: keys in [0, p) lie outside the reference API's domain (SURVEY 8a a3): Horner with the
+        # reference's own Alg 3 per step (the route make_golden.py pins)
+        kp = orc.gen_below_p61(SK, 0, 1 << 23)
+        for k in (4, 8):
+            ck = ref.coeffs(61, k, S)
+            lines(f"c2_k{k}", "hashes/s", "config-2 keys", lambda ck=ck: ref.hash_full(61, ck, kp[:1 << 21]),
+                  lambda ck=ck: ref.hash_full(61, ck, kp, threads=allc), 1 << 21, 1 << 23,
+                  "Horner on the reference's mersenne_divmod (field.cpp:208-222)")
+            ops, _ = ref.bench_hash(61, k, 10_000_000, S)
+            out[f"c2_k{k}"]["reference_bench_hash"] = {
+                "value": ops, "unit": "hashes/s", "cores": 1,
+                "sample": "cli::bench_hash(61, k, 1e7): PolyHashFamily::operator() on 32-bit keys incl. key "
+                          "generation, median of 5 after 3 warm-ups (bench.cpp:96-144)"}
+        # config 3: pseudo_mersenne_div + pseudo_mersenne_mod by 2^64 - 59
+        v3 = orc.gen_pm_inputs(SK, 59, 0, 1 << 22)
+        lines("c3", "divmod/s", "config-3 inputs", lambda: ref.pm_divmod_batch(64, 59, v3[:2 << 20]),
+              lambda: ref.pm_divmod_batch(64, 59, v3, threads=allc), 1 << 20, 1 << 22,
+              "pseudo_mersenne_div + pseudo_mersenne_mod (field.cpp:260-273), Generic engine")
+        bops, casc, _ = ref.bench_div(64, 59, 2_000_000, S)
+        out["c3"]["reference_bench_div"] = {
+            "value": bops, "cascade_value": casc, "unit": "divmod/s", "cores": 1,
+            "sample": "cli::bench_div(64, 59, 2e6): branch-free Alg 4+5 and the cch_divmod cascade, "
+                      "median of 5 after 3 warm-ups (bench.cpp:146-189)"}
+        # config 4: 89-bit hash -> two-for-one split -> two rows (reference hash + split_pow2)
+        c89 = ref.coeffs(89, 4, S, key_bits=64)
+        k4 = orc.gen_u64_keys(SK, 0, 1 << 23)
+        lines("c4", "keys/s", "config-4 keys", lambda: ref.two_for_one(c89, k4[:1 << 21]),
+              lambda: ref.two_for_one(c89, k4, threads=allc), 1 << 21, 1 << 23,
+              "PolyHashFamily(m89)::operator() + split_pow2 twice (SURVEY 7.4)")
+        # config 5: CountSketch(5, 65536)::process over the Zipf stream
+        zk, zw = orc.gen_zipf_items(S, 0, 1 << 23)
+        lines("c5", "updates/s", "config-5 Zipf items", lambda: ref.cs_run(5, 65536, 61, 32, 0, S, zk[:1 << 21], zw[:1 << 21]),
+              lambda: ref.cs_run(5, 65536, 61, 32, 0, S, zk, zw, threads=allc), 1 << 21, 1 << 23,
+              "CountSketch::process (sketch.cpp:133-140), all-core = contiguous shards + merge()")
+    else:  # oracle port (oracle.c, OpenMP): config 5 only
+        zk, zw = orc.gen_zipf_items(S, 0, 1 << 22)
+        lines("c5", "updates/s", "config-5 Zipf items",
+              lambda: orc.cs_process(5, 65536, 61, fams5, 32, 0, zk[:1 << 20], zw[:1 << 20]),
+              lambda: orc.cs_process(5, 65536, 61, fams5, 32, 0, zk, zw), 1 << 20, 1 << 22, "oracle port")
+    return out
 
 
 def run_reference_arm(args):
@@ -272,7 +350,7 @@ def run_reference_arm(args):
                    "rows": C5_ROWS, "width": C5_WIDTH, "prime": "2^61-1", "k": 4},
         "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": kind,
                          "sample": f"{per_step} items of the config-5 stream per step, CountSketch::process "
-                                   f"sharded over {cores} threads + merge()"},
+                                   f"sharded over {cores} threads + merge()", "cpu": cpu_info()},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -514,7 +592,13 @@ def main():
         line["configs"] = bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ranks, merge)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_reference_c5(1 << 23)
+        cb = cpu_baselines()
+        cpu = cb.pop("_cpu")
+        head = cb.pop("c5")
+        line["cpu_baseline"] = {**head, "cpu": cpu}
+        for name, ent in cb.items():
+            if name in line.get("configs", {}):
+                line["configs"][name]["cpu_baseline"] = ent
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -334,15 +334,27 @@ uint64_t ref_cs_resume(const uint8_t* bytes, uint64_t len, const uint64_t* keys,
 // (row 0: split_pow2(h, 89, 16); row 1: split_pow2((h >> 16) & (2^72 - 1), 72, 16)),
 // unit deltas, wrapping adds like CountSketch::process.  Serial.
 void ref_two_for_one_run(const uint64_t* clo, const uint64_t* chi, unsigned k, const uint64_t* keys, uint64_t n,
-                         int64_t* table) {
+                         int64_t* table, int threads) {
     const PolyHashFamily fam(MersenneModulus(89, true), coeff_vec(clo, chi, k), u128(1) << 64);
-    for (uint64_t i = 0; i < n; ++i) {
-        const u128 h = fam(keys[i]);
-        const auto a = split_pow2(h, 89, 16);
-        const auto b = split_pow2((h >> 16) & ((u128(1) << 72) - 1), 72, 16);
-        table[size_t(a.index)] = int64_t(uint64_t(table[size_t(a.index)]) + uint64_t(int64_t(a.sign)));
-        table[65536 + size_t(b.index)] = int64_t(uint64_t(table[65536 + size_t(b.index)]) + uint64_t(int64_t(b.sign)));
+    // contiguous shards over host threads, per-thread tables summed after (the
+    // table is linear, like CountSketch::merge); threads = 1 is one serial pass
+    const int t = threads > 0 ? threads : 1;
+    std::vector<std::vector<uint64_t>> part(size_t(t), std::vector<uint64_t>(2 * 65536, 0));
+#pragma omp parallel num_threads(t)
+    {
+        const int id = omp_get_thread_num();
+        std::vector<uint64_t>& tab = part[size_t(id)];
+        const uint64_t lo = n * uint64_t(id) / uint64_t(t), hi = n * uint64_t(id + 1) / uint64_t(t);
+        for (uint64_t i = lo; i < hi; ++i) {
+            const u128 h = fam(keys[i]);
+            const auto a = split_pow2(h, 89, 16);
+            const auto b = split_pow2((h >> 16) & ((u128(1) << 72) - 1), 72, 16);
+            tab[size_t(a.index)] += uint64_t(int64_t(a.sign));
+            tab[65536 + size_t(b.index)] += uint64_t(int64_t(b.sign));
+        }
     }
+    for (const auto& tab : part)
+        for (size_t j = 0; j < tab.size(); ++j) table[j] = int64_t(uint64_t(table[j]) + tab[j]);
 }
 
 // The reference's own benchmark loops (bench.cpp:96-189): median of 5 after 3 warm-ups.

@@ -306,7 +306,7 @@ class Ref:
         _sig(lib, "ref_hash_full_batch", None, [U, P, U, P, u64, P, I])
         _sig(lib, "ref_mersenne_divmod", I, [U, u64, u64, P, P, P, P])
         _sig(lib, "ref_cs_resume", u64, [P, u64, P, P, u64, P, u64, P, P])
-        _sig(lib, "ref_two_for_one_run", None, [P, P, U, P, u64, P])
+        _sig(lib, "ref_two_for_one_run", None, [P, P, U, P, u64, P, I])
         _sig(lib, "ref_pm_setup", U, [U, u64, u64, U, I, P])
         _sig(lib, "ref_pm_divmod_batch", u64, [U, u64, U, P, u64, P, P, I])
         _sig(lib, "ref_pm_divmod", I, [U, u64, U, u64, u64, P, P, P, P])
@@ -472,13 +472,13 @@ class Ref:
             raise ValueError("malformed sketch payload")
         return bytes(out[:n]), lo.value | (hi.value << 64)
 
-    def two_for_one(self, coeffs89, keys):
+    def two_for_one(self, coeffs89, keys, threads=1):
         """Config 4's 2 x 65536 table from the reference's hash + split_pow2."""
         lo = np.array([c & (2**64 - 1) for c in coeffs89], np.uint64)
         hi = np.array([c >> 64 for c in coeffs89], np.uint64)
         keys = np.ascontiguousarray(keys, np.uint64)
         table = np.zeros(2 * 65536, np.int64)
-        self.lib.ref_two_for_one_run(ptr(lo), ptr(hi), len(coeffs89), ptr(keys), len(keys), ptr(table))
+        self.lib.ref_two_for_one_run(ptr(lo), ptr(hi), len(coeffs89), ptr(keys), len(keys), ptr(table), threads)
         return table
 
     def bench_hash(self, b, k, n, seed):

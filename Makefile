@@ -4,6 +4,7 @@
 #                      reference sources are present)
 #   make lib        -> the product library (+ the bench harness library)
 #   make cpptest    -> tests/cpp/test_host_api (C++ host-API tests, run by pytest -m gpu)
+#   make cli        -> paper_2008_08654_b200/mersenne_b200_cli (the reference CLI's `sketch` ingest)
 PKG      := paper_2008_08654_b200
 CUDA     ?= /usr/local/cuda
 NVCC     ?= $(CUDA)/bin/nvcc
@@ -22,8 +23,9 @@ H_OBJS   := $(patsubst $(PKG)/harness/%.cu,$(BUILD)/harness_%.cu.o,$(H_SRCS))
 LIB      := $(PKG)/libmersenne_b200.so
 HLIB     := $(PKG)/libmersenne_b200_harness.so
 
-.PHONY: all lib oracle cpptest clean
-all: lib oracle
+.PHONY: all lib oracle cpptest cli clean
+CLI      := $(PKG)/mersenne_b200_cli
+all: lib oracle cli
 
 lib: $(LIB) $(HLIB)
 
@@ -54,6 +56,11 @@ cpptest: $(LIB) tests/cpp/test_host_api.cpp oracle
 	    -L$(PKG) -lmersenne_b200 -Loracle -loracle -L$(CUDA)/lib64 -lcudart \
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle'
 
+cli: $(CLI)
+
+$(CLI): $(PKG)/cli/mersenne_cli.cpp $(LIB) include/mersenne_b200/mersenne_b200.hpp include/mersenne_b200.h
+	g++ $(CXXFLAGS) -o $@ $< -L$(PKG) -lmersenne_b200 -Wl,-rpath,'$$ORIGIN'
+
 clean:
-	rm -rf $(BUILD) $(LIB) $(HLIB) tests/cpp/test_host_api
+	rm -rf $(BUILD) $(LIB) $(HLIB) $(CLI) tests/cpp/test_host_api
 	$(MAKE) -C oracle clean

@@ -259,7 +259,7 @@ def test_cli_input_file_equals_stdin(cli, tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("splitter,rows,key_bits", [("pow2", 5, 32), ("uniform", 3, 64), ("mersenne", 2, 20)])
+@pytest.mark.parametrize("splitter,rows,key_bits", [("pow2", 5, 32), ("uniform", 3, 60), ("mersenne", 2, 20)])
 def test_cli_long_stream_matches_reference(cli, ref, tmp_path, splitter, rows, key_bits):
     """A multi-block stream (> 32 MiB of text) through the CLI equals the
     reference CountSketch fed the same items: F2 (median), point queries and the

@@ -283,6 +283,13 @@ int mb200_sketch_allreduce(mb200_sketch* s, void* nccl_comm);
  * [7] batches binned from the raw stream (no hot pass).  L2 reductions issued =
  * rows x [2] + [5] + [6]. */
 int mb200_hot_stats(uint64_t out[8], int reset);
+/* Bench hook: while enabled, every large-table Count Sketch call records CUDA
+ * events around its dominant scatter kernel (cs_hot / cs_private /
+ * cs_private89) on the stream it runs on; _read synchronizes on them, returns
+ * the summed kernel time and the number of launches, and starts a new period.
+ * Enabling also starts a new period. */
+int mb200_kernel_timer(int enable);
+int mb200_kernel_timer_read(double* total_ms, uint64_t* launches);
 /* Strategy for Count Sketch tables larger than shared memory (both exact):
  * MB200_LARGE_DIRECT (default) sends hot-set misses straight to L2 reductions;
  * MB200_LARGE_BINNED routes them through HBM bins summed in shared memory.

@@ -488,6 +488,20 @@ def probe_dsmem(cluster: int, mode: int, blocks: int, threads: int, iters: int, 
     check(harness().mb200_probe_dsmem(cluster, mode, blocks, threads, iters, words, _dptr(out), _stream(stream)))
 
 
+def kernel_timer(enable: bool = True) -> None:
+    """Bench hook: CUDA events around the dominant scatter kernel of every
+    large-table cs_update (mb200_kernel_timer)."""
+    check(lib.mb200_kernel_timer(int(enable)))
+
+
+def kernel_timer_read():
+    """(summed kernel seconds, launches) since the timer was enabled / last read."""
+    ms = C.c_double()
+    n = C.c_uint64()
+    check(lib.mb200_kernel_timer_read(C.byref(ms), C.byref(n)))
+    return ms.value / 1e3, n.value
+
+
 def hot_stats(reset: bool = False) -> dict:
     """Counters of the heavy-hitter Count Sketch kernel since the last reset."""
     out = np.zeros(8, np.uint64)

@@ -122,6 +122,8 @@ SIGNATURES = [
     ("mb200_cs_allreduce", I, [P, u64, P, P]),
     ("mb200_sketch_allreduce", I, [P, P]),
     ("mb200_hot_stats", I, [P, I]),
+    ("mb200_kernel_timer", I, [I]),
+    ("mb200_kernel_timer_read", I, [P, P]),
     ("mb200_set_large_table_strategy", I, [I, P]),
 ]
 

@@ -489,6 +489,16 @@ int mb200_cs_point_query(const mb200_sketch_desc* desc, const int64_t* d_counter
     return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_cs_point_query");
 }
 
+int mb200_kernel_timer(int enable) {
+    kernel_timer(enable != 0);
+    return MB200_OK;
+}
+
+int mb200_kernel_timer_read(double* total_ms, uint64_t* launches) {
+    cudaError_t e = kernel_timer_read(total_ms, launches);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_kernel_timer_read");
+}
+
 int mb200_hot_stats(uint64_t out[8], int reset) {
     cudaError_t e = hot_stats(out, reset != 0);
     return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_hot_stats");

@@ -44,6 +44,8 @@
 // The table is bit-identical to the per-item path for ANY hot set (integer
 // addition commutes); the hot set only decides how much L2 traffic is saved.
 #include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "mb200_sketch_dev.cuh"
 
@@ -57,6 +59,11 @@ namespace mb200 {
 // that ran in raw mode (no hot pass)
 __device__ unsigned long long g_hot_stats[8];
 
+}  // namespace mb200
+
+#include "mb200_private89.cuh"
+
+namespace mb200 {
 namespace {
 
 using namespace sk;
@@ -672,7 +679,9 @@ __device__ __forceinline__ u32 other_slot(KeyT k, u32 s) {
 template <typename KeyT>
 __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict__ hot, const u32* __restrict__ hot_cnt,
                                                          const u32* __restrict__ hot_count, u32 cap,
-                                                         KeyT* __restrict__ sorted, KeyT* __restrict__ layout) {
+                                                         KeyT* __restrict__ sorted, KeyT* __restrict__ layout,
+                                                         const u32* __restrict__ priv_go) {
+    if (priv_go && *priv_go == 0) return;  // the private byte tables took this stream: no hot set
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
     constexpr uint32_t S = G::kSlots;
@@ -1185,6 +1194,30 @@ __global__ void __launch_bounds__(kPrivThreads, 1)
 
 inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
+// Bench hook (mb200_kernel_timer): CUDA events around the dominant scatter
+// kernel of every launch_cs_hot call (cs_hot / cs_private / cs_private89), on
+// the stream it runs on, so the roofline divides by that kernel's own time.
+struct KernelTimer {
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    size_t used = 0;
+};
+KernelTimer g_ktimer;
+inline void ktimer_mark(cudaStream_t s, bool start) {
+    KernelTimer& t = g_ktimer;
+    if (!t.on) return;
+    if (start) {
+        if (t.used == t.ev.size()) {
+            std::pair<cudaEvent_t, cudaEvent_t> p{};
+            if (cudaEventCreate(&p.first) != cudaSuccess || cudaEventCreate(&p.second) != cudaSuccess) return;
+            t.ev.push_back(p);
+        }
+        cudaEventRecord(t.ev[t.used].first, s);
+    } else if (t.used < t.ev.size()) {
+        cudaEventRecord(t.ev[t.used++].second, s);
+    }
+}
+
 // large-table strategy (mb200_set_large_table_strategy): misses either go
 // straight to L2 (fire-and-forget reductions, overlapped with the hot-key work;
 // measured fastest on configs 4 and 5) or through the binned passes 4-5
@@ -1202,10 +1235,11 @@ struct HotPlan {
     uint64_t cap_m = 0;        // miss-buffer capacity
     size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, wraps_bytes = 0, sum_bytes = 0, hot_bytes = 0,
            layout_bytes = 0, mk_bytes = 0, md_bytes = 0, bin_bytes = 0;
+    size_t p89_bytes = 0;  // config-4 shape: per-CTA byte tables (cs_private89_kernel), else 0
     // tc .. slot sums are contiguous and zeroed per call
     size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes + wraps_bytes + sum_bytes; }
     size_t total() const {
-        return tk_bytes + zero_bytes() + hot_bytes + layout_bytes + mk_bytes + md_bytes + bin_bytes;
+        return tk_bytes + zero_bytes() + hot_bytes + layout_bytes + mk_bytes + md_bytes + bin_bytes + p89_bytes;
     }
 };
 
@@ -1306,22 +1340,50 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     const size_t lbytes = sizeof(KeyT) * G::kSlots;
     if ((e = cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbytes)) != cudaSuccess)
         return e;
-    fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, cap, reinterpret_cast<KeyT*>(hot_cnt + G::kCap), layout);
     // streams without heavy hitters and unit deltas whose whole table fits
     // shared memory as bytes: private byte tables instead of one L2 reduction
     // per row update
     const uint64_t pcells = (uint64_t)sp.rows * sp.width;
     const bool priv = !binned && WK == W_NONE && SPL != SPC_ANY && pcells <= 200u * 1024 && pcells % 4 == 0 &&
                       sp.width % 4 == 0 && n >= (1u << 20);
-    if (priv) {
+    fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, cap, reinterpret_cast<KeyT*>(hot_cnt + G::kCap), layout,
+                               priv ? go : nullptr);
+    if (priv && P.p89_bytes) {
+        // config 4's shape: the specialised kernel + the fold of the per-CTA tables
+        Coef89 c89;
+        for (int j = 0; j < 4; ++j) {
+            c89.a[j][0] = (u32)sp.lo[j];
+            c89.a[j][1] = (u32)(sp.lo[j] >> 32);
+            c89.a[j][2] = (u32)sp.hi[j];
+        }
+        constexpr int LW = 16;
+        auto fp = cs_private89_kernel<LW>;
+        constexpr size_t tbytes = 2u << LW;
+        if ((e = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes)) != cudaSuccess)
+            return e;
+        uint4* scratch = reinterpret_cast<uint4*>(ws + P.total() - P.p89_bytes);
+        const u64* k64 = reinterpret_cast<const u64*>(keys);
+        ktimer_mark(s, true);
+        fp<<<sms, kP89Threads, tbytes, s>>>(c89, reinterpret_cast<const ulonglong2*>(keys), n / 2,
+                                            (n & 1) ? k64 + n - 1 : nullptr, scratch,
+                                            reinterpret_cast<uint64_t*>(table), go);
+        ktimer_mark(s, false);
+        const u32 cols = (u32)(tbytes / 16);
+        private_fold_kernel<<<(cols + kFoldCols - 1) / kFoldCols, kFoldThreads, 0, s>>>(scratch, cols, (u32)sms,
+                                                                                        table, go);
+    } else if (priv) {
         auto fp = cs_private_kernel<MODE, K, SPL, KeyT>;
         if ((e = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcells)) != cudaSuccess)
             return e;
+        ktimer_mark(s, true);
         fp<<<sms, kPrivThreads, pcells, s>>>(sp, keys, n, table, go);
+        ktimer_mark(s, false);
     }
+    if (!priv) ktimer_mark(s, true);
     fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, layout, slot_sum, hot_sum,
                                                           binned ? P.m : 0, mb, vec_ok, wraps,
                                                           priv ? go : nullptr);
+    if (!priv) ktimer_mark(s, false);
     hh_merge_kernel<MODE, K, SPL, KeyT><<<(G::kSlots + 255) / 256, 256, 0, s>>>(sp, layout, slot_sum, table);
     if ((e = cudaGetLastError()) != cudaSuccess || !binned) return e;
     auto fb_raw = g.bpr == 1 ? cs_bin_kernel<MODE, K, SPL, KeyT, WK, true, true>
@@ -1353,7 +1415,13 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
 template <int MODE, int K, typename KeyT, int WK>
 cudaError_t launch_hot(const SketchParams& sp, const void* keys, const void* w, uint64_t n, int64_t* table,
                        cudaStream_t s) {
-    const HotPlan<KeyT> P = plan_hot<KeyT>(sp, n);
+    HotPlan<KeyT> P = plan_hot<KeyT>(sp, n);
+    // config 4's shape (cs_private89_kernel): 2^89-1, k = 4, u64 keys (16-byte
+    // aligned), unit deltas, one family split two-for-one into 2 x 2^16 counters
+    if (MODE == M89 && K == 4 && std::is_same<KeyT, u64>::value && WK == W_NONE &&
+        sp.splitter == SPLIT_TWO_FOR_ONE && sp.families == 1 && sp.rows == 2 && sp.width == 65536 &&
+        P.g.nb == 0 && n >= (1u << 20) && (reinterpret_cast<uintptr_t>(keys) & 15) == 0)
+        P.p89_bytes = (size_t)sm_count() * (2u << 16);
     unsigned char* ws = nullptr;
     cudaError_t e = cudaMallocAsync(&ws, P.total(), s);
     if (e != cudaSuccess) return e;
@@ -1403,6 +1471,26 @@ int set_large_table_strategy(int s) {
     const int old = g_strategy;
     g_strategy = s;
     return old;
+}
+
+void kernel_timer(bool enable) {
+    g_ktimer.on = enable;
+    g_ktimer.used = 0;
+}
+
+cudaError_t kernel_timer_read(double* total_ms, uint64_t* launches) {
+    double tot = 0;
+    for (size_t i = 0; i < g_ktimer.used; ++i) {
+        cudaError_t e = cudaEventSynchronize(g_ktimer.ev[i].second);
+        if (e != cudaSuccess) return e;
+        float ms = 0;
+        if ((e = cudaEventElapsedTime(&ms, g_ktimer.ev[i].first, g_ktimer.ev[i].second)) != cudaSuccess) return e;
+        tot += ms;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = g_ktimer.used;
+    g_ktimer.used = 0;
+    return cudaSuccess;
 }
 
 cudaError_t hot_stats(uint64_t out[8], bool reset) {

@@ -1003,3 +1003,61 @@ def test_private_byte_tables_wrap_exactly(cuda, mb, orc, c0):
     assert (got == exp).all()
     assert np.count_nonzero(got) == 2 and abs(got).sum() == 2 * n
     assert hs["direct"] == 0 and hs["bin_merges"] > 0
+
+
+# --- config 4's specialised kernel (cs_private89_kernel + private_fold_kernel) ---
+
+
+def _c4_run(mb, orc, fam, keys):
+    import torch
+
+    spec = mb.SketchSpec(2, 1 << 16, 89, [fam], 64, mb.SPLIT_TWO_FOR_ONE)
+    table = torch.zeros(2 << 16, dtype=torch.int64, device="cuda")
+    mb.hot_stats(reset=True)
+    mb.cs_update(spec, keys if not isinstance(keys, np.ndarray) else dev(keys), table)
+    hs = mb.hot_stats(reset=True)
+    kh = keys if isinstance(keys, np.ndarray) else host_u64(keys)
+    exp = orc.cs_process(2, 1 << 16, 89, [fam], 64, mb.SPLIT_TWO_FOR_ONE, kh)
+    return table.cpu().numpy(), exp, hs
+
+
+@pytest.mark.parametrize("c0", [0x0123456789ABCDEF01234 & P89, P89 - 1, 12345, (1 << 87) | 0xFF])
+def test_c4_kernel_byte_cells_wrap_exactly(cuda, mb, orc, c0):
+    """A constant 89-bit polynomial sends 2^23 distinct keys to one cell per row
+    (both signs, every byte position of the word): each CTA's byte cell wraps
+    hundreds of times; the table equals the oracle's and nothing went to L2
+    directly."""
+    n = 1 << 23
+    keys = (np.arange(n, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)).astype(np.uint64)
+    got, exp, hs = _c4_run(mb, orc, [c0, 0, 0, 0], keys)
+    assert (got == exp).all()
+    assert np.count_nonzero(got) == 2 and abs(got).sum() == 2 * n
+    assert hs["direct"] == 0 and hs["items"] == n
+
+
+def test_c4_kernel_hash_equal_to_p(cuda, mb, orc):
+    """h(x) = x - 12345 mod p: for x = 12345 the last fold leaves y = p exactly
+    (h = 0), the one value the kernel's shortcut reduction patches."""
+    rng = np.random.default_rng(3)
+    n = (1 << 21) + 1  # odd: the last key takes the odd-key path
+    keys = rng.integers(0, 1 << 64, n, dtype=np.uint64)
+    keys[[0, 1000, n // 2, n - 1]] = 12345
+    keys[[5, 6]] = [12344, 12346]
+    got, exp, _ = _c4_run(mb, orc, [P89 - 12345, 1, 0, 0], keys)
+    assert (got == exp).all()
+
+
+def test_c4_kernel_unaligned_and_random(cuda, mb, orc):
+    """Random 89-bit families on random keys: the specialised kernel (16-byte
+    aligned keys) and, for a view 8 bytes off, the generic private kernel."""
+    import torch
+
+    rng = np.random.default_rng(9)
+    n = (1 << 21) + 7
+    keys = rng.integers(0, 1 << 64, n + 1, dtype=np.uint64)
+    fam = orc.coeffs(89, 4, 77)
+    d = torch.from_numpy(keys.view(np.int64)).cuda()
+    got, exp, _ = _c4_run(mb, orc, fam, d[:n])
+    assert (got == exp).all()
+    got, exp, _ = _c4_run(mb, orc, fam, d[1:])
+    assert (got == exp).all()

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 import ncu_summary  # noqa: E402
 
-KERNEL_KEY = {"c5": "cs_update_kernel", "c1": "cs_update_kernel", "c4": "cs_private_kernel",
+KERNEL_KEY = {"c5": "cs_hot_kernel", "c1": "cs_small_k32_kernel", "c4": "cs_private89_kernel",
               "c2k4": "hash61_key64_kernel", "c2k8": "hash61_key64_kernel", "c3": "pm_divmod_kernel"}
 
 
@@ -76,6 +76,7 @@ def main(tag):
         traffic[t] = {"kernel": v[h.index("Kernel Name")].split("(")[0], "dram_bytes_per_launch": rd + wr,
                       "pipes": {"alu": pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
                                 "fma": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                                "fmaheavy": pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
                                 "issue": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                                 "dram": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                                 "lts": pct("lts__throughput.avg.pct_of_peak_sustained_elapsed")}}

@@ -21,8 +21,9 @@ else
 fi
 for t in $TARGETS; do
   case $t in
-    c5|c1) K="regex:cs_update|cs_hot|cs_small" ;;
-    c4) K="regex:cs_private" ;;
+    c5) K="regex:cs_hot_kernel" ;;
+    c1) K="regex:cs_small" ;;
+    c4) K="regex:cs_private89" ;;
     c2k4|c2k8) K="regex:hash61_key64" ;;
     c3) K="regex:pm_divmod" ;;
   esac

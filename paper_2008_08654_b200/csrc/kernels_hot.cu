@@ -28,19 +28,23 @@
 //                  counter, so they finish together.  Each CTA adds its slot
 //                  sums into per-slot totals, and hh_merge applies every hot
 //                  key once (hash -> split -> red).
-//   4. cs_bin    : the misses (or, when the sample shows no heavy hitters, the
-//                  raw stream -- pass 3 is then skipped) are hashed, split and
-//                  turned into 4-byte entries (13-bit cell | 19-bit signed
-//                  delta) that are staged per (row, 8192-cell bin) in shared
-//                  memory and written to per-bin buffers in HBM in 16-byte
-//                  groups (one global atomic per bin per round).
+//   4. cs_bin    : (opt-in binned strategy) the misses (or, when the sample
+//                  shows no heavy hitters, the raw stream -- pass 3 is then
+//                  skipped) are hashed, split and turned into 4-byte entries
+//                  (16-bit cell | 16-bit signed delta) that are staged per
+//                  (row, 65536-cell bin) in shared memory and written to per-bin
+//                  buffers in HBM in 16-byte groups (one global atomic per bin
+//                  per round).
 //   5. cs_accum  : one CTA per (bin, part) sums its bin's entries into an exact
-//                  shared-memory table of 8192 cells and merges it into the L2
-//                  table with one red.global per non-zero cell.
-// Passes 4-5 replace ~rows L2 reductions per missed item (the L2 atomic unit
-// runs at ~1.8e11/s, config 5's old bound) by 8 bytes of streaming HBM traffic
-// per row update.  Anything that does not fit a staging buffer, a bin, the
-// miss buffer or the 19-bit delta field takes the direct red.global path.
+//                  shared-memory table of packed 16-bit cells and merges it into
+//                  the L2 table with one red.global per non-zero cell.
+// Passes 4-5 replace ~rows L2 reductions per missed item by 8 bytes of
+// streaming HBM traffic per row update (measured slower than the direct path
+// on config 5).  Anything that does not fit a staging buffer, a bin,
+// the miss buffer or the 16-bit delta field takes the direct red.global path.
+// Streams without heavy hitters whose table fits shared memory as bytes (unit
+// deltas) take the private byte tables instead (cs_private_kernel, and config
+// 4's shape cs_private89_kernel, mb200_private89.cuh).
 // The table is bit-identical to the per-item path for ANY hot set (integer
 // addition commutes); the hot set only decides how much L2 traffic is saved.
 #include <type_traits>
@@ -488,7 +492,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
     static_assert(S % 2 == 0, "two cells per word");
     u32* cells = reinterpret_cast<u32*>(hk + S);  // S 16-bit cells
-    u64* hi = wraps + (uint64_t)blockIdx.x * S;   // this CTA's wrap counters (HBM, zeroed by the launcher)
+    u64* hi = wraps + (uint64_t)blockIdx.x * S;   // this CTA's wrap counters (HBM, zeroed below by the CTA)
     QEnt<KeyT>* q = reinterpret_cast<QEnt<KeyT>*>(cells + S / 2);
     __shared__ u32 s_next;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -518,6 +522,10 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     // of all CTAs can be merged per slot before the keys are hashed
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) hk[s] = layout[s];
     for (uint32_t s = threadIdx.x; s < S / 2; s += kHotThreads) cells[s] = 0x80008000u;
+    // the CTA's wrap counters: zeroed here, by the CTA that uses them (only calls
+    // that run this kernel pay for it; the barrier orders the stores before the
+    // CTA's atomics on them)
+    for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) hi[s] = 0;
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
 
@@ -1235,11 +1243,10 @@ struct HotPlan {
     uint64_t cap_m = 0;        // miss-buffer capacity
     size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, wraps_bytes = 0, sum_bytes = 0, hot_bytes = 0,
            layout_bytes = 0, mk_bytes = 0, md_bytes = 0, bin_bytes = 0;
-    size_t p89_bytes = 0;  // config-4 shape: per-CTA byte tables (cs_private89_kernel), else 0
     // tc .. slot sums are contiguous and zeroed per call
-    size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes + wraps_bytes + sum_bytes; }
+    size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes + sum_bytes; }
     size_t total() const {
-        return tk_bytes + zero_bytes() + hot_bytes + layout_bytes + mk_bytes + md_bytes + bin_bytes + p89_bytes;
+        return tk_bytes + zero_bytes() + wraps_bytes + hot_bytes + layout_bytes + mk_bytes + md_bytes + bin_bytes;
     }
 };
 
@@ -1307,9 +1314,11 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     u32* hot_sum = hot_count + 1;
     unsigned long long* mcount = reinterpret_cast<unsigned long long*>(hot_count + 2);
     g.gcnt = reinterpret_cast<unsigned long long*>(ws + P.tk_bytes + P.tc_bytes + P.misc);
-    u64* wraps = reinterpret_cast<u64*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes);
-    u64* slot_sum = reinterpret_cast<u64*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes + P.wraps_bytes);
-    unsigned char* p = ws + P.tk_bytes + P.zero_bytes();
+    // zeroed per call: tc | misc | gcnt | slot sums; then the wrap counters (zeroed
+    // by cs_hot_kernel's CTAs themselves)
+    u64* slot_sum = reinterpret_cast<u64*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes);
+    u64* wraps = reinterpret_cast<u64*>(ws + P.tk_bytes + P.zero_bytes());
+    unsigned char* p = ws + P.tk_bytes + P.zero_bytes() + P.wraps_bytes;
     KeyT* hot = reinterpret_cast<KeyT*>(p);
     u32* hot_cnt = reinterpret_cast<u32*>(hot + G::kCap);
     p += P.hot_bytes;
@@ -1348,30 +1357,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
                       sp.width % 4 == 0 && n >= (1u << 20);
     fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, cap, reinterpret_cast<KeyT*>(hot_cnt + G::kCap), layout,
                                priv ? go : nullptr);
-    if (priv && P.p89_bytes) {
-        // config 4's shape: the specialised kernel + the fold of the per-CTA tables
-        Coef89 c89;
-        for (int j = 0; j < 4; ++j) {
-            c89.a[j][0] = (u32)sp.lo[j];
-            c89.a[j][1] = (u32)(sp.lo[j] >> 32);
-            c89.a[j][2] = (u32)sp.hi[j];
-        }
-        constexpr int LW = 16;
-        auto fp = cs_private89_kernel<LW>;
-        constexpr size_t tbytes = 2u << LW;
-        if ((e = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes)) != cudaSuccess)
-            return e;
-        uint4* scratch = reinterpret_cast<uint4*>(ws + P.total() - P.p89_bytes);
-        const u64* k64 = reinterpret_cast<const u64*>(keys);
-        ktimer_mark(s, true);
-        fp<<<sms, kP89Threads, tbytes, s>>>(c89, reinterpret_cast<const ulonglong2*>(keys), n / 2,
-                                            (n & 1) ? k64 + n - 1 : nullptr, scratch,
-                                            reinterpret_cast<uint64_t*>(table), go);
-        ktimer_mark(s, false);
-        const u32 cols = (u32)(tbytes / 16);
-        private_fold_kernel<<<(cols + kFoldCols - 1) / kFoldCols, kFoldThreads, 0, s>>>(scratch, cols, (u32)sms,
-                                                                                        table, go);
-    } else if (priv) {
+    if (priv) {
         auto fp = cs_private_kernel<MODE, K, SPL, KeyT>;
         if ((e = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcells)) != cudaSuccess)
             return e;
@@ -1412,16 +1398,49 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     return cudaGetLastError();
 }
 
+// config 4's shape: cs_private89_kernel + private_fold_kernel, one CTA per SM,
+// per-CTA byte tables (128 KiB each) in a scratch area of the stream-ordered pool
+cudaError_t run_private89(const SketchParams& sp, const u64* keys, uint64_t n, int64_t* table, cudaStream_t s) {
+    constexpr int LW = 16;
+    constexpr size_t tbytes = 2u << LW;
+    const int sms = sm_count();
+    Coef89 c89;
+    for (int j = 0; j < 4; ++j) {
+        c89.a[j][0] = (u32)sp.lo[j];
+        c89.a[j][1] = (u32)(sp.lo[j] >> 32);
+        c89.a[j][2] = (u32)sp.hi[j];
+    }
+    auto fp = cs_private89_kernel<LW>;
+    cudaError_t e = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes);
+    if (e != cudaSuccess) return e;
+    uint4* scratch = nullptr;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (size_t)sms * tbytes, s)) != cudaSuccess) return e;
+    ktimer_mark(s, true);
+    fp<<<sms, kP89Threads, tbytes, s>>>(c89, reinterpret_cast<const ulonglong2*>(keys), n / 2,
+                                        (n & 1) ? keys + n - 1 : nullptr, scratch,
+                                        reinterpret_cast<uint64_t*>(table), nullptr);
+    ktimer_mark(s, false);
+    const u32 cols = (u32)(tbytes / 16);
+    private_fold_kernel<<<(cols + kFoldCols - 1) / kFoldCols, kFoldThreads, 0, s>>>(scratch, cols, (u32)sms, table,
+                                                                                    nullptr);
+    e = cudaGetLastError();
+    const cudaError_t e2 = cudaFreeAsync(scratch, s);
+    return e != cudaSuccess ? e : e2;
+}
+
 template <int MODE, int K, typename KeyT, int WK>
 cudaError_t launch_hot(const SketchParams& sp, const void* keys, const void* w, uint64_t n, int64_t* table,
                        cudaStream_t s) {
-    HotPlan<KeyT> P = plan_hot<KeyT>(sp, n);
     // config 4's shape (cs_private89_kernel): 2^89-1, k = 4, u64 keys (16-byte
-    // aligned), unit deltas, one family split two-for-one into 2 x 2^16 counters
+    // aligned), unit deltas, one family split two-for-one into 2 x 2^16 counters.
+    // Byte tables are exact for any stream and their cost does not depend on its
+    // skew (a hot cell leaves [0, 2^8) once per 2^8 updates of one CTA), so this
+    // shape skips the heavy-hitter probe and its chain of kernels altogether.
     if (MODE == M89 && K == 4 && std::is_same<KeyT, u64>::value && WK == W_NONE &&
         sp.splitter == SPLIT_TWO_FOR_ONE && sp.families == 1 && sp.rows == 2 && sp.width == 65536 &&
-        P.g.nb == 0 && n >= (1u << 20) && (reinterpret_cast<uintptr_t>(keys) & 15) == 0)
-        P.p89_bytes = (size_t)sm_count() * (2u << 16);
+        g_strategy == STRAT_DIRECT && n >= (1u << 20) && (reinterpret_cast<uintptr_t>(keys) & 15) == 0)
+        return run_private89(sp, reinterpret_cast<const u64*>(keys), n, table, s);
+    HotPlan<KeyT> P = plan_hot<KeyT>(sp, n);
     unsigned char* ws = nullptr;
     cudaError_t e = cudaMallocAsync(&ws, P.total(), s);
     if (e != cudaSuccess) return e;
@@ -1451,7 +1470,9 @@ cudaError_t launch_mode(const SketchParams& sp, const void* keys, const void* w,
 }
 
 // Keep the default stream-ordered pool's memory between calls: the hot path
-// allocates its ~12 MiB workspace per call with cudaMallocAsync.
+// allocates its workspace per call with cudaMallocAsync (sample tables, the
+// per-CTA wrap counters -- sms x slots x 8 B, 42 MB for u32 keys -- and, for
+// the binned strategy, the bins; config 4's shape: 148 x 128 KiB byte tables).
 void retain_pool() {
     static bool done[64] = {false};
     const int dev = device_id();

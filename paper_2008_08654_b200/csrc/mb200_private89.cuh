@@ -243,7 +243,7 @@ template <int LW>
 __global__ void __launch_bounds__(kP89Threads, 1)
     cs_private89_kernel(const Coef89 c, const ulonglong2* __restrict__ kv, uint64_t npairs, const u64* __restrict__ odd,
                         uint4* __restrict__ scratch, uint64_t* __restrict__ l2, const u32* __restrict__ go) {
-    if (*go) return;
+    if (go && *go) return;
     extern __shared__ __align__(16) u32 pwords[];
     constexpr u32 kWords = (2u << LW) / 4;
     uint4* pw4 = reinterpret_cast<uint4*>(pwords);
@@ -290,7 +290,7 @@ constexpr int kFoldMaxPer = 10;  // CTAs per group handled in one unrolled batch
 __global__ void __launch_bounds__(kFoldThreads)
     private_fold_kernel(const uint4* __restrict__ scratch, u32 cols, u32 ctas, i64* __restrict__ table,
                         const u32* __restrict__ go) {
-    if (*go) return;
+    if (go && *go) return;
     __shared__ i32 part[kFoldGroups][kFoldCols][17];
     const u32 ci = threadIdx.x % kFoldCols, grp = threadIdx.x / kFoldCols;
     const u32 col = blockIdx.x * kFoldCols + ci;

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <exception>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -576,6 +577,17 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
     cudaStream_t cs = (cudaStream_t)stream_;
     const u64 chunks = (n + st.chunk - 1) / st.chunk;
     st.narrow_bits = 8;
+    // A throw mid-loop (CUDA error, status) must not leave copies in flight from
+    // the staging slots the next call repacks: drain both streams first.
+    struct Drain {
+        cudaStream_t a, b;
+        ~Drain() {
+            if (std::uncaught_exceptions()) {
+                cudaStreamSynchronize(a);
+                cudaStreamSynchronize(b);
+            }
+        }
+    } drain{st.copy, cs};
     for (u64 c = 0; c < chunks; ++c) {
         const int slot = int(c & 1);
         const u64 off = c * st.chunk;

@@ -290,13 +290,16 @@ int mb200_hot_stats(uint64_t out[8], int reset);
  * Enabling also starts a new period. */
 int mb200_kernel_timer(int enable);
 int mb200_kernel_timer_read(double* total_ms, uint64_t* launches);
-/* Strategy for Count Sketch tables larger than shared memory (both exact):
+/* Strategy for Count Sketch tables larger than shared memory (all exact):
  * MB200_LARGE_DIRECT (default) sends hot-set misses straight to L2 reductions;
- * MB200_LARGE_BINNED routes them through HBM bins summed in shared memory.
+ * MB200_LARGE_BINNED routes them through HBM bins summed in shared memory;
+ * MB200_LARGE_ROWS leaves them in an HBM miss buffer that row passes (one CTA =
+ * one whole row of <= 2^16 cells in shared memory) sum per row.
  * *previous (if not NULL) receives the strategy in force before the call.
  * MB200_INVALID_ARGUMENT for an unknown strategy. */
 #define MB200_LARGE_DIRECT 0
 #define MB200_LARGE_BINNED 1
+#define MB200_LARGE_ROWS 2
 int mb200_set_large_table_strategy(int strategy, int* previous);
 #ifdef __cplusplus
 }

@@ -510,12 +510,13 @@ def hot_stats(reset: bool = False) -> dict:
             "binned": int(out[4]), "direct": int(out[5]), "bin_merges": int(out[6]), "raw_batches": int(out[7])}
 
 
-LARGE_DIRECT, LARGE_BINNED = 0, 1
+LARGE_DIRECT, LARGE_BINNED, LARGE_ROWS = 0, 1, 2
 
 
 def set_large_table_strategy(strategy: int) -> int:
     """Route hot-set misses of large tables to L2 reductions (LARGE_DIRECT, default) or
-    through HBM bins (LARGE_BINNED); returns the previous strategy."""
+    through HBM bins (LARGE_BINNED) or through the miss buffer and per-row passes
+    (LARGE_ROWS); returns the previous strategy."""
     prev = C.c_int(0)
     check(lib.mb200_set_large_table_strategy(int(strategy), C.byref(prev)))
     return prev.value

@@ -1200,6 +1200,120 @@ __global__ void __launch_bounds__(kPrivThreads, 1)
     if (threadIdx.x == 0) atomicAdd(&g_hot_stats[0], (unsigned long long)(hi - lo));
 }
 
+// ---------------------------------------------------------------------------
+// Row passes over the miss buffer (strategy STRAT_ROWS).  The hot pass leaves
+// every missed item in the HBM miss buffer instead of sending rows L2
+// reductions; then each CTA takes ONE row r = blockIdx % rows and a slice of the
+// buffer, keeps that whole row in shared memory as 2^15-biased 16-bit cells
+// (two per word, 2^16 cells = 128 KiB), hashes its slice for row r only and
+// adds with one shared atomic per item.  The CTAs of one slice (blockIdx / rows)
+// read it at the same time, so it comes from HBM once and from L2 rows - 1
+// times.  A cell leaving [0, 2^16) (any i32 delta) records, per 16-bit cell the
+// carry / borrow reached, (intended - displayed) change to L2 -- byte_add's
+// exact accounting on 16-bit cells.  The rows' tables go to scratch and
+// rows_fold_kernel sums each row's CTAs per cell: 148 x 2^16 cells instead of
+// rows L2 reductions per missed item.
+constexpr int kRowThreads = 1024;
+
+__device__ __noinline__ void cell16_fix(uint64_t* l2row, u32 cell, i64 d, u32 old, u32 dw) {
+    const u32 q = cell & 1u, base = cell & ~1u;
+    const u32 nw = old + dw;
+    for (u32 j = q; j < 2; ++j) {
+        const i32 disp = (i32)((nw >> (16 * j)) & 0xffffu) - (i32)((old >> (16 * j)) & 0xffffu);
+        const i64 rec = (j == q ? d : 0) - disp;
+        if (rec) red_add_u64(l2row + base + j, (u64)rec);
+    }
+}
+
+template <int MODE, int K, int SPL, typename KeyT>
+__device__ __forceinline__ u32 row_cell(const SketchParams& sp, u32 f, u32 sub, KeyT key, bool& neg) {
+    if constexpr ((MODE == M61_K32 || MODE == M61_K64) && K > 0 && SPL == SPC_POW2) {
+        return h61_pow2_split(hash61_lazy<MODE, K>(sp, f, (u64)key), (u32)(sp.width - 1), neg);
+    } else {
+        u64 hlo, hhi = 0;
+        if (MODE == M89) hash89<K>(sp, f, (u64)key, hlo, hhi);
+        else hlo = hash_small<MODE, K>(sp, f, (u64)key);
+        return split_c<MODE, SPL>(sp, hlo, hhi, sub, neg);
+    }
+}
+
+template <int MODE, int K, int SPL, typename KeyT>
+__global__ void __launch_bounds__(kRowThreads, 1)
+    cs_rowpass_kernel(const SketchParams sp, const MissBuf<KeyT> mb, u32* __restrict__ scratch, i64* __restrict__ table) {
+    extern __shared__ __align__(16) u32 rw[];
+    const u32 W = (u32)sp.width, nw = W / 2;
+    for (u32 i = threadIdx.x; i < nw; i += kRowThreads) rw[i] = 0x80008000u;
+    __syncthreads();
+    const u32 row = blockIdx.x % sp.rows, part = blockIdx.x / sp.rows;
+    const u32 nparts = (gridDim.x - row + sp.rows - 1) / sp.rows;
+    const u32 f = SPL == SPC_TFO ? row / 2 : row, sub = SPL == SPC_TFO ? row % 2 : 0;
+    uint64_t* l2row = reinterpret_cast<uint64_t*>(table) + (size_t)row * W;
+    const uint64_t stored = *mb.count;
+    const uint64_t n = stored < mb.cap ? stored : mb.cap;
+    const uint64_t lo = n * part / nparts, hi = n * (part + 1) / nparts;
+    constexpr int kU = 4;  // items per thread in flight
+    auto one = [&](KeyT key, i32 d) {
+        bool neg;
+        const u32 cell = row_cell<MODE, K, SPL, KeyT>(sp, f, sub, key, neg);
+        const i64 dd = neg ? -(i64)d : (i64)d;  // (-INT32_MIN = 2^31: the reference's wrapping negation)
+        const u32 sh = (cell & 1u) << 4;
+        const u32 dw = (u32)dd << sh;
+        const u32 old = atomicAdd(rw + (cell >> 1), dw);
+        const i64 nb = (i64)((old >> sh) & 0xffffu) + dd;
+        if (__builtin_expect((u64)nb > 0xffffu, 0)) cell16_fix(l2row, cell, dd, old, dw);
+    };
+    uint64_t i = lo + threadIdx.x;
+    for (; i + (kU - 1) * kRowThreads < hi; i += kU * kRowThreads) {
+        KeyT k[kU];
+        i32 d[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            k[u] = __ldcg(mb.keys + i + u * kRowThreads);
+            d[u] = __ldcg(mb.deltas + i + u * kRowThreads);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) one(k[u], d[u]);
+    }
+    for (; i < hi; i += kRowThreads) one(__ldcg(mb.keys + i), __ldcg(mb.deltas + i));
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(scratch + (size_t)blockIdx.x * nw);
+    const uint4* src = reinterpret_cast<const uint4*>(rw);
+    for (u32 j = threadIdx.x; j < nw / 4; j += kRowThreads) dst[j] = src[j];
+    if (threadIdx.x == 0) atomicAdd(&g_hot_stats[4], (unsigned long long)(hi - lo));
+}
+
+// table[row][cell] += sum over the row's CTAs of (cell - 2^15); one thread per
+// word (two cells) of one row
+__global__ void __launch_bounds__(256)
+    rows_fold_kernel(const u32* __restrict__ scratch, u32 rows, u32 width, u32 ctas, i64* __restrict__ table) {
+    const u32 nw = width / 2;
+    const u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (u64)rows * nw) return;
+    const u32 row = (u32)(gid / nw), w = (u32)(gid % nw);
+    const u32 nparts = (ctas - row + rows - 1) / rows;
+    i32 lo = 0, hi = 0;
+    u32 p = 0;
+    for (; p + 8 <= nparts; p += 8) {
+        u32 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(scratch + (size_t)(row + (p + u) * rows) * nw + w);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            lo += (i32)(v[u] & 0xffffu);
+            hi += (i32)(v[u] >> 16);
+        }
+    }
+    for (; p < nparts; ++p) {
+        const u32 v = __ldcg(scratch + (size_t)(row + p * rows) * nw + w);
+        lo += (i32)(v & 0xffffu);
+        hi += (i32)(v >> 16);
+    }
+    const i32 bias = 0x8000 * (i32)nparts;
+    i64* t = table + (size_t)row * width + 2 * w;
+    if (lo != bias) t[0] = (i64)((u64)t[0] + (u64)(i64)(lo - bias));
+    if (hi != bias) t[1] = (i64)((u64)t[1] + (u64)(i64)(hi - bias));
+}
+
 inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 // Bench hook (mb200_kernel_timer): CUDA events around the dominant scatter
@@ -1243,10 +1357,13 @@ struct HotPlan {
     uint64_t cap_m = 0;        // miss-buffer capacity
     size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, wraps_bytes = 0, sum_bytes = 0, hot_bytes = 0,
            layout_bytes = 0, mk_bytes = 0, md_bytes = 0, bin_bytes = 0;
+    bool rows_mode = false;  // STRAT_ROWS: misses to the buffer, then the row passes
+    size_t rows_bytes = 0;   // row passes' per-CTA tables
     // tc .. slot sums are contiguous and zeroed per call
     size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes + sum_bytes; }
     size_t total() const {
-        return tk_bytes + zero_bytes() + wraps_bytes + hot_bytes + layout_bytes + mk_bytes + md_bytes + bin_bytes;
+        return tk_bytes + zero_bytes() + wraps_bytes + hot_bytes + layout_bytes + mk_bytes + md_bytes + bin_bytes +
+               rows_bytes;
     }
 };
 
@@ -1294,6 +1411,14 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     P.sum_bytes = align256((size_t)G::kSlots * 8);
     P.layout_bytes = align256((size_t)G::kSlots * sizeof(KeyT));
     P.hot_bytes = align256((size_t)G::kCap * (2 * sizeof(KeyT) + 4));  // hot list, counts, sorted keys
+    // row passes: Pow2 / two-for-one splitters of power-of-two rows <= 2^16 cells
+    P.rows_mode = g_strategy == STRAT_ROWS && !binned && (sp.b == 61 || sp.b == 89) &&
+                  (sp.splitter == SPLIT_POW2 || sp.splitter == SPLIT_TWO_FOR_ONE) && sp.width >= 8 &&
+                  sp.width <= 65536 && (sp.width & (sp.width - 1)) == 0 && sp.rows <= (uint32_t)sm_count();
+    if (P.rows_mode) {
+        P.cap_m = (n / 2 + 31) & ~31ull;  // the rest, if ever, goes straight to L2
+        P.rows_bytes = align256((size_t)sm_count() * sp.width * 2);
+    }
     P.mk_bytes = align256((size_t)P.cap_m * sizeof(KeyT));
     P.md_bytes = align256((size_t)P.cap_m * 4);
     P.bin_bytes = (size_t)g.nb * g.cap * 4;
@@ -1336,7 +1461,9 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots, go);
     hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(tk, tc, hist, cap, hot, hot_cnt,
                                                                             hot_count, hot_sum, P.slots, go);
-    auto fn = binned ? cs_hot_kernel<MODE, K, SPL, KeyT, WK, true> : cs_hot_kernel<MODE, K, SPL, KeyT, WK, false>;
+    const bool rows_mode = P.rows_mode && SPL != SPC_ANY;
+    auto fn = binned || rows_mode ? cs_hot_kernel<MODE, K, SPL, KeyT, WK, true>
+                                  : cs_hot_kernel<MODE, K, SPL, KeyT, WK, false>;
     const size_t smem = ((size_t)sizeof(KeyT) + 2) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * sizeof(QEnt<KeyT>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes));
@@ -1371,6 +1498,19 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
                                                           priv ? go : nullptr);
     if (!priv) ktimer_mark(s, false);
     hh_merge_kernel<MODE, K, SPL, KeyT><<<(G::kSlots + 255) / 256, 256, 0, s>>>(sp, layout, slot_sum, table);
+    if (rows_mode) {
+        if constexpr (SPL != SPC_ANY) {
+            auto fr = cs_rowpass_kernel<MODE, K, SPL, KeyT>;
+            const size_t rbytes = (size_t)sp.width * 2;
+            if ((e = cudaFuncSetAttribute(fr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rbytes)) != cudaSuccess)
+                return e;
+            u32* rscratch = reinterpret_cast<u32*>(ws + P.total() - P.rows_bytes);
+            fr<<<sms, kRowThreads, rbytes, s>>>(sp, mb, rscratch, table);
+            const uint64_t words = (uint64_t)sp.rows * (sp.width / 2);
+            rows_fold_kernel<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(rscratch, sp.rows, (u32)sp.width,
+                                                                          (u32)sms, table);
+        }
+    }
     if ((e = cudaGetLastError()) != cudaSuccess || !binned) return e;
     auto fb_raw = g.bpr == 1 ? cs_bin_kernel<MODE, K, SPL, KeyT, WK, true, true>
                              : cs_bin_kernel<MODE, K, SPL, KeyT, WK, true, false>;
@@ -1488,7 +1628,7 @@ void retain_pool() {
 }  // namespace
 
 int set_large_table_strategy(int s) {
-    if (s != STRAT_DIRECT && s != STRAT_BINNED) return -1;
+    if (s != STRAT_DIRECT && s != STRAT_BINNED && s != STRAT_ROWS) return -1;
     const int old = g_strategy;
     g_strategy = s;
     return old;

@@ -63,7 +63,7 @@ cudaError_t hot_stats(uint64_t out[8], bool reset);
 // bench hook: events around the dominant scatter kernel of each launch_cs_hot call
 void kernel_timer(bool enable);
 cudaError_t kernel_timer_read(double* total_ms, uint64_t* launches);
-enum LargeTableStrategy { STRAT_DIRECT = 0, STRAT_BINNED = 1 };
+enum LargeTableStrategy { STRAT_DIRECT = 0, STRAT_BINNED = 1, STRAT_ROWS = 2 };
 int set_large_table_strategy(int s);  // returns the previous strategy, -1 if invalid
 cudaError_t launch_cs_moments(const int64_t* table, uint32_t rows, uint64_t width, uint64_t* out,
                               cudaStream_t s);

@@ -378,15 +378,19 @@ HOT_CASES = [
 ]
 
 
-@pytest.mark.parametrize("strategy", ["direct", "binned"])
+STRATEGIES = {"direct": 0, "binned": 1, "rows": 2}
+
+
+@pytest.mark.parametrize("strategy", ["direct", "binned", "rows"])
 @pytest.mark.parametrize("case", HOT_CASES, ids=[f"r{c[0]}b{c[2]}{c[5]}" for c in HOT_CASES])
 def test_hot_path_large_batches(cuda, mb, orc, case, strategy):
-    """Both large-table strategies (misses -> L2 reductions, misses -> HBM bins summed
-    in shared memory) give the oracle's table bit for bit."""
+    """Every large-table strategy (misses -> L2 reductions, misses -> HBM bins summed
+    in shared memory, misses -> miss buffer summed by per-row passes) gives the
+    oracle's table bit for bit."""
     import torch
 
     rows, width, b, kb, sp, kind, wdt = case
-    prev = mb.set_large_table_strategy(mb.LARGE_BINNED if strategy == "binned" else mb.LARGE_DIRECT)
+    prev = mb.set_large_table_strategy(STRATEGIES[strategy])
     spec, fams = make_spec(mb, orc, rows, width, b, kb, sp, 0xB16 + rows)
     n = (1 << 22) + 12345
     zk, zw = orc.gen_zipf_items(7, 0, n)
@@ -413,10 +417,13 @@ def test_hot_path_large_batches(cuda, mb, orc, case, strategy):
     assert st["items"] == n
     if strategy == "binned" and rows * -(-width // 65536) <= 64:
         assert st["binned"] > 0  # the binned passes really ran
+    if strategy == "rows" and sp in (0, 3) and b in (61, 89) and width <= 65536:
+        assert st["binned"] > 0  # the row passes really ran (entries they summed)
 
 
-@pytest.mark.parametrize("shape", ["overflow", "wide", "bigdelta"])
-def test_binned_strategy_edge_paths(cuda, mb, orc, shape):
+@pytest.mark.parametrize("shape,strategy", [("overflow", "binned"), ("wide", "binned"), ("bigdelta", "binned"),
+                                            ("overflow", "rows"), ("bigdelta", "rows")])
+def test_binned_strategy_edge_paths(cuda, mb, orc, shape, strategy):
     """The binned strategy's fall-backs stay exact: more misses than the miss buffer
     holds (35% one key, 65% distinct keys: not raw mode, misses > n/2), rows wider
     than one 65536-cell bin (several bins per row, ballot grouping), and deltas
@@ -437,7 +444,7 @@ def test_binned_strategy_edge_paths(cuda, mb, orc, shape):
         big = rng.random(n) < 0.1
         w[big] = rng.integers(-(2**31), 2**31, size=int(big.sum())).astype(np.int32)
     cnt = torch.zeros(rows * width, dtype=torch.int64, device="cuda")
-    prev = mb.set_large_table_strategy(mb.LARGE_BINNED)
+    prev = mb.set_large_table_strategy(STRATEGIES[strategy])
     mb.hot_stats(reset=True)
     try:
         mb.cs_update(spec, dev(keys), cnt, dev(w))
@@ -446,7 +453,11 @@ def test_binned_strategy_edge_paths(cuda, mb, orc, shape):
     st = mb.hot_stats(reset=True)
     exp = orc.cs_process(rows, width, 61, fams, 32, 0, keys, w)
     assert (cnt.cpu().numpy() == exp).all()
-    assert st["binned"] > 0 and st["direct"] > 0  # both the bins and a fall-back path ran
+    if strategy == "binned":
+        assert st["binned"] > 0 and st["direct"] > 0  # both the bins and a fall-back path ran
+    else:
+        assert st["binned"] > 0  # the row passes ran (and, for "overflow", the direct fall-back)
+        assert shape != "overflow" or st["direct"] > 0
 
 
 def test_large_table_strategy_rejects_unknown(cuda, mb):

@@ -19,11 +19,14 @@ def main():
     ap.add_argument("which", choices=["c1", "c2k4", "c2k8", "c3", "c4", "c5"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--binned", action="store_true", help="large tables: binned strategy")
+    ap.add_argument("--rows", action="store_true", help="large tables: miss buffer + row passes")
     ap.add_argument("--items", type=int, default=1 << 31, help="config-5 stream length (one shard of N GPUs)")
     a = ap.parse_args()
     w = a.which
     if a.binned:
         mb.set_large_table_strategy(mb.LARGE_BINNED)
+    if a.rows:
+        mb.set_large_table_strategy(mb.LARGE_ROWS)
     if w == "c5":
         zs = mb.ZipfStream(S)
         keys, wts = zs.generate(0, a.items)

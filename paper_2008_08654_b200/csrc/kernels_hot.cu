@@ -323,32 +323,36 @@ __global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restr
     if (threadIdx.x == 0 && cta_sum) atomicAdd(hot_sum, cta_sum);  // sampled items the hot set covers
 }
 
-// Exact 64-bit accumulation in a 16-bit shared cell + a u64 wrap counter in
-// HBM (units of 2^16).  sm_100 has no 16-bit (or native 64-bit) shared atomic
-// add, so two cells share a 32-bit word: cell h is bits 16 (h & 1) of word
-// h >> 1, biased by 2^15 so a sum hovering around zero rarely leaves [0, 2^16).
-// The delta is added to the word shifted to its cell.  Every atomic change x
-// of a cell whose value was c records floor((c + x) / 2^16) in the cell's wrap
-// counter, which keeps cell + 2^16 wraps = bias + sum of its deltas exactly,
-// under any interleaving: a low-cell add that leaves [0, 2^16) also carries w
-// into the high cell (recorded against the high cell's value at that same
-// atomic), and w is then taken back out of the high cell by a second atomic
-// (recorded against its value then).  Halving the cell width fits 35840
-// instead of 24576 slots into shared memory.
-__device__ __forceinline__ void hot_accumulate(u32* cells, u64* wraps_cta, u32 h, i32 d) {
+// Exact 64-bit accumulation in a 16-bit shared cell; the cell's wraps (units of
+// 2^16) go straight into its slot's total in HBM.  sm_100 has no 16-bit (or
+// native 64-bit) shared atomic add, so two cells share a 32-bit word: cell h is
+// bits 16 (h & 1) of word h >> 1, biased by 2^15 so a sum hovering around zero
+// rarely leaves [0, 2^16).  The delta is added to the word shifted to its cell.
+// Every atomic change x of a cell whose value was c adds 2^16 floor((c + x) /
+// 2^16) to the slot's total slot_sum[h] (shared by all CTAs: every CTA holds
+// the same layout, and the totals are sums anyway), which keeps
+//   sum over CTAs of (cell - bias) + slot_sum = sum of the slot's deltas
+// exactly, under any interleaving: a low-cell add that leaves [0, 2^16) also
+// carries w into the high cell (recorded against the high cell's value at that
+// same atomic), and w is then taken back out of the high cell by a second
+// atomic (recorded against its value then).  The range test is a 32-bit
+// compare: c + x as a mathematical value lies in [-2^31, 2^31 + 2^16), so its
+// u32 image exceeds 0xFFFF exactly when it is outside [0, 2^16).  Halving the
+// cell width fits 35840 instead of 24576 slots into shared memory.
+__device__ __forceinline__ void hot_accumulate(u32* cells, u64* slot_sum, u32 h, i32 d) {
     typedef unsigned long long ull;
     const u32 sh = (h & 1u) << 4;
     u32* word = cells + (h >> 1);
     const u32 old = atomicAdd(word, (u32)d << sh);
-    const i64 t = (i64)((old >> sh) & 0xFFFFu) + d;
-    if ((u64)t >= 0x10000ull) {  // rare: the cell left [0, 2^16)
+    if (((old >> sh) & 0xFFFFu) + (u32)d > 0xFFFFu) {  // rare: the cell left [0, 2^16)
+        const i64 t = (i64)((old >> sh) & 0xFFFFu) + d;
         const i64 w = t >> 16;
-        atomicAdd(reinterpret_cast<ull*>(wraps_cta + h), (ull)w);
+        atomicAdd(reinterpret_cast<ull*>(slot_sum + h), (ull)(w << 16));
         if (sh == 0) {  // w also entered the high cell (slot h + 1): take it back
             const i64 w1 = ((i64)(old >> 16) + w) >> 16;
             const u32 old2 = atomicAdd(word, (u32)(-(i32)w) << 16);
             const i64 w2 = ((i64)(old2 >> 16) - w) >> 16;
-            if (w1 + w2) atomicAdd(reinterpret_cast<ull*>(wraps_cta + h + 1), (ull)(w1 + w2));
+            if (w1 + w2) atomicAdd(reinterpret_cast<ull*>(slot_sum + h + 1), (ull)((w1 + w2) << 16));
         }
     }
 }
@@ -478,7 +482,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     cs_hot_kernel(const SketchParams sp, const KeyT* __restrict__ keys, const void* __restrict__ w, uint64_t n,
                   i64* __restrict__ table, const KeyT* __restrict__ layout, u64* __restrict__ slot_sum,
                   const u32* __restrict__ hot_sum, uint32_t sample, const MissBuf<KeyT> mb, bool vec_ok,
-                  u64* __restrict__ wraps, const u32* __restrict__ priv_go) {
+                  const u32* __restrict__ priv_go) {
     if (priv_go && *priv_go == 0) return;  // cs_private_kernel took this stream
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
@@ -492,7 +496,6 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
     static_assert(S % 2 == 0, "two cells per word");
     u32* cells = reinterpret_cast<u32*>(hk + S);  // S 16-bit cells
-    u64* hi = wraps + (uint64_t)blockIdx.x * S;   // this CTA's wrap counters (HBM, zeroed below by the CTA)
     QEnt<KeyT>* q = reinterpret_cast<QEnt<KeyT>*>(cells + S / 2);
     __shared__ u32 s_next;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -522,10 +525,6 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     // of all CTAs can be merged per slot before the keys are hashed
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) hk[s] = layout[s];
     for (uint32_t s = threadIdx.x; s < S / 2; s += kHotThreads) cells[s] = 0x80008000u;
-    // the CTA's wrap counters: zeroed here, by the CTA that uses them (only calls
-    // that run this kernel pay for it; the barrier orders the stores before the
-    // CTA's atomics on them)
-    for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) hi[s] = 0;
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
 
@@ -542,7 +541,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         const KeyT c1 = hk[h1], c2 = hk[h2];
         const u32 h = c1 == key ? h1 : h2;
         const bool hit = valid && (c1 == key || c2 == key);  // empty slots hold foreign keys
-        if (hit) hot_accumulate(cells, hi, h, d);
+        if (hit) hot_accumulate(cells, slot_sum, h, d);
         const bool miss = valid && !hit;
         const unsigned m = __ballot_sync(kFull, miss);
         if (miss) {
@@ -649,8 +648,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     // u64 adds commute); hh_merge_kernel hashes each hot key once
     unsigned merged = 0;
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
-        const u64 v = (hi[s] << 16) + ((cells[s >> 1] >> ((s & 1) << 4)) & 0xFFFFu) -
-                      0x8000ull;  // 0 in empty (foreign-key) slots
+        const u64 v = ((cells[s >> 1] >> ((s & 1) << 4)) & 0xFFFFu) - 0x8000ull;  // 0 in empty (foreign-key) slots
         if (v) {
             red_add_u64(slot_sum + s, v);
             ++merged;
@@ -1355,14 +1353,14 @@ struct HotPlan {
     uint32_t chunks = 0;       // (pass 4, pass 5) round trips
     uint64_t chunk_items = 0;  // items per round trip
     uint64_t cap_m = 0;        // miss-buffer capacity
-    size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, wraps_bytes = 0, sum_bytes = 0, hot_bytes = 0,
+    size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, sum_bytes = 0, hot_bytes = 0,
            layout_bytes = 0, mk_bytes = 0, md_bytes = 0, bin_bytes = 0;
     bool rows_mode = false;  // STRAT_ROWS: misses to the buffer, then the row passes
     size_t rows_bytes = 0;   // row passes' per-CTA tables
     // tc .. slot sums are contiguous and zeroed per call
     size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes + sum_bytes; }
     size_t total() const {
-        return tk_bytes + zero_bytes() + wraps_bytes + hot_bytes + layout_bytes + mk_bytes + md_bytes + bin_bytes +
+        return tk_bytes + zero_bytes() + hot_bytes + layout_bytes + mk_bytes + md_bytes + bin_bytes +
                rows_bytes;
     }
 };
@@ -1407,7 +1405,6 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     P.tc_bytes = (size_t)P.slots * 4;
     P.misc = 256 * 4 + 64;  // hist[256], hot_count, hot_sum, miss count (u64), go words, class-1 count
     P.gcnt_bytes = align256((size_t)P.chunks * g.nb * 8 + 8);
-    P.wraps_bytes = align256((size_t)sm_count() * G::kSlots * 8);
     P.sum_bytes = align256((size_t)G::kSlots * 8);
     P.layout_bytes = align256((size_t)G::kSlots * sizeof(KeyT));
     P.hot_bytes = align256((size_t)G::kCap * (2 * sizeof(KeyT) + 4));  // hot list, counts, sorted keys
@@ -1439,11 +1436,9 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     u32* hot_sum = hot_count + 1;
     unsigned long long* mcount = reinterpret_cast<unsigned long long*>(hot_count + 2);
     g.gcnt = reinterpret_cast<unsigned long long*>(ws + P.tk_bytes + P.tc_bytes + P.misc);
-    // zeroed per call: tc | misc | gcnt | slot sums; then the wrap counters (zeroed
-    // by cs_hot_kernel's CTAs themselves)
+    // zeroed per call: tc | misc | gcnt | slot sums
     u64* slot_sum = reinterpret_cast<u64*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes);
-    u64* wraps = reinterpret_cast<u64*>(ws + P.tk_bytes + P.zero_bytes());
-    unsigned char* p = ws + P.tk_bytes + P.zero_bytes() + P.wraps_bytes;
+    unsigned char* p = ws + P.tk_bytes + P.zero_bytes();
     KeyT* hot = reinterpret_cast<KeyT*>(p);
     u32* hot_cnt = reinterpret_cast<u32*>(hot + G::kCap);
     p += P.hot_bytes;
@@ -1494,7 +1489,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     }
     if (!priv) ktimer_mark(s, true);
     fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, layout, slot_sum, hot_sum,
-                                                          binned ? P.m : 0, mb, vec_ok, wraps,
+                                                          binned ? P.m : 0, mb, vec_ok,
                                                           priv ? go : nullptr);
     if (!priv) ktimer_mark(s, false);
     hh_merge_kernel<MODE, K, SPL, KeyT><<<(G::kSlots + 255) / 256, 256, 0, s>>>(sp, layout, slot_sum, table);
@@ -1610,9 +1605,9 @@ cudaError_t launch_mode(const SketchParams& sp, const void* keys, const void* w,
 }
 
 // Keep the default stream-ordered pool's memory between calls: the hot path
-// allocates its workspace per call with cudaMallocAsync (sample tables, the
-// per-CTA wrap counters -- sms x slots x 8 B, 42 MB for u32 keys -- and, for
-// the binned strategy, the bins; config 4's shape: 148 x 128 KiB byte tables).
+// allocates its workspace per call with cudaMallocAsync (sample tables, hot
+// list and layout, and for the binned / rows strategies the miss buffer, bins or
+// row tables; config 4's shape: 148 x 128 KiB byte tables).
 void retain_pool() {
     static bool done[64] = {false};
     const int dev = device_id();

@@ -88,6 +88,13 @@ int mb200_hash61(const void* d_keys, int key_width, uint64_t n, unsigned b, cons
 int mb200_hash89(const uint64_t* d_keys, uint64_t n, const uint64_t* coeffs_lo,
                  const uint64_t* coeffs_hi, unsigned k, unsigned key_bits, uint64_t* d_out_lo,
                  uint64_t* d_out_hi, void* stream);
+/* Generic Horner for 62 <= b <= 127 (polyhash.cpp:78-88: UWide products,
+ * mersenne_reduce_partial field.hpp:66-73, branch-free finish), u64 keys in
+ * [0, 2^key_bits) (key_bits <= b - 1 for b <= 64); coefficients as (lo, hi)
+ * 64-bit halves, lowest first; outputs split into low and high 64 bits. */
+int mb200_hash_wide(const uint64_t* d_keys, uint64_t n, unsigned b, const uint64_t* coeffs_lo,
+                    const uint64_t* coeffs_hi, unsigned k, unsigned key_bits, uint64_t* d_out_lo,
+                    uint64_t* d_out_hi, void* stream);
 
 /* ------------------------------------------------------------ division --- */
 /* K6 -- Alg 4 + Alg 5 for p = 2^b - c (2 <= b <= 64, 1 <= c < 2^(b-1)):

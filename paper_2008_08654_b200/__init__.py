@@ -135,6 +135,22 @@ def hash89(keys, coeffs: Sequence[int], key_bits: int = 64, out_lo=None, out_hi=
     return out_lo, out_hi
 
 
+def hash_wide(keys, b: int, coeffs: Sequence[int], key_bits: int = 64, out_lo=None, out_hi=None, stream=None):
+    """Alg 1 mod 2^b - 1 for 62 <= b <= 127 (the reference's generic path) over u64
+    device keys; returns (low 64 bits, high bits)."""
+    torch = _torch()
+    n = keys.numel()
+    if out_lo is None:
+        out_lo = torch.empty(n, dtype=torch.int64, device=keys.device)
+    if out_hi is None:
+        out_hi = torch.empty(n, dtype=torch.int64, device=keys.device)
+    lo = np.array([int(a) & MASK64 for a in coeffs], np.uint64)
+    hi = np.array([int(a) >> 64 for a in coeffs], np.uint64)
+    check(lib.mb200_hash_wide(_dptr(keys), n, b, _p(lo), _p(hi), len(coeffs), key_bits, _dptr(out_lo),
+                              _dptr(out_hi), _stream(stream)))
+    return out_lo, out_hi
+
+
 def pm_divmod(v, b: int, c: int, m_iters: int = 0, q=None, r=None, overflow=None, stream=None):
     """Alg 4 + Alg 5 by p = 2^b - c over u128 inputs stored as an (n, 2) int64 tensor of
     (lo, hi) words; returns (q, r) int64 tensors holding u64 values."""

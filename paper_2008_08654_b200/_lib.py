@@ -82,6 +82,7 @@ SIGNATURES = [
     ("mb200_row_seeds", I, [u64, U, P]),
     ("mb200_hash61", I, [P, I, u64, U, P, U, U, P, P]),
     ("mb200_hash89", I, [P, u64, P, P, U, U, P, P, P]),
+    ("mb200_hash_wide", I, [P, u64, U, P, P, U, U, P, P, P]),
     ("mb200_pm_divmod", I, [P, u64, U, u64, U, P, P, P, P]),
     ("mb200_pm_div", I, [P, u64, U, u64, U, P, P, P]),
     ("mb200_pm_mod", I, [P, P, u64, U, u64, P, P]),

@@ -70,7 +70,6 @@ int build_sketch_params(const mb200_sketch_desc* d, SketchParams& sp) {
     if (d->k == 0) return fail(MB200_INVALID_ARGUMENT, "independence degree must be at least 1");
     if (d->k > (unsigned)kMaxK) return fail(MB200_UNSUPPORTED, "GPU path supports independence <= 16");
     if (d->b < 2 || d->b > 127) return fail(MB200_INVALID_ARGUMENT, "exponent must be in [2, 127]");
-    if (d->b > 61 && d->b != 89) return fail(MB200_UNSUPPORTED, "GPU path supports b <= 61 and b == 89");
     if (d->width < 2) return fail(MB200_INVALID_ARGUMENT, "width must be at least 2");  // sketch.cpp:99
     const bool pow2 = (d->width & (d->width - 1)) == 0;
     switch (d->splitter) {
@@ -84,7 +83,6 @@ int build_sketch_params(const mb200_sketch_desc* d, SketchParams& sp) {
         case MB200_SPLIT_MERSENNE_ARB:
             if (d->b < 64 && d->width > (1ull << (d->b - 1)))
                 return fail(MB200_INVALID_ARGUMENT, "width exceeds half the hash range");  // sketch.cpp:109-113
-            if (d->b > 64) return fail(MB200_UNSUPPORTED, "arbitrary-width splitters run for b <= 61 on the GPU");
             break;
         default:
             return fail(MB200_INVALID_ARGUMENT, "unknown splitter");
@@ -93,7 +91,7 @@ int build_sketch_params(const mb200_sketch_desc* d, SketchParams& sp) {
         return fail(MB200_INVALID_ARGUMENT, "sketch dimensions too large");  // sketch.cpp:116-118
     // key domain: polyhash.cpp:48-57 (p >= 2u - 1); b == 61 also admits full 64-bit keys
     if (d->key_bits > 64) return fail(MB200_UNSUPPORTED, "keys wider than 64 bits");
-    if (d->b != 61 && d->b < 64 && d->key_bits > d->b - 1)
+    if (d->b != 61 && d->b <= 64 && d->key_bits > d->b - 1)
         return fail(MB200_INVALID_ARGUMENT, "modulus too small for key domain");
     const unsigned lw = (unsigned)__builtin_ctzll(d->width);
     const unsigned families = d->splitter == MB200_SPLIT_TWO_FOR_ONE ? (d->rows + 1) / 2 : d->rows;
@@ -213,6 +211,34 @@ int mb200_hash89(const uint64_t* d_keys, uint64_t n, const uint64_t* coeffs_lo, 
     cudaError_t e = launch_hash89(d_keys, n, hp, d_out_lo, d_out_hi, s);
     if (e == cudaErrorMisalignedAddress) return fail(MB200_INVALID_ARGUMENT, "mb200_hash89 needs 16-byte aligned buffers");
     return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_hash89");
+}
+
+int mb200_hash_wide(const uint64_t* d_keys, uint64_t n, unsigned b, const uint64_t* coeffs_lo,
+                    const uint64_t* coeffs_hi, unsigned k, unsigned key_bits, uint64_t* d_out_lo, uint64_t* d_out_hi,
+                    void* stream) {
+    if (b < 62 || b > 127) return fail(MB200_INVALID_ARGUMENT, "mb200_hash_wide needs 62 <= b <= 127");
+    if (k == 0) return fail(MB200_INVALID_ARGUMENT, "independence degree must be at least 1");
+    if (k > (unsigned)kMaxK) return fail(MB200_UNSUPPORTED, "GPU path supports independence <= 16");
+    if (key_bits > 64) return fail(MB200_UNSUPPORTED, "keys wider than 64 bits");
+    if (b <= 64 && key_bits > b - 1) return fail(MB200_INVALID_ARGUMENT, "modulus too small for key domain");
+    if (!coeffs_lo || !coeffs_hi) return fail(MB200_INVALID_ARGUMENT, "null coefficients");
+    HashParams hp;
+    std::memset(&hp, 0, sizeof(hp));
+    hp.b = b;
+    hp.k = k;
+    for (unsigned i = 0; i < k; ++i) {  // coefficient < p = 2^b - 1 (polyhash.cpp:43)
+        const unsigned __int128 a = ((unsigned __int128)coeffs_hi[i] << 64) | coeffs_lo[i];
+        const unsigned __int128 p = (((unsigned __int128)1) << b) - 1;
+        if (a >= p) return fail(MB200_INVALID_ARGUMENT, "coefficient not reduced");
+        hp.lo[i] = coeffs_lo[i];
+        hp.hi[i] = coeffs_hi[i];
+    }
+    if (n == 0) return MB200_OK;
+    if (!d_keys || !d_out_lo || !d_out_hi) return fail(MB200_INVALID_ARGUMENT, "null buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (int rc = check_keys(d_keys, 64, n, key_bits, s)) return rc;
+    cudaError_t e = launch_hash_wide(d_keys, n, hp, d_out_lo, d_out_hi, s);
+    return e == cudaSuccess ? MB200_OK : cuda_fail(e, "mb200_hash_wide");
 }
 
 int mb200_pm_divmod(const uint64_t* d_v, uint64_t n, unsigned b, uint64_t c, unsigned m_iters, uint64_t* d_q,

@@ -261,6 +261,29 @@ cudaError_t launch_hash_generic(const void* keys, int key_width, uint64_t n, con
     return cudaGetLastError();
 }
 
+// 62 <= b <= 127: the generic four-limb Horner (polyhash.cpp:78-88), scalar
+// per key (no BASELINE config uses these moduli)
+__global__ void __launch_bounds__(kThreads) hash_wide_kernel(const u64* __restrict__ keys, uint64_t n,
+                                                             const HashParams hp, u64* __restrict__ out_lo,
+                                                             u64* __restrict__ out_hi) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        u64 lo, hi;
+        hash_wide(hp.lo, hp.hi, (int)hp.k, hp.b, keys[i], lo, hi);
+        out_lo[i] = lo;
+        out_hi[i] = hi;
+    }
+}
+
+cudaError_t launch_hash_wide(const uint64_t* keys, uint64_t n, const HashParams& hp, uint64_t* out_lo,
+                             uint64_t* out_hi, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    uint64_t grid = (n + kThreads - 1) / kThreads;
+    if (grid > (uint64_t)sm_count() * 8) grid = (uint64_t)sm_count() * 8;
+    hash_wide_kernel<<<(unsigned)grid, kThreads, 0, s>>>(keys, n, hp, out_lo, out_hi);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_hash89(const uint64_t* keys, uint64_t n, const HashParams& hp, uint64_t* out_lo,
                           uint64_t* out_hi, cudaStream_t s) {
     if (n == 0) return cudaSuccess;

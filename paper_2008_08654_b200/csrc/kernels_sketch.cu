@@ -333,12 +333,15 @@ __global__ void cs_point_query_kernel(const SketchParams sp, const i64* __restri
             const uint32_t subs = sp.splitter == SPLIT_TWO_FOR_ONE ? 2 : 1;
             u64 hlo = 0, hhi = 0;
             if (MODE == M89) hash89<0>(sp, f, x, hlo, hhi);
+            else if (MODE == MWIDE) hash_wide_f(sp, f, x, hlo, hhi);
             else hlo = hash_small<MODE, 0>(sp, f, x);
             for (uint32_t s = 0; s < subs; ++s) {
                 const uint32_t row = subs * f + s;
                 if (row >= sp.rows) break;
                 bool neg;
-                const u64 idx = MODE == M89 ? split89(sp, hlo, hhi, s, neg) : split_small(sp, hlo, s, neg);
+                const u64 idx = MODE == M89     ? split89(sp, hlo, hhi, s, neg)
+                                : MODE == MWIDE ? split_wide(sp, hlo, hhi, s, neg)
+                                                : split_small(sp, hlo, s, neg);
                 const i64 c = table[(u64)row * sp.width + idx];
                 est[ne++] = neg ? (i64)(0ull - (u64)c) : c;
             }
@@ -427,7 +430,8 @@ cudaError_t launch_w(const SketchParams& sp, const void* keys, const void* w, ui
     if (cells * 8 <= 64 * 1024) return launch_strat<MODE, K, KeyT, WK, SMEM64>(sp, keys, w, n, table, s, false);
     // large batches: heavy-hitter accumulation in shared memory (|delta| < 2^31 for the
     // exact two-word accumulator), everything else straight to L2
-    if (WK != W_I64 && n >= (1ull << 22)) return launch_cs_hot(sp, keys, (int)(sizeof(KeyT) * 8), w, WK, n, table, s);
+    if (MODE != MWIDE && WK != W_I64 && n >= (1ull << 22))
+        return launch_cs_hot(sp, keys, (int)(sizeof(KeyT) * 8), w, WK, n, table, s);
     return launch_strat<MODE, K, KeyT, WK, GLOBAL>(sp, keys, w, n, table, s, WK != W_NONE);
 }
 
@@ -454,6 +458,13 @@ cudaError_t launch_mode(const SketchParams& sp, const void* keys, const void* w,
 cudaError_t launch_cs_update(const SketchParams& sp, const void* keys, int key_width, const void* w,
                              int w_kind, uint64_t n, int64_t* table, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    // 62 <= b <= 127 (and b = 89 with the arbitrary-width splitters): the generic
+    // four-limb Horner and 128-bit splitters
+    if ((sp.b > 61 && sp.b != 89) ||
+        (sp.b == 89 && sp.splitter != SPLIT_POW2 && sp.splitter != SPLIT_TWO_FOR_ONE)) {
+        if (key_width == 32) return launch_mode<MWIDE, u32>(sp, keys, w, w_kind, n, table, s);
+        return launch_mode<MWIDE, u64>(sp, keys, w, w_kind, n, table, s);
+    }
     if (sp.b == 89) {
         if (key_width == 32) return launch_mode<M89, u32>(sp, keys, w, w_kind, n, table, s);
         return launch_mode<M89, u64>(sp, keys, w, w_kind, n, table, s);
@@ -497,7 +508,11 @@ cudaError_t launch_cs_point_query(const SketchParams& sp, const int64_t* table, 
     uint64_t grid = (n + 255) / 256;
     if (grid > (uint64_t)sm_count() * 8) grid = (uint64_t)sm_count() * 8;
     const unsigned g = (unsigned)grid;
-    if (sp.b == 89) {
+    if ((sp.b > 61 && sp.b != 89) ||
+        (sp.b == 89 && sp.splitter != SPLIT_POW2 && sp.splitter != SPLIT_TWO_FOR_ONE)) {
+        if (key_width == 32) cs_point_query_kernel<MWIDE, u32><<<g, 256, 0, s>>>(sp, table, (const u32*)keys, n, out);
+        else cs_point_query_kernel<MWIDE, u64><<<g, 256, 0, s>>>(sp, table, (const u64*)keys, n, out);
+    } else if (sp.b == 89) {
         if (key_width == 32) cs_point_query_kernel<M89, u32><<<g, 256, 0, s>>>(sp, table, (const u32*)keys, n, out);
         else cs_point_query_kernel<M89, u64><<<g, 256, 0, s>>>(sp, table, (const u64*)keys, n, out);
     } else if (sp.b == 61) {

@@ -250,6 +250,104 @@ __device__ __forceinline__ void h89_finish(u32& y0, u32& y1, u32& y2) {
 }
 
 // ---------------------------------------------------------------------------
+// Generic Mersenne p = 2^b - 1 for 62 <= b <= 127 (polyhash.cpp:78-88 on
+// UWide, field.hpp:66-73): y < 2p in four 32-bit limbs, x < 2^64 (two limbs),
+// a < p.  On the key domain x < 2^(b-1) the reference's invariant y < 2p
+// holds after every partial fold.  t = y x + a < 2^192 as six words, each row
+// term a product of two words plus at most two words (<= 2^64 - 1); then
+// (t & p) + (t >> b) with b = 32 Q + R: Q = b / 32 is a template parameter (the
+// word indices are static), R runtime.  t >> b < 2^65 fits three words.
+// Performance is not the point here (no BASELINE config uses these moduli;
+// b = 89's config runs h89_step / the config-4 kernel): exactness is.
+template <int Q>
+__device__ __forceinline__ void hw_step(u32 (&y)[4], u32 x0, u32 x1, const u32 (&a)[4], u32 R) {
+    u32 w[7];
+    u64 r = (u64)y[0] * x0 + a[0];
+    w[0] = (u32)r;
+    u32 c0, c1, c2, c3;  // row x0, words 1..4
+    r = (u64)y[1] * x0 + (r >> 32) + a[1];
+    c0 = (u32)r;
+    r = (u64)y[2] * x0 + (r >> 32) + a[2];
+    c1 = (u32)r;
+    r = (u64)y[3] * x0 + (r >> 32) + a[3];
+    c2 = (u32)r;
+    c3 = (u32)(r >> 32);
+    u64 q = (u64)y[0] * x1 + c0;
+    w[1] = (u32)q;
+    q = (u64)y[1] * x1 + (q >> 32) + c1;
+    w[2] = (u32)q;
+    q = (u64)y[2] * x1 + (q >> 32) + c2;
+    w[3] = (u32)q;
+    q = (u64)y[3] * x1 + (q >> 32) + c3;
+    w[4] = (u32)q;
+    w[5] = (u32)(q >> 32);
+    w[6] = 0;
+    const u32 mask = R ? (0xffffffffu >> (32 - R)) : 0u;
+    u32 L[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) L[j] = j < Q ? w[j] : (j == Q ? w[j] & mask : 0u);
+    u32 H[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) H[j] = __funnelshift_r(w[Q + j], w[Q + j + 1], R);
+    u64 acc = (u64)L[0] + H[0];
+    y[0] = (u32)acc;
+    acc = (u64)L[1] + H[1] + (acc >> 32);
+    y[1] = (u32)acc;
+    acc = (u64)L[2] + H[2] + (acc >> 32);
+    y[2] = (u32)acc;
+    y[3] = L[3] + (u32)(acc >> 32);
+}
+
+// The reference's branch-free finish for y < 2p: z = (y + 1) >> b; (y + z) & p
+template <int Q>
+__device__ __forceinline__ void hw_finish(u32 (&y)[4], u32 R) {
+    u64 acc = (u64)y[0] + 1;
+    u32 t[4];
+    t[0] = (u32)acc;
+#pragma unroll
+    for (int j = 1; j < 4; ++j) {
+        acc = (u64)y[j] + (acc >> 32);
+        t[j] = (u32)acc;
+    }
+    const u32 z = (t[Q] >> R) & 1u;  // y + 1 < 2^(b+1): bit b is the whole quotient
+    acc = (u64)y[0] + z;
+    y[0] = (u32)acc;
+#pragma unroll
+    for (int j = 1; j < 4; ++j) {
+        acc = (u64)y[j] + (acc >> 32);
+        y[j] = (u32)acc;
+    }
+    const u32 mask = R ? (0xffffffffu >> (32 - R)) : 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) y[j] = j < Q ? y[j] : (j == Q ? y[j] & mask : 0u);
+}
+
+template <int Q>
+__device__ __forceinline__ void hash_wide_q(const u64* clo, const u64* chi, int k, u32 R, u64 x, u64& lo, u64& hi) {
+    u32 y[4] = {lo32(clo[k - 1]), hi32(clo[k - 1]), lo32(chi[k - 1]), hi32(chi[k - 1])};
+    const u32 x0 = lo32(x), x1 = hi32(x);
+#pragma unroll 1
+    for (int i = k - 2; i >= 0; --i) {
+        const u32 a[4] = {lo32(clo[i]), hi32(clo[i]), lo32(chi[i]), hi32(chi[i])};
+        hw_step<Q>(y, x0, x1, a, R);
+    }
+    hw_finish<Q>(y, R);
+    lo = ((u64)y[1] << 32) | y[0];
+    hi = ((u64)y[3] << 32) | y[2];
+}
+
+// h = (sum_i a_i x^i) mod (2^b - 1) as (low 64 bits, high bits), 62 <= b <= 127;
+// coefficients lowest first as (lo, hi) 64-bit halves
+__device__ __forceinline__ void hash_wide(const u64* clo, const u64* chi, int k, u32 b, u64 x, u64& lo, u64& hi) {
+    const u32 R = b & 31u;
+    switch (b >> 5) {
+        case 1: hash_wide_q<1>(clo, chi, k, R, x, lo, hi); break;
+        case 2: hash_wide_q<2>(clo, chi, k, R, x, lo, hi); break;
+        default: hash_wide_q<3>(clo, chi, k, R, x, lo, hi); break;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // SplitMix64 (prng.hpp:10-38) in counter form: the i-th next() of
 // SplitMix64(seed) is mix(seed + (i+1) * golden).
 constexpr u64 kGolden = 0x9E3779B97F4A7C15ull;

@@ -44,6 +44,9 @@ cudaError_t launch_hash_generic(const void* keys, int key_width, uint64_t n, con
                                 uint64_t* out, cudaStream_t s);
 cudaError_t launch_hash89(const uint64_t* keys, uint64_t n, const HashParams& hp, uint64_t* out_lo,
                           uint64_t* out_hi, cudaStream_t s);
+// 62 <= b <= 127: generic four-limb Horner, outputs low 64 / high bits
+cudaError_t launch_hash_wide(const uint64_t* keys, uint64_t n, const HashParams& hp, uint64_t* out_lo,
+                             uint64_t* out_hi, cudaStream_t s);
 // domain validation: counts keys >= 2^key_bits into *d_count (pre-zeroed)
 cudaError_t launch_count_out_of_domain(const void* keys, int key_width, uint64_t n, uint32_t key_bits,
                                        unsigned long long* d_count, cudaStream_t s);

@@ -16,7 +16,7 @@ namespace sk {
 constexpr int kSlots = 4;  // items per lane per warp-iteration (loads in flight)
 constexpr unsigned kFull = 0xffffffffu;
 
-enum Mode { M61_K32 = 0, M61_K64 = 1, M89 = 2, MGEN = 3 };
+enum Mode { M61_K32 = 0, M61_K64 = 1, M89 = 2, MGEN = 3, MWIDE = 4 };  // MWIDE: 62 <= b <= 127
 enum Strat { SMEM32 = 0, SMEM64 = 1, GLOBAL = 2, SMEM_LOHI = 3 };
 constexpr uint32_t kLohiCells = 8192;  // SMEM_LOHI table capacity (2 x 32 KiB)
 
@@ -125,6 +125,43 @@ __device__ __forceinline__ u64 split89(const SketchParams& sp, u64 lo, u64 hi, u
     return (lo >> (sp.lw * sub)) & (sp.width - 1);
 }
 
+// hash of family f for 62 <= b <= 127 (any splitter), as (lo 64 bits, hi bits)
+__device__ __forceinline__ void hash_wide_f(const SketchParams& sp, uint32_t f, u64 x, u64& lo, u64& hi) {
+    hash_wide(sp.lo + (size_t)f * sp.k, sp.hi + (size_t)f * sp.k, (int)sp.k, sp.b, x, lo, hi);
+}
+
+// Every splitter on a 128-bit hash h < 2^b, 62 <= b <= 127 (sketch.cpp:13-34;
+// map_pow2 bucketing.cpp:61-66 = (j r) >> (b - 1)); index < width < 2^34.
+__device__ __forceinline__ u64 split_wide(const SketchParams& sp, u64 lo, u64 hi, uint32_t sub, bool& neg) {
+    const u32 b = sp.b;
+    auto bit = [&](u64 l, u64 h, u32 pos) -> bool { return pos >= 64 ? (h >> (pos - 64)) & 1 : (l >> pos) & 1; };
+    if (sp.splitter == SPLIT_POW2) {  // index = low l bits, sign = 1 - 2 * bit b-1
+        neg = bit(lo, hi, b - 1);
+        return lo & (sp.width - 1);
+    }
+    if (sp.splitter == SPLIT_TWO_FOR_ONE) {  // bits [l sub, l sub + l) (2 l <= 64), sign bit b-1-sub
+        neg = bit(lo, hi, b - 1 - sub);
+        return (lo >> (sp.lw * sub)) & (sp.width - 1);
+    }
+    u64 l2 = lo, h2 = hi;
+    if (sp.splitter == SPLIT_MERSENNE_ARB) {  // split_arb_uniform(h + 1, ...), h < p
+        l2 = lo + 1;
+        h2 = hi + (l2 == 0);
+    }
+    const u32 s = b - 1;        // >= 61
+    neg = !bit(l2, h2, s);      // sign = 2 a - 1
+    const u64 jl = s >= 64 ? l2 : l2 & ((1ull << s) - 1);
+    const u64 jh = s > 64 ? h2 & ((1ull << (s - 64)) - 1) : 0;
+    const u64 r = sp.width;     // < 2^34
+    const u64 p1l = jl * r, p1h = __umul64hi(jl, r);
+    const u64 p2l = jh * r, p2h = __umul64hi(jh, r);
+    const u64 mid = p1h + p2l;
+    const u64 top = p2h + (mid < p1h);
+    if (s < 64) return (p1l >> s) | (mid << (64 - s));
+    if (s == 64) return mid;
+    return (mid >> (s - 64)) | (top << (128 - s));
+}
+
 template <int WK>
 __device__ __forceinline__ i64 load_weight(const void* w, uint64_t i) {
     if (WK == W_NONE) return 1;
@@ -158,17 +195,18 @@ template <int MODE, int K, int STRAT>
 __device__ __forceinline__ void process_item(const SketchParams& sp, u64 x, i64 delta, void* smem,
                                              i64* table) {
     const u64 d = (u64)delta;
-    if (MODE == M89) {
+    if (MODE == M89 || MODE == MWIDE) {
         const uint32_t subs = sp.splitter == SPLIT_TWO_FOR_ONE ? 2 : 1;
 #pragma unroll 1
         for (uint32_t f = 0; f < sp.families; ++f) {
             u64 hlo, hhi;
-            hash89<K>(sp, f, x, hlo, hhi);
+            if (MODE == M89) hash89<K>(sp, f, x, hlo, hhi);
+            else hash_wide_f(sp, f, x, hlo, hhi);
             for (uint32_t s = 0; s < subs; ++s) {
                 const uint32_t row = subs * f + s;
                 if (row >= sp.rows) break;
                 bool neg;
-                const u64 idx = split89(sp, hlo, hhi, s, neg);
+                const u64 idx = MODE == M89 ? split89(sp, hlo, hhi, s, neg) : split_wide(sp, hlo, hhi, s, neg);
                 table_add<STRAT>(smem, table, (u64)row * sp.width + idx, neg ? (0ull - d) : d);
             }
         }
@@ -203,7 +241,7 @@ __device__ __forceinline__ void process_item(const SketchParams& sp, u64 x, i64 
 template <int MODE, int K, int STRAT, int U, int FAM = 0, typename KeyT>
 __device__ __forceinline__ void process_items(const SketchParams& sp, const KeyT (&x)[U], const i64 (&delta)[U],
                                               unsigned valid, void* smem, i64* table) {
-    if (FAM == 1 && MODE != M89) {
+    if (FAM == 1 && MODE != M89 && MODE != MWIDE) {
         // one family, Pow2 splitter (the caller checked): no loops, no splitter switch
         u64 h[U];
 #pragma unroll
@@ -218,13 +256,16 @@ __device__ __forceinline__ void process_items(const SketchParams& sp, const KeyT
         }
         return;
     }
-    if (MODE == M89) {
+    if (MODE == M89 || MODE == MWIDE) {
         const uint32_t subs = sp.splitter == SPLIT_TWO_FOR_ONE ? 2 : 1;
 #pragma unroll 1
         for (uint32_t f = 0; f < sp.families; ++f) {
             u64 hlo[U], hhi[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) hash89<K>(sp, f, (u64)x[u], hlo[u], hhi[u]);
+            for (int u = 0; u < U; ++u) {
+                if (MODE == M89) hash89<K>(sp, f, (u64)x[u], hlo[u], hhi[u]);
+                else hash_wide_f(sp, f, (u64)x[u], hlo[u], hhi[u]);
+            }
             for (uint32_t s = 0; s < subs; ++s) {
                 const uint32_t row = subs * f + s;
                 if (row >= sp.rows) break;
@@ -232,7 +273,8 @@ __device__ __forceinline__ void process_items(const SketchParams& sp, const KeyT
                 for (int u = 0; u < U; ++u) {
                     if (!((valid >> u) & 1)) continue;
                     bool neg;
-                    const u64 idx = split89(sp, hlo[u], hhi[u], s, neg);
+                    const u64 idx = MODE == M89 ? split89(sp, hlo[u], hhi[u], s, neg)
+                                                : split_wide(sp, hlo[u], hhi[u], s, neg);
                     const u64 d = (u64)delta[u];
                     table_add<STRAT>(smem, table, (u64)row * sp.width + idx, neg ? (0ull - d) : d);
                 }

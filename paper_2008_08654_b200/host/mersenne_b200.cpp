@@ -245,8 +245,11 @@ void PolyHashFamily::hash_device(const void* d_keys, int key_width, u64 n, u64* 
         if (key_width != 64) throw std::invalid_argument("the 89-bit path takes u64 keys");
         if (!d_out_hi) throw std::invalid_argument("b > 64 needs a high-word output");
         throw_status(mb200_hash89((const u64*)d_keys, n, lo.data(), hi.data(), k, kb, d_out_lo, d_out_hi, stream));
-    } else {
-        throw std::invalid_argument("GPU path supports b <= 61 and b == 89");
+    } else {  // 62 <= b <= 127: the generic four-limb path
+        if (key_width != 64) throw std::invalid_argument("the b > 61 paths take u64 keys");
+        if (!d_out_hi) throw std::invalid_argument("b > 64 needs a high-word output");
+        throw_status(
+            mb200_hash_wide((const u64*)d_keys, n, b, lo.data(), hi.data(), k, kb, d_out_lo, d_out_hi, stream));
     }
 }
 

@@ -1072,3 +1072,78 @@ def test_c4_kernel_unaligned_and_random(cuda, mb, orc):
     assert (got == exp).all()
     got, exp, _ = _c4_run(mb, orc, fam, d[1:])
     assert (got == exp).all()
+
+
+# --- 62 <= b <= 127: the generic four-limb path (polyhash.cpp:78-88) ---
+
+WIDE_BS = [62, 63, 64, 65, 89, 96, 100, 107, 127]
+
+
+@pytest.mark.parametrize("b", WIDE_BS)
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+def test_hash_wide_random(cuda, mb, orc, b, k):
+    """mb200_hash_wide (any 62 <= b <= 127, including composite exponents) against
+    the oracle's generic Horner, which is pinned to the reference at b <= 127."""
+    rng = np.random.default_rng(b * 31 + k)
+    kb = min(b - 1, 64)
+    n = 40000
+    keys = rng.integers(0, 1 << 64, n, dtype=np.uint64)
+    if kb < 64:
+        keys &= np.uint64((1 << kb) - 1)
+    keys[:3] = [0, (1 << kb) - 1, 1]
+    c = orc.coeffs(b, k, 1000 + b + k)
+    lo, hi = mb.hash_wide(dev(keys), b, c, key_bits=kb)
+    el, eh, _ = orc.hash_batch(b, c, keys, kb)
+    assert (host_u64(lo) == el).all() and (host_u64(hi) == eh).all()
+
+
+def test_hash_wide_extreme_coefficients(cuda, mb, orc):
+    """Coefficients at p - 1 and 0, keys at the domain edge: every partial fold and the
+    finish's y >= p branch (h = y - p) get exercised."""
+    for b in (64, 107, 127):
+        p = (1 << b) - 1
+        kb = min(b - 1, 64)
+        keys = np.array([0, 1, 2, (1 << kb) - 1, (1 << kb) - 2, 12345], np.uint64)
+        for c in ([p - 1] * 4, [0, 0, 0, p - 1], [p - 1, 0, 0, 1], [1, p - 1, 1, p - 1]):
+            lo, hi = mb.hash_wide(dev(keys), b, c, key_bits=kb)
+            el, eh, _ = orc.hash_batch(b, c, keys, kb)
+            assert (host_u64(lo) == el).all() and (host_u64(hi) == eh).all(), (b, c)
+
+
+WIDE_SKETCH = [
+    # rows, width, b, splitter, weights
+    (3, 1024, 107, 0, np.int32),
+    (4, 1000, 107, 1, np.int64),
+    (2, 777, 127, 2, np.int32),
+    (5, 4096, 127, 3, None),
+    (2, 65536, 64, 0, np.int32),
+    (3, 3000, 89, 1, np.int32),      # b = 89 with an arbitrary-width splitter
+    (2, 1 << 20, 89, 2, None),       # ... and a table larger than shared memory (L2 path)
+    (6, 8192, 62, 3, np.int64),
+]
+
+
+@pytest.mark.parametrize("case", WIDE_SKETCH, ids=[f"b{c[2]}s{c[3]}w{c[1]}" for c in WIDE_SKETCH])
+def test_sketch_wide_moduli(cuda, mb, orc, case):
+    """Count Sketch updates and point queries for 62 <= b <= 127 (and b = 89 with the
+    arbitrary-width splitters) equal the oracle's per-item process, every splitter."""
+    import torch
+
+    rows, width, b, sp, wdt = case
+    kb = min(b - 1, 64)
+    spec, fams = make_spec(mb, orc, rows, width, b, kb, sp, 0x51DE + b)
+    rng = np.random.default_rng(b + sp)
+    n = 300_000
+    keys = rng.integers(0, 1 << 64, n, dtype=np.uint64)
+    if kb < 64:
+        keys &= np.uint64((1 << kb) - 1)
+    keys[: n // 3] = keys[n // 3: 2 * (n // 3)] % np.uint64(777)  # repeats
+    w = None if wdt is None else rng.integers(-(2**31), 2**31, n).astype(wdt)
+    cnt = torch.zeros(rows * width, dtype=torch.int64, device="cuda")
+    mb.cs_update(spec, dev(keys), cnt, None if w is None else dev(w))
+    exp = orc.cs_process(rows, width, b, fams, kb, sp, keys, w)
+    assert (cnt.cpu().numpy() == exp).all()
+    q = keys[:2000]
+    got = mb.cs_point_query(spec, cnt, dev(q)).cpu().numpy()
+    want = orc.point_query(rows, width, b, fams, kb, sp, exp, q)
+    assert (got == want).all()

@@ -259,12 +259,14 @@ def test_cli_input_file_equals_stdin(cli, tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("splitter,rows,key_bits", [("pow2", 5, 32), ("uniform", 3, 60), ("mersenne", 2, 20)])
-def test_cli_long_stream_matches_reference(cli, ref, tmp_path, splitter, rows, key_bits):
+@pytest.mark.parametrize("splitter,rows,key_bits,b", [("pow2", 5, 32, 61), ("uniform", 3, 60, 61),
+                                                      ("mersenne", 2, 20, 61), ("pow2", 3, 64, 127),
+                                                      ("uniform", 2, 64, 89)])
+def test_cli_long_stream_matches_reference(cli, ref, tmp_path, splitter, rows, key_bits, b):
     """A multi-block stream (> 32 MiB of text) through the CLI equals the
     reference CountSketch fed the same items: F2 (median), point queries and the
     saved MCSK1 bytes."""
-    rng = np.random.default_rng(rows)
+    rng = np.random.default_rng(rows + b)
     n = 2_500_000
     keys = rng.integers(0, 1 << key_bits, n, dtype=np.uint64)
     keys[: n // 4] = keys[n // 2: n // 2 + n // 4] % 1000  # repeats
@@ -276,12 +278,12 @@ def test_cli_long_stream_matches_reference(cli, ref, tmp_path, splitter, rows, k
     path = str(tmp_path / "s.bin")
     q = keys[:5]
     j = out_json(run(["sketch", "--width", str(width), "--rows", str(rows), "--seed", "77", "--key-bits",
-                      str(key_bits), "--splitter", splitter, "--f2-median", "--save", path, "--queries",
-                      ",".join(str(x) for x in q.tolist())], data))
-    assert j["processed"] == n
-    payload = ref.serialize(rows, width, 61, key_bits, spl, 77, keys, w)
+                      str(key_bits), "--prime", f"2^{b}-1", "--splitter", splitter, "--f2-median", "--save", path,
+                      "--queries", ",".join(str(x) for x in q.tolist())], data))
+    assert j["processed"] == n and j["b"] == b
+    payload = ref.serialize(rows, width, b, key_bits, spl, 77, keys, w)
     assert open(path, "rb").read() == payload
     _, f2 = ref.resume(payload)
     assert j["f2"] == str(f2)
-    est = ref.point_query(rows, width, 61, key_bits, spl, 77, keys, w, q)
+    est = ref.point_query(rows, width, b, key_bits, spl, 77, keys, w, q)
     assert [x["estimate"] for x in j["queries"]] == est.tolist()

@@ -90,23 +90,39 @@ struct alignas(sizeof(KeyT) * 2) QEnt {
     KeyT k;
     i32 d;
 };
-// shared slot = key + a 16-bit cell, the low 16 bits of its exact sum (the
-// rarely used wrap counter lives in HBM, one u64 array per CTA); slot counts
-// need not be powers of 2 (they are even: two cells per 32-bit word)
+// u32 keys: a TAGGED slot, one 32-bit word = 14-bit cell (bits 18-31, the low
+// 14 bits of the slot's sum, 2^13-biased) | choice bit (17) | 17-bit tag.  A
+// key's two choices are the bijections pi1(K) = K c1 and pi2(K) = (K ^ K >> 15)
+// c2 of the u32 key; slot_i = floor(pi_i S / 2^32) and tag_i = pi_i mod 2^17.
+// The pi values of one slot form an interval of ceil(2^32 / S) = 80660 < 2^17
+// values, so (slot, choice, tag) identifies the key exactly, and the value
+// just below a slot's interval (mod 2^17) with choice 0 is a tag no key can
+// have there: the empty-slot marker.  The cell sits in the word's top bits, so
+// an add's carry leaves the word instead of touching the tag.  4 bytes per slot:
+// 53248 slots in 208 KiB (35840 in the 6-byte key + 16-bit cell layout before;
+// misses 10.8% -> ~9.7% on config 5).
+// u64 keys: slot = 8-byte key + a 16-bit cell (two per 32-bit word).
+// Slot counts need not be powers of 2.  The wraps of either cell go straight
+// into the slot's shared total in HBM (hot_accumulate / tag_accumulate).
 template <>
 struct HotGeom<u32> {
-    static constexpr uint32_t kSlots = 35840;  // x (4 B key + 2 B cell) = 210 KiB
-    static constexpr uint32_t kCap = 40960;    // selected candidates (the layout places ~31K)
+    static constexpr bool kTagged = true;
+    static constexpr uint32_t kSlots = 53248;  // x 4 B = 208 KiB
+    static constexpr uint32_t kCap = 61440;    // selected candidates (the layout places ~46K)
     static constexpr u32 kEmpty = 0xffffffffu;
     using Cas = unsigned;
 };
 template <>
 struct HotGeom<u64> {
+    static constexpr bool kTagged = false;
     static constexpr uint32_t kSlots = 19456;  // x (8 B key + 2 B cell) = 190 KiB
     static constexpr uint32_t kCap = 16384;
     static constexpr u64 kEmpty = ~0ull;
     using Cas = unsigned long long;
 };
+constexpr u32 kTagMask = 0x3ffffu;  // choice bit + 17-bit tag
+constexpr u32 kCellShift = 18;      // 14-bit cell in bits 18-31
+constexpr u32 kCellBias = 0x2000u;
 
 // two independent slot choices in [0, S): multiply-high range reduction of two
 // independent 32-bit mixes (any S, not only powers of two)
@@ -121,6 +137,15 @@ __device__ __forceinline__ u32 slot1(u32 key) {
 template <uint32_t S>
 __device__ __forceinline__ u32 slot2(u32 key) {
     return slot_of<S>((key ^ (key >> 15)) * 0x2C1B3C6Du);
+}
+// the tagged table's identity of key K in slot_i(K): tag_i(K) (choice bit i)
+__device__ __forceinline__ u32 tag1(u32 key) { return (key * 0x9E3779B1u) & 0x1ffffu; }
+__device__ __forceinline__ u32 tag2(u32 key) { return (((key ^ (key >> 15)) * 0x2C1B3C6Du) & 0x1ffffu) | 0x20000u; }
+// empty-slot marker of slot s: choice 0, tag = (first pi1 value of the slot) - 1 mod 2^17
+template <uint32_t S>
+__device__ __forceinline__ u32 empty_tag(u32 s) {
+    const u64 lo = (((u64)s << 32) + S - 1) / S;  // ceil(s 2^32 / S)
+    return (u32)(lo - 1) & 0x1ffffu;
 }
 template <uint32_t S>
 __device__ __forceinline__ u32 slot1(u64 key) {
@@ -357,6 +382,20 @@ __device__ __forceinline__ void hot_accumulate(u32* cells, u64* slot_sum, u32 h,
     }
 }
 
+// The tagged table's cell (bits 18-31 of the slot word, 2^13-biased): one
+// shared atomic; a cell that leaves [0, 2^14) records 2^14 floor((c + d) / 2^14)
+// into the slot's total (its carry left the word; the tag below is untouched).
+// The range test is the 32-bit compare of hot_accumulate.
+__device__ __forceinline__ void tag_accumulate(u32* words, u64* slot_sum, u32 h, i32 d) {
+    typedef unsigned long long ull;
+    const u32 old = atomicAdd(words + h, (u32)d << kCellShift);
+    const u32 c = old >> kCellShift;
+    if (c + (u32)d > 0x3fffu) {  // rare
+        const i64 t = (i64)c + d;
+        atomicAdd(reinterpret_cast<ull*>(slot_sum + h), (ull)((t >> 14) << 14));
+    }
+}
+
 // Raw mode: the hot set covers under 30% of the sample, so the hot pass would
 // mostly copy the stream into the miss buffer; the binning pass then reads the
 // stream itself.  Every kernel of the pipeline evaluates this on the same inputs.
@@ -480,9 +519,9 @@ struct WVec {
 template <int MODE, int K, int SPL, typename KeyT, int WK, bool BUF>
 __global__ void __launch_bounds__(kHotThreads, 1)
     cs_hot_kernel(const SketchParams sp, const KeyT* __restrict__ keys, const void* __restrict__ w, uint64_t n,
-                  i64* __restrict__ table, const KeyT* __restrict__ layout, u64* __restrict__ slot_sum,
-                  const u32* __restrict__ hot_sum, uint32_t sample, const MissBuf<KeyT> mb, bool vec_ok,
-                  const u32* __restrict__ priv_go) {
+                  i64* __restrict__ table, const KeyT* __restrict__ layout, const u32* __restrict__ tags,
+                  u64* __restrict__ slot_sum, const u32* __restrict__ hot_sum, uint32_t sample,
+                  const MissBuf<KeyT> mb, bool vec_ok, const u32* __restrict__ priv_go) {
     if (priv_go && *priv_go == 0) return;  // cs_private_kernel took this stream
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
@@ -493,10 +532,13 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     constexpr uint64_t kT = 32ull * kIt;
     constexpr uint32_t S = G::kSlots;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // tagged (u32 keys): S slot words; else S keys + S 16-bit cells
     KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
+    u32* tw = reinterpret_cast<u32*>(smem_raw);
     static_assert(S % 2 == 0, "two cells per word");
-    u32* cells = reinterpret_cast<u32*>(hk + S);  // S 16-bit cells
-    QEnt<KeyT>* q = reinterpret_cast<QEnt<KeyT>*>(cells + S / 2);
+    u32* cells = reinterpret_cast<u32*>(hk + S);  // S 16-bit cells (untagged)
+    QEnt<KeyT>* q = reinterpret_cast<QEnt<KeyT>*>(G::kTagged ? reinterpret_cast<unsigned char*>(tw + S)
+                                                             : reinterpret_cast<unsigned char*>(cells + S / 2));
     __shared__ u32 s_next;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     u32 lanes_below;  // evaluated once (a volatile read is never rematerialised)
@@ -523,8 +565,12 @@ __global__ void __launch_bounds__(kHotThreads, 1)
 
     // every CTA holds the same table layout (hh_layout_kernel), so the slot sums
     // of all CTAs can be merged per slot before the keys are hashed
-    for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) hk[s] = layout[s];
-    for (uint32_t s = threadIdx.x; s < S / 2; s += kHotThreads) cells[s] = 0x80008000u;
+    if constexpr (G::kTagged) {
+        for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) tw[s] = tags[s] | (kCellBias << kCellShift);
+    } else {
+        for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) hk[s] = layout[s];
+        for (uint32_t s = threadIdx.x; s < S / 2; s += kHotThreads) cells[s] = 0x80008000u;
+    }
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
 
@@ -538,10 +584,20 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         // both slots probed speculatively (no divergent second probe); a key never
         // sits in its slot2 unless its slot1 was taken first, so this is exact
         const u32 h1 = slot1<S>(key), h2 = slot2<S>(key);
-        const KeyT c1 = hk[h1], c2 = hk[h2];
-        const u32 h = c1 == key ? h1 : h2;
-        const bool hit = valid && (c1 == key || c2 == key);  // empty slots hold foreign keys
-        if (hit) hot_accumulate(cells, slot_sum, h, d);
+        bool m1, m2;
+        if constexpr (G::kTagged) {  // (slot, choice, tag) is the key; empty slots hold a marker
+            m1 = (tw[h1] & kTagMask) == tag1((u32)key);
+            m2 = (tw[h2] & kTagMask) == tag2((u32)key);
+        } else {  // empty slots hold foreign keys
+            m1 = hk[h1] == key;
+            m2 = hk[h2] == key;
+        }
+        const u32 h = m1 ? h1 : h2;
+        const bool hit = valid && (m1 || m2);
+        if (hit) {
+            if constexpr (G::kTagged) tag_accumulate(tw, slot_sum, h, d);
+            else hot_accumulate(cells, slot_sum, h, d);
+        }
         const bool miss = valid && !hit;
         const unsigned m = __ballot_sync(kFull, miss);
         if (miss) {
@@ -648,7 +704,9 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     // u64 adds commute); hh_merge_kernel hashes each hot key once
     unsigned merged = 0;
     for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
-        const u64 v = ((cells[s >> 1] >> ((s & 1) << 4)) & 0xFFFFu) - 0x8000ull;  // 0 in empty (foreign-key) slots
+        // 0 in empty slots
+        const u64 v = G::kTagged ? (u64)(tw[s] >> kCellShift) - kCellBias
+                                 : ((cells[s >> 1] >> ((s & 1) << 4)) & 0xFFFFu) - 0x8000ull;
         if (v) {
             red_add_u64(slot_sum + s, v);
             ++merged;
@@ -686,7 +744,7 @@ template <typename KeyT>
 __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict__ hot, const u32* __restrict__ hot_cnt,
                                                          const u32* __restrict__ hot_count, u32 cap,
                                                          KeyT* __restrict__ sorted, KeyT* __restrict__ layout,
-                                                         const u32* __restrict__ priv_go) {
+                                                         u32* __restrict__ tags, const u32* __restrict__ priv_go) {
     if (priv_go && *priv_go == 0) return;  // the private byte tables took this stream: no hot set
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
@@ -805,20 +863,38 @@ __global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict_
         }
         __syncthreads();
     }
-    // an empty slot s gets a FOREIGN key, one with slot1 != s and slot2 != s: no
-    // lookup can match it, so the hot kernel needs no empty-slot test
     unsigned placed = 0;
-    for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
-        KeyT k = hk[s];
-        if (k == G::kEmpty) {
-            for (KeyT t = 0;; ++t) {
-                k = G::kEmpty - t;
-                if (slot1<S>(k) != s && slot2<S>(k) != s) break;
+    if constexpr (G::kTagged) {
+        // the slot words the hot kernel copies: the placed key's tag for the slot it
+        // sits in (choice 1 only when it is not its slot1), else the empty marker;
+        // layout[] keeps the keys for hh_merge_kernel (empty slots never have a sum)
+        for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
+            const KeyT k = hk[s];
+            u32 t;
+            if (k == G::kEmpty) {
+                t = empty_tag<S>(s);
+            } else {
+                t = slot1<S>(k) == s ? tag1((u32)k) : tag2((u32)k);
+                ++placed;
             }
-        } else {
-            ++placed;
+            tags[s] = t;
+            layout[s] = k;
         }
-        layout[s] = k;
+    } else {
+        // an empty slot s gets a FOREIGN key, one with slot1 != s and slot2 != s: no
+        // lookup can match it, so the hot kernel needs no empty-slot test
+        for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
+            KeyT k = hk[s];
+            if (k == G::kEmpty) {
+                for (KeyT t = 0;; ++t) {
+                    k = G::kEmpty - t;
+                    if (slot1<S>(k) != s && slot2<S>(k) != s) break;
+                }
+            } else {
+                ++placed;
+            }
+            layout[s] = k;
+        }
     }
     placed = __reduce_add_sync(0xffffffffu, placed);
     if ((threadIdx.x & 31) == 0 && placed) atomicAdd(&g_hot_stats[3], (unsigned long long)placed);  // keys in the table
@@ -1355,12 +1431,13 @@ struct HotPlan {
     uint64_t cap_m = 0;        // miss-buffer capacity
     size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, sum_bytes = 0, hot_bytes = 0,
            layout_bytes = 0, mk_bytes = 0, md_bytes = 0, bin_bytes = 0;
+    size_t tags_bytes = 0;   // tagged hot table (u32 keys): the slot words hh_layout writes
     bool rows_mode = false;  // STRAT_ROWS: misses to the buffer, then the row passes
     size_t rows_bytes = 0;   // row passes' per-CTA tables
     // tc .. slot sums are contiguous and zeroed per call
     size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes + sum_bytes; }
     size_t total() const {
-        return tk_bytes + zero_bytes() + hot_bytes + layout_bytes + mk_bytes + md_bytes + bin_bytes +
+        return tk_bytes + zero_bytes() + hot_bytes + layout_bytes + tags_bytes + mk_bytes + md_bytes + bin_bytes +
                rows_bytes;
     }
 };
@@ -1407,6 +1484,7 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     P.gcnt_bytes = align256((size_t)P.chunks * g.nb * 8 + 8);
     P.sum_bytes = align256((size_t)G::kSlots * 8);
     P.layout_bytes = align256((size_t)G::kSlots * sizeof(KeyT));
+    P.tags_bytes = G::kTagged ? align256((size_t)G::kSlots * 4) : 0;
     P.hot_bytes = align256((size_t)G::kCap * (2 * sizeof(KeyT) + 4));  // hot list, counts, sorted keys
     // row passes: Pow2 / two-for-one splitters of power-of-two rows <= 2^16 cells
     P.rows_mode = g_strategy == STRAT_ROWS && !binned && (sp.b == 61 || sp.b == 89) &&
@@ -1444,6 +1522,8 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     p += P.hot_bytes;
     KeyT* layout = reinterpret_cast<KeyT*>(p);
     p += P.layout_bytes;
+    u32* tags = P.tags_bytes ? reinterpret_cast<u32*>(p) : nullptr;
+    p += P.tags_bytes;
     const MissBuf<KeyT> mb{reinterpret_cast<KeyT*>(p), reinterpret_cast<i32*>(p + P.mk_bytes), mcount, P.cap_m};
     p += P.mk_bytes + P.md_bytes;
     g.bins = reinterpret_cast<u32*>(p);
@@ -1459,7 +1539,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     const bool rows_mode = P.rows_mode && SPL != SPC_ANY;
     auto fn = binned || rows_mode ? cs_hot_kernel<MODE, K, SPL, KeyT, WK, true>
                                   : cs_hot_kernel<MODE, K, SPL, KeyT, WK, false>;
-    const size_t smem = ((size_t)sizeof(KeyT) + 2) * G::kSlots;
+    const size_t smem = G::kTagged ? (size_t)4 * G::kSlots : ((size_t)sizeof(KeyT) + 2) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * sizeof(QEnt<KeyT>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes));
     if (e != cudaSuccess) return e;
@@ -1478,7 +1558,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     const bool priv = !binned && WK == W_NONE && SPL != SPC_ANY && pcells <= 200u * 1024 && pcells % 4 == 0 &&
                       sp.width % 4 == 0 && n >= (1u << 20);
     fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, cap, reinterpret_cast<KeyT*>(hot_cnt + G::kCap), layout,
-                               priv ? go : nullptr);
+                               tags, priv ? go : nullptr);
     if (priv) {
         auto fp = cs_private_kernel<MODE, K, SPL, KeyT>;
         if ((e = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcells)) != cudaSuccess)
@@ -1488,7 +1568,7 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
         ktimer_mark(s, false);
     }
     if (!priv) ktimer_mark(s, true);
-    fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, layout, slot_sum, hot_sum,
+    fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, layout, tags, slot_sum, hot_sum,
                                                           binned ? P.m : 0, mb, vec_ok,
                                                           priv ? go : nullptr);
     if (!priv) ktimer_mark(s, false);

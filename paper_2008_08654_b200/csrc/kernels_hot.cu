@@ -583,20 +583,25 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     auto item = [&](KeyT key, i32 d, bool valid) {
         // both slots probed speculatively (no divergent second probe); a key never
         // sits in its slot2 unless its slot1 was taken first, so this is exact
-        const u32 h1 = slot1<S>(key), h2 = slot2<S>(key);
-        bool m1, m2;
+        bool hit;
         if constexpr (G::kTagged) {  // (slot, choice, tag) is the key; empty slots hold a marker
-            m1 = (tw[h1] & kTagMask) == tag1((u32)key);
-            m2 = (tw[h2] & kTagMask) == tag2((u32)key);
+            // the two choices' products give both the slots (high bits) and the tags
+            // (low 17 bits); the chosen slot is selected as a shared-memory address
+            const u32 p1 = (u32)key * 0x9E3779B1u, p2 = ((u32)key ^ ((u32)key >> 15)) * 0x2C1B3C6Du;
+            u32* a1 = tw + slot_of<S>(p1);
+            u32* a2 = tw + slot_of<S>(p2);
+            const bool m1 = (*a1 & kTagMask) == (p1 & 0x1ffffu);
+            const bool m2 = (*a2 & kTagMask) == ((p2 & 0x1ffffu) | 0x20000u);
+            hit = valid && (m1 || m2);
+            if (hit) {
+                u32* a = m1 ? a1 : a2;
+                tag_accumulate(tw, slot_sum, (u32)(a - tw), d);
+            }
         } else {  // empty slots hold foreign keys
-            m1 = hk[h1] == key;
-            m2 = hk[h2] == key;
-        }
-        const u32 h = m1 ? h1 : h2;
-        const bool hit = valid && (m1 || m2);
-        if (hit) {
-            if constexpr (G::kTagged) tag_accumulate(tw, slot_sum, h, d);
-            else hot_accumulate(cells, slot_sum, h, d);
+            const u32 h1 = slot1<S>(key), h2 = slot2<S>(key);
+            const bool m1 = hk[h1] == key, m2 = hk[h2] == key;
+            hit = valid && (m1 || m2);
+            if (hit) hot_accumulate(cells, slot_sum, m1 ? h1 : h2, d);
         }
         const bool miss = valid && !hit;
         const unsigned m = __ballot_sync(kFull, miss);

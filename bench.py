@@ -121,11 +121,21 @@ def sketch_step(ops, spec, keys, wts, table, mom, merge, ev=None):
 
 def e2e_step(sk, h_keys, h_wts, merge, zeros):
     """The same step through the public host API: counters reset, process() of HOST
-    buffers (H2D inside), merge of the replicas' HBM tables, median F2 read back."""
+    buffers (H2D inside), merge of the replicas' HBM tables, median F2 read back.
+    BENCH_TRACE_E2E=1 prints the parts' wall times to stderr."""
+    t = [time.perf_counter()]
     sk.set_counters(zeros)
+    t.append(time.perf_counter())
     sk.process(h_keys, h_wts)
+    t.append(time.perf_counter())
     merge.sketch(sk)
-    return sk.second_moment(True)
+    t.append(time.perf_counter())
+    m = sk.second_moment(True)
+    t.append(time.perf_counter())
+    if os.environ.get("BENCH_TRACE_E2E"):
+        parts = ", ".join(f"{k} {1e3 * (b - a):.1f}" for k, a, b in zip(("reset", "process", "merge", "moment"), t, t[1:]))
+        print(f"[e2e step] {parts} ms", file=sys.stderr, flush=True)
+    return m
 
 
 def load_peaks():

@@ -9,6 +9,8 @@
 #include <sched.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -507,7 +509,9 @@ void CountSketch::init_device() {
     cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = s;
     const size_t bytes = size_t(rows_) * width_ * sizeof(i64);
-    cuda_check(cudaMalloc(&d_counters_, bytes), "cudaMalloc counters");
+    // the counters, then the estimator's 4 x rows u64 words (row_moments reuses
+    // them: no allocation -- and no device-synchronising cudaFree -- per call)
+    cuda_check(cudaMalloc(&d_counters_, bytes + 4 * size_t(rows_) * sizeof(u64)), "cudaMalloc counters");
     cuda_check(cudaMemsetAsync(d_counters_, 0, bytes, s), "memset");
     cuda_check(cudaStreamSynchronize(s), "sync");
 }
@@ -591,8 +595,21 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
             }
         }
     } drain{st.copy, cs};
+    // MB200_TRACE_PROCESS=1: per-chunk copy / kernel event times and host-side
+    // waits to stderr (diagnosis of slow host-buffer calls; off by default)
+    static const bool trace = std::getenv("MB200_TRACE_PROCESS") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    std::vector<double> t_pack, t_wait;
+    const auto t_call = std::chrono::steady_clock::now();
+    auto tevent = [&](cudaStream_t on) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, on);
+        tev.push_back(e);
+    };
     for (u64 c = 0; c < chunks; ++c) {
         const int slot = int(c & 1);
+        const auto t0 = std::chrono::steady_clock::now();
         const u64 off = c * st.chunk;
         const u64 m = std::min<u64>(st.chunk, n - off);
         // Deltas cross PCIe in the narrowest of i8 / i16 that holds the whole
@@ -601,6 +618,7 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
         // call, and config 5's |delta| <= 100 ship 5 instead of 8 bytes per item.
         // Updates are bit-identical; a chunk that fits neither ships as is.
         if (c >= 2 && narrow) cuda_check(cudaEventSynchronize(st.shipped[slot]), "sync staging");
+        const auto t1 = std::chrono::steady_clock::now();
         int nbits = 0;
         if (wbytes && narrow) {
             const char* src = (const char*)h_weights + off * wbytes;
@@ -615,6 +633,12 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
             for (long long i = 0; i < (long long)m; ++i) dst[i] = uint32_t(src[i]);
         }
         if (c >= 2) cuda_check(cudaStreamWaitEvent(st.copy, st.freed[slot], 0), "wait");
+        if (trace) {
+            const auto t2 = std::chrono::steady_clock::now();
+            t_wait.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+            t_pack.push_back(std::chrono::duration<double, std::milli>(t2 - t1).count());
+            tevent(st.copy);
+        }
         if (narrow_keys)
             cuda_check(cudaMemcpyAsync(st.d_keys[slot], st.h_kn[slot], m * 4, cudaMemcpyHostToDevice, st.copy),
                        "H2D keys");
@@ -635,14 +659,39 @@ void CountSketch::process_batch(const void* h_keys, int key_width, const void* h
         }
         cuda_check(cudaEventRecord(st.shipped[slot], st.copy), "record");
         cuda_check(cudaEventRecord(st.ready[slot], st.copy), "record");
+        if (trace) tevent(st.copy);
         cuda_check(cudaStreamWaitEvent(cs, st.ready[slot], 0), "wait");
+        if (trace) tevent(cs);
         if (nbits) cuda_check(mb200::launch_widen_deltas(st.d_wn[slot], nbits, st.d_w[slot], weight_kind, m, cs), "widen");
         // keys were validated on the host above: skip the per-chunk device check
         throw_status(mb200::cs_update_nocheck(&d, st.d_keys[slot], kw_dev, wbytes ? st.d_w[slot] : nullptr, weight_kind,
                                      m, d_counters_, cs));
         cuda_check(cudaEventRecord(st.freed[slot], cs), "record");
+        if (trace) tevent(cs);
     }
     cuda_check(cudaStreamSynchronize(cs), "sync");
+    if (trace && !tev.empty()) {
+        double copy = 0, cmax = 0, kern = 0, kmax = 0, span = 0;
+        for (size_t c = 0; c + 3 < tev.size(); c += 4) {
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, tev[c], tev[c + 1]);
+            cudaEventElapsedTime(&b, tev[c + 2], tev[c + 3]);
+            copy += a, cmax = std::max(cmax, (double)a), kern += b, kmax = std::max(kmax, (double)b);
+        }
+        float sp = 0;
+        cudaEventElapsedTime(&sp, tev.front(), tev.back());
+        span = sp;
+        double pk = 0, pmax = 0, wt = 0, wmax = 0;
+        for (double v : t_pack) pk += v, pmax = std::max(pmax, v);
+        for (double v : t_wait) wt += v, wmax = std::max(wmax, v);
+        const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count();
+        std::fprintf(stderr,
+                     "[mb200 process] n=%llu chunks=%llu wall %.1f ms | device span %.1f | copies %.1f (max %.2f) | "
+                     "kernels %.1f (max %.2f) | host pack %.1f (max %.2f) | host waits %.1f (max %.2f)\n",
+                     (unsigned long long)n, (unsigned long long)chunks, wall, span, copy, cmax, kern, kmax, pk, pmax, wt,
+                     wmax);
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
 }
 
 u64 CountSketch::h2d_bytes() const { return staging_ ? staging_->h2d_bytes : 0; }
@@ -657,11 +706,11 @@ void CountSketch::process(u128 x, i64 delta) {
 }
 
 std::vector<CountSketch::Moment> CountSketch::row_moments() const {
-    DevBuf<u64> out(4 * size_t(rows_));
+    u64* out = reinterpret_cast<u64*>(d_counters_ + size_t(rows_) * width_);  // init_device's moment words
     cudaStream_t s = (cudaStream_t)stream_;
-    throw_status(mb200_cs_moments(d_counters_, rows_, width_, out.p, s));
+    throw_status(mb200_cs_moments(d_counters_, rows_, width_, out, s));
     std::vector<u64> h(4 * size_t(rows_));
-    cuda_check(cudaMemcpyAsync(h.data(), out.p, h.size() * sizeof(u64), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaMemcpyAsync(h.data(), out, h.size() * sizeof(u64), cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaStreamSynchronize(s), "sync");
     std::vector<Moment> m(rows_);
     for (unsigned r = 0; r < rows_; ++r) m[r] = {(u128(h[4 * r + 1]) << 64) | h[4 * r], h[4 * r + 2] != 0};

@@ -663,6 +663,31 @@ def kernel_time(torch, mb, steps, warmup, fn, name=None):
     return total / launches
 
 
+def graph_step(torch, eager_fn, local_fn, tail_fn, world, name):
+    """A short step replayed as one CUDA graph (launch gaps out): the rank-local part
+    (zero + scatter (+ estimator at N = 1)) is captured; with N > 1 the merge and the
+    estimator (`tail_fn`) follow the replay eagerly.  Eager launches if capture fails."""
+    try:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            local_fn()
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            local_fn()
+        if world == 1:
+            return graph.replay, True
+
+        def step():
+            graph.replay()
+            tail_fn()
+        return step, True
+    except Exception as exc:  # eager launches when capture is unavailable
+        print(f"{name}: graph capture failed ({exc}); eager", file=sys.stderr)
+        return eager_fn, False
+
+
 def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ranks, merge):
     out = {}
     SK = S ^ mb.SALT_KEYS
@@ -691,26 +716,8 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
         if world == 1:
             mb.cs_moments(table, 1, 1024, mom)
 
-    step_fn, graphed = c1, False
-    try:
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            c1_local()
-        torch.cuda.current_stream().wait_stream(side)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            c1_local()
-        if world == 1:
-            step_fn = graph.replay
-        else:
-            def step_fn():
-                graph.replay()
-                merge.table(table)
-                mb.cs_moments(table, 1, 1024, mom)
-        graphed = True
-    except Exception as exc:  # eager launches when capture is unavailable
-        print(f"config 1: graph capture failed ({exc}); eager", file=sys.stderr)
+    step_fn, graphed = graph_step(torch, c1, c1_local, lambda: (merge.table(table), mb.cs_moments(table, 1, 1024, mom)),
+                                  world, "config 1")
     t = max_over_ranks(timed_steps(torch, steps, args.warmup, step_fn, flush))
     tk = max_over_ranks(timed_steps(torch, steps, args.warmup, lambda: mb.cs_update(spec, keys, table), flush))
     out["c1"] = {"value": C1_ITEMS / t, "unit": "updates/s", "ms_per_step": t * 1e3,
@@ -757,13 +764,23 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
     def c4():
         sketch_step(mb, spec, keys, None, table, mom, merge)
 
-    t = max_over_ranks(timed_steps(torch, steps, args.warmup, c4))
+    # zero + scatter (kernel + fold) + estimator replayed as one CUDA graph, as config 1
+    def c4_local():
+        table.zero_()
+        mb.cs_update(spec, keys, table)
+        if world == 1:
+            mb.cs_moments(table, 2, 1 << 16, mom)
+
+    step_fn, graphed4 = graph_step(torch, c4, c4_local,
+                                   lambda: (merge.table(table), mb.cs_moments(table, 2, 1 << 16, mom)), world,
+                                   "config 4")
+    t = max_over_ranks(timed_steps(torch, steps, args.warmup, step_fn))
     # the scatter kernel alone (cs_private89_kernel), on the stream it is launched on
     tk = max_over_ranks(kernel_time(torch, mb, steps, args.warmup, lambda: mb.cs_update(spec, keys, table),
                                     "cs_private89"))
     out["c4"] = {"value": C4_KEYS / t, "unit": "keys/s", "row_updates_per_s": 2 * C4_KEYS / t,
                  "ms_per_step": t * 1e3, "workload": "2^89-1 two-for-one, 2^26 u64 keys, 2 x 2^16 counters",
-                 "l2": "inputs 512 MiB > L2", "kernel_ms": tk * 1e3,
+                 "l2": "inputs 512 MiB > L2", "kernel_ms": tk * 1e3, "cuda_graph": graphed4,
                  "roofline": roofline("c4", hi - lo, tk, "c4"),
                  "path": "cs_private89_kernel (config 4's shape: whole table per CTA in 8-bit shared cells, "
                          "per-CTA tables summed by private_fold_kernel); bound by the FMA-heavy + ALU pipes "

@@ -156,10 +156,18 @@ struct Batch {
     u64 n = 0;
 };
 
+// Per-thread parse buffers, kept across blocks (no allocation or first-touch
+// page faults per block).
+struct ParseScratch {
+    std::vector<std::vector<u64>> keys;
+    std::vector<std::vector<i64>> deltas;
+};
+
 // Parse the complete lines of [buf, buf + len) (ends on '\n', or at EOF on the
 // last line) with every host thread.  first_line = number of lines before the
-// block.  Throws the reference's stream_error for the first bad line.
-void parse_block(const char* buf, size_t len, u64 first_line, u128 domain, Batch& out) {
+// block.  Throws the reference's stream_error for the first bad line; returns
+// the number of lines parsed.
+u64 parse_block(const char* buf, size_t len, u64 first_line, u128 domain, Batch& out, ParseScratch& ps) {
     const int T = std::max(1, std::min<int>(omp_get_max_threads(), int(len / (1 << 16)) + 1));
     std::vector<size_t> cut(T + 1, len);
     cut[0] = 0;
@@ -170,16 +178,24 @@ void parse_block(const char* buf, size_t len, u64 first_line, u128 domain, Batch
     }
     std::vector<u64> lines(T, 0), items(T, 0);
     std::vector<LineError> errs(T);
-    std::vector<std::vector<u64>> tk(T);
-    std::vector<std::vector<i64>> td(T);
+    if (ps.keys.size() < (size_t)T) {
+        ps.keys.resize(T);
+        ps.deltas.resize(T);
+    }
+    auto& tk = ps.keys;
+    auto& td = ps.deltas;
 #pragma omp parallel for num_threads(T) schedule(static, 1)
     for (int t = 0; t < T; ++t) {
         const char* p = buf + cut[t];
         const char* end = buf + cut[t + 1];
         auto& K = tk[t];
         auto& D = td[t];
-        K.reserve(size_t(end - p) / 4 + 1);
-        D.reserve(size_t(end - p) / 4 + 1);
+        const size_t cap = size_t(end - p) / 4 + 1;  // a line holds at least "k d\n" + 1
+        if (K.size() < cap) {
+            K.resize(cap);
+            D.resize(cap);
+        }
+        size_t ni = 0;
         u64 ln = 0;
         std::string msg;
         while (p < end) {
@@ -194,13 +210,14 @@ void parse_block(const char* buf, size_t len, u64 first_line, u128 domain, Batch
                 break;
             }
             if (kind == LineKind::Item) {
-                K.push_back(key);
-                D.push_back(delta);
+                K[ni] = key;
+                D[ni] = delta;
+                ++ni;
             }
             p = nl ? le + 1 : end;
         }
         if (!errs[t].line) lines[t] = ln;
-        items[t] = K.size();
+        items[t] = ni;
     }
     u64 before = first_line;
     for (int t = 0; t < T; ++t) {
@@ -224,6 +241,7 @@ void parse_block(const char* buf, size_t len, u64 first_line, u128 domain, Batch
         std::memcpy(out.deltas.data() + off[t], td[t].data(), items[t] * sizeof(i64));
     }
     out.n = total;
+    return before - first_line;
 }
 
 // Streams "key delta" lines from `in` into `sink(batch)` (run on a worker
@@ -236,6 +254,7 @@ u64 ingest(FILE* in, u128 domain, Sink sink) {
     size_t have = 0;  // bytes in buf (an incomplete last line carried over)
     u64 line_base = 0, processed = 0;
     Batch batches[2];
+    ParseScratch ps;
     int cur = 0;
     std::thread worker;
     std::exception_ptr worker_err;
@@ -266,8 +285,7 @@ u64 ingest(FILE* in, u128 domain, Sink sink) {
             }
             if (len == 0) break;
             Batch& bt = batches[cur];
-            parse_block(buf.data(), len, line_base, domain, bt);
-            line_base += u64(std::count(buf.data(), buf.data() + len, '\n')) + (eof && buf[len - 1] != '\n' ? 1 : 0);
+            line_base += parse_block(buf.data(), len, line_base, domain, bt, ps);
             std::memmove(buf.data(), buf.data() + len, have - len);
             have -= len;
             join();  // the previous batch is on the device; its buffer is free again

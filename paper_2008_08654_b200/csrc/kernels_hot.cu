@@ -1630,20 +1630,39 @@ cudaError_t run_private89(const SketchParams& sp, const u64* keys, uint64_t n, i
         c89.a[j][1] = (u32)(sp.lo[j] >> 32);
         c89.a[j][2] = (u32)sp.hi[j];
     }
-    auto fp = cs_private89_kernel<LW>;
+    auto fp = cs_private89_kernel<LW, false>;
+    auto ff = cs_private89_kernel<LW, true>;
     cudaError_t e = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes);
     if (e != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tbytes)) != cudaSuccess)
+        return e;
     uint4* scratch = nullptr;
     if ((e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (size_t)sms * tbytes, s)) != cudaSuccess) return e;
+    const ulonglong2* kv = reinterpret_cast<const ulonglong2*>(keys);
+    uint64_t np = n / 2;
+    const u64* odd = (n & 1) ? keys + n - 1 : nullptr;
+    uint64_t* l2 = reinterpret_cast<uint64_t*>(table);
+    const u32* nogo = nullptr;
+    // one cooperative launch (grid barrier, then every CTA folds its share of the
+    // columns) where the device supports it; else the kernel + private_fold_kernel
+    static const bool coop = [] {
+        int v = 0, dev = 0;
+        cudaGetDevice(&dev);
+        return cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && v != 0;
+    }();
     ktimer_mark(s, true);
-    fp<<<sms, kP89Threads, tbytes, s>>>(c89, reinterpret_cast<const ulonglong2*>(keys), n / 2,
-                                        (n & 1) ? keys + n - 1 : nullptr, scratch,
-                                        reinterpret_cast<uint64_t*>(table), nullptr);
-    ktimer_mark(s, false);
-    const u32 cols = (u32)(tbytes / 16);
-    private_fold_kernel<<<(cols + kFoldCols - 1) / kFoldCols, kFoldThreads, 0, s>>>(scratch, cols, (u32)sms, table,
-                                                                                    nullptr);
-    e = cudaGetLastError();
+    if (coop) {
+        void* args[] = {(void*)&c89, (void*)&kv, (void*)&np, (void*)&odd, (void*)&scratch, (void*)&l2, (void*)&nogo};
+        e = cudaLaunchCooperativeKernel((const void*)ff, dim3(sms), dim3(kP89Threads), args, tbytes, s);
+        ktimer_mark(s, false);
+    } else {
+        fp<<<sms, kP89Threads, tbytes, s>>>(c89, kv, np, odd, scratch, l2, nogo);
+        ktimer_mark(s, false);
+        const u32 cols = (u32)(tbytes / 16);
+        private_fold_kernel<<<(cols + kFoldCols - 1) / kFoldCols, kFoldThreads, 0, s>>>(scratch, cols, (u32)sms,
+                                                                                        table, nullptr);
+        e = cudaGetLastError();
+    }
     const cudaError_t e2 = cudaFreeAsync(scratch, s);
     return e != cudaSuccess ? e : e2;
 }

@@ -27,6 +27,8 @@
 //     stores and private_fold_kernel sums the 148 tables per cell.
 #pragma once
 
+#include <cooperative_groups.h>
+
 namespace mb200 {
 namespace {
 
@@ -239,7 +241,7 @@ __device__ __forceinline__ void keys_c4(const Coef89& c, const u64 (&x)[KP], u32
 // keys as 16-byte pairs [0, npairs) (+ one odd last key, taken by CTA 0);
 // each CTA a contiguous share.  The CTA's byte table goes to scratch[blockIdx]
 // (2^(LW+1) bytes), summed by private_fold_kernel.
-template <int LW>
+template <int LW, bool FUSED>
 __global__ void __launch_bounds__(kP89Threads, 1)
     cs_private89_kernel(const Coef89 c, const ulonglong2* __restrict__ kv, uint64_t npairs, const u64* __restrict__ odd,
                         uint4* __restrict__ scratch, uint64_t* __restrict__ l2, const u32* __restrict__ go) {
@@ -276,6 +278,46 @@ __global__ void __launch_bounds__(kP89Threads, 1)
     uint4* dst = scratch + (size_t)blockIdx.x * (kWords / 4);
     for (u32 j = threadIdx.x; j < kWords / 4; j += kP89Threads) dst[j] = pw4[j];
     if (threadIdx.x == 0) atomicAdd(&g_hot_stats[0], (unsigned long long)(2 * (hi - lo) + (odd && blockIdx.x == 0)));
+    if constexpr (FUSED) {
+        // cooperative launch: every CTA's table is in scratch after the grid barrier;
+        // CTA b then folds its share of the 16-byte columns (64 columns x 16 groups
+        // of CTAs per pass, partial sums in the freed shared table)
+        cooperative_groups::this_grid().sync();
+        constexpr u32 cols = kWords / 4, kC = 64, kG = kP89Threads / kC;
+        const u32 per = (cols + gridDim.x - 1) / gridDim.x;
+        const u32 ci = threadIdx.x % kC, grp = threadIdx.x / kC;
+        i32(*part)[kC][17] = reinterpret_cast<i32(*)[kC][17]>(pwords);
+        for (u32 c0 = blockIdx.x * per; c0 < min((blockIdx.x + 1) * per, cols); c0 += kC) {
+            const u32 col = c0 + ci;
+            const bool live = ci < per && col < min((blockIdx.x + 1) * per, cols);
+            i32 acc[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = 0;
+            if (live) {
+                for (u32 cta = grp; cta < gridDim.x; cta += kG) {
+                    const uint4 v = __ldcg(scratch + (size_t)cta * cols + col);
+                    const u32 wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) acc[4 * w + b] += (i32)((wv[w] >> (8 * b)) & 0xffu);
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) part[grp][ci][j] = acc[j];
+            __syncthreads();
+            if (live) {  // thread (ci, grp) finishes cell grp of column ci
+                i32 v = -0x80 * (i32)gridDim.x;
+#pragma unroll
+                for (int g = 0; g < (int)kG; ++g) v += part[g][ci][grp];
+                if (v) {
+                    i64* t = reinterpret_cast<i64*>(l2) + (size_t)col * 16 + grp;
+                    *t = (i64)((u64)*t + (u64)(i64)v);
+                }
+            }
+        }
+    }
 }
 
 // table[cell] += sum over the CTAs' byte tables of (byte - 2^7).  A block of

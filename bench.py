@@ -460,6 +460,9 @@ def main():
             out["l2_red"] = {"achieved": l2_reds / kernel_s / 1e9, "peak": red_peak / 1e9, "unit": "G red/s",
                              "frac": l2_reds / kernel_s / red_peak, "reds_per_launch": l2_reds,
                              "peak_kind": "measured (probe_atomics random red.global.add.u64, this run)"}
+        wi = ent.get("warp_instructions_per_launch")
+        if wi and world == 1:  # ncu's executed warp instructions of the same-size launch, per unit of work
+            out["thread_instructions_per_unit"] = wi * 32 / units
         pipes = ent.get("pipes")
         if pipes:
             busy = {k: v for k, v in pipes.items() if v is not None}

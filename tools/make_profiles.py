@@ -73,7 +73,9 @@ def main(tag):
         def pct(metric):
             return float(v[h.index(metric)]) / 100.0 if metric in h else None
 
+        inst = float(v[h.index("smsp__inst_executed.sum")].replace(",", "")) if "smsp__inst_executed.sum" in h else None
         traffic[t] = {"kernel": v[h.index("Kernel Name")].split("(")[0], "dram_bytes_per_launch": rd + wr,
+                      "warp_instructions_per_launch": inst,
                       "pipes": {"alu": pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
                                 "fma": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
                                 "fmaheavy": pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),

@@ -102,6 +102,21 @@ static void test_polyhash() {  // test_polyhash.cpp:57-88
     same = true;
     for (size_t i = 0; i < keys.size(); ++i) same &= h89[i] == ((u128(oh[i]) << 64) | out[i]);
     CHECK(same);
+    // generic wide moduli (62 <= b <= 127) through mb200_hash_wide
+    for (unsigned b : {62u, 107u, 127u}) {
+        MersenneModulus mb(b, b != 62);  // 2^62-1 is composite: unchecked modulus
+        for (unsigned k : {1u, 3u, 8u}) {
+            PolyHashFamily gb(mb, k, u128(1) << 60, 11 + b + k);
+            std::vector<u64> wl(k), wh(k);
+            orc_draw_coeffs(b, k, 11 + b + k, wl.data(), wh.data());
+            for (auto& x : keys) x &= (u64(1) << 60) - 1;
+            auto hb = gb.hash(keys);
+            CHECK(orc_hash_batch(b, wl.data(), wh.data(), k, 60, keys.data(), keys.size(), out.data(), oh.data()) == 0);
+            same = true;
+            for (size_t i = 0; i < keys.size(); ++i) same &= hb[i] == ((u128(oh[i]) << 64) | out[i]);
+            CHECK(same);
+        }
+    }
 }
 
 static void test_bucketing() {  // test_bucketing.cpp:101-127

@@ -405,7 +405,8 @@ def main():
     hbm_peak, peak_kind = load_peaks()
     traffic = load_traffic()
 
-    # ---- integer-pipe peak: independent mad.wide.u32 chains ----
+    # ---- integer-pipe peak: independent IMAD.WIDE.U32 product chains (
+    # the SASS of the probe loop is IMAD.WIDE only, profiles/r02f/imad_probe.txt) ----
     sink = torch.zeros(1, dtype=torch.int64, device=dev)
     blocks, threads, iters = mb_sm_count(torch) * 8, 256, 4096
     for _ in range(2):
@@ -463,6 +464,13 @@ def main():
         wi = ent.get("warp_instructions_per_launch")
         if wi and world == 1:  # ncu's executed warp instructions of the same-size launch, per unit of work
             out["thread_instructions_per_unit"] = wi * 32 / units
+        iw = ent.get("imad_wide_warp_per_launch")
+        if iw and world == 1:  # the IMAD.WIDE the kernel executes (ncu SASS opcode counts), same peak
+            out["int_executed"] = {"imad_wide_per_unit": iw * 32 / units, "achieved": iw * 32 / kernel_s / 1e12,
+                                   "peak": imad_peak / 1e12, "unit": "T IMAD.WIDE/s",
+                                   "frac": iw * 32 / kernel_s / imad_peak,
+                                   "note": "executed IMAD.WIDE.U32 warp instructions x 32 (ncu SASS source page "
+                                           "of the same-size launch) / measured peak"}
         pipes = ent.get("pipes")
         if pipes:
             busy = {k: v for k, v in pipes.items() if v is not None}

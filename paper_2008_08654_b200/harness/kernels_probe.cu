@@ -14,17 +14,24 @@ namespace {
 
 constexpr int kChains = 8;
 
-// kChains independent mad.wide.u32 accumulation chains per thread.
+// kChains independent IMAD.WIDE.U32 chains per thread: acc = hi32(acc) * b.
+// The next multiplicand is the product's own high word, so the products
+// cannot be hoisted, and there is no accumulate: a mad.wide with a register
+// addend is split by ptxas into IMAD.WIDE + IADD3/IADD3.X, and with
+// loop-invariant operands the product is hoisted and only the 64-bit add is
+// left (the round-1/2 form of this probe up to r02e measured that add rate,
+// 1.72e13/s).  The SASS of this loop is IMAD.WIDE.U32 only.
 __global__ void probe_imad_kernel(int iters, u64* sink) {
     u64 acc[kChains];
-    const u32 a = threadIdx.x | 1u;
     const u32 b = blockIdx.x * 2654435761u + 12345u;
 #pragma unroll
-    for (int j = 0; j < kChains; ++j) acc[j] = j;
+    for (int j = 0; j < kChains; ++j) acc[j] = threadIdx.x * 0x9E3779B97F4A7C15ull + j;
     for (int i = 0; i < iters; ++i) {
 #pragma unroll
         for (int j = 0; j < kChains; ++j)
-            asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc[j]) : "r"(a + (u32)j), "r"(b));
+            asm volatile("{\n\t.reg .u32 l, h;\n\tmov.b64 {l, h}, %0;\n\tmul.wide.u32 %0, h, %1;\n\t}"
+                         : "+l"(acc[j])
+                         : "r"(b));
     }
     u64 s = 0;
 #pragma unroll

@@ -82,6 +82,10 @@ def main(tag):
                                 "issue": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                                 "dram": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                                 "lts": pct("lts__throughput.avg.pct_of_peak_sustained_elapsed")}}
+        mix = ncu_summary.opcode_mix(rep)
+        if mix:
+            traffic[t]["imad_wide_warp_per_launch"] = sum(n for k, n in mix.items() if k.startswith("IMAD.WIDE"))
+            traffic[t]["opcodes_per_launch"] = dict(sorted(mix.items(), key=lambda kv: -kv[1])[:16])
     with open(os.path.join(dst, "ncu_traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:

@@ -29,6 +29,33 @@ def raw(rep):
     return r[0], r[1], r[2:]
 
 
+def opcode_mix(rep):
+    """Executed warp instructions per SASS mnemonic (predicate stripped), from the
+    SASS source page of the report."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(out)))
+    hdr = next((x for x in r if x and x[0] == "Address"), None)
+    if not hdr:
+        return {}
+    iS, iI = hdr.index("Source"), hdr.index("Instructions Executed")
+    mix = {}
+    for x in r:
+        if len(x) <= iI or not x[0].startswith("0x"):
+            continue
+        toks = x[iS].split()
+        if toks and toks[0].startswith("@"):
+            toks = toks[1:]
+        if not toks:
+            continue
+        try:
+            n = float(x[iI])
+        except ValueError:
+            continue
+        mix[toks[0]] = mix.get(toks[0], 0.0) + n
+    return mix
+
+
 def main(rep, top=12):
     h, u, rows = raw(rep)
     for v in rows:
@@ -42,6 +69,11 @@ def main(rep, top=12):
         tot = sum(s for s, _ in stalls) or 1
         print("  stall mix:", ", ".join(f"{n.replace('smsp__pcsamp_warps_issue_stalled_', '')} {s / tot:.0%}"
                                          for s, n in stalls[:8]))
+    mix = opcode_mix(rep)
+    if mix:
+        tot = sum(mix.values()) or 1
+        print("  SASS opcode mix (warp instructions):", ", ".join(
+            f"{k} {v / tot:.1%}" for k, v in sorted(mix.items(), key=lambda kv: -kv[1])[:12]))
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))

@@ -62,6 +62,10 @@ def main():
         e1.record()
         e1.synchronize()
         print(f"{w} launch {i}: {e0.elapsed_time(e1):.3f} ms", flush=True)
+    if w == "c5":
+        hs = mb.hot_stats(reset=True)
+        print(f"c5 hot set: {hs['hot_keys'] / a.reps:.0f} keys placed, miss fraction "
+              f"{hs['misses'] / max(1, hs['items']):.4f}", flush=True)
 
 
 if __name__ == "__main__":

@@ -47,10 +47,13 @@
 // 4's shape cs_private89_kernel, mb200_private89.cuh).
 // The table is bit-identical to the per-item path for ANY hot set (integer
 // addition commutes); the hot set only decides how much L2 traffic is saved.
+#include <cstdlib>
 #include <type_traits>
 #include <utility>
 #include <vector>
 
+#include "mb200_hot_geom.cuh"
+#include "mb200_hotprep.h"
 #include "mb200_sketch_dev.cuh"
 
 namespace mb200 {
@@ -82,272 +85,12 @@ constexpr uint32_t kMinSample = 1u << 18, kMaxSample = 1u << 22;
 constexpr int kQueue = 64;     // < 32 queued + one slot of 32 misses
 constexpr uint32_t kMissChunk = 1024;  // miss-buffer slots a warp reserves at once
 
-template <typename KeyT>
-struct HotGeom;
 // a queued miss: key and delta side by side (one 8-byte shared store for u32 keys)
 template <typename KeyT>
 struct alignas(sizeof(KeyT) * 2) QEnt {
     KeyT k;
     i32 d;
 };
-// u32 keys: a TAGGED slot, one 32-bit word = 14-bit cell (bits 18-31, the low
-// 14 bits of the slot's sum, 2^13-biased) | choice bit (17) | 17-bit tag.  A
-// key's two choices are the bijections pi1(K) = K c1 and pi2(K) = (K ^ K >> 15)
-// c2 of the u32 key; slot_i = floor(pi_i S / 2^32) and tag_i = pi_i mod 2^17.
-// The pi values of one slot form an interval of ceil(2^32 / S) = 80660 < 2^17
-// values, so (slot, choice, tag) identifies the key exactly, and the value
-// just below a slot's interval (mod 2^17) with choice 0 is a tag no key can
-// have there: the empty-slot marker.  The cell sits in the word's top bits, so
-// an add's carry leaves the word instead of touching the tag.  4 bytes per slot:
-// 53248 slots in 208 KiB (35840 in the 6-byte key + 16-bit cell layout before;
-// misses 10.8% -> ~9.7% on config 5).
-// u64 keys: slot = 8-byte key + a 16-bit cell (two per 32-bit word).
-// Slot counts need not be powers of 2.  The wraps of either cell go straight
-// into the slot's shared total in HBM (hot_accumulate / tag_accumulate).
-template <>
-struct HotGeom<u32> {
-    static constexpr bool kTagged = true;
-    static constexpr uint32_t kSlots = 53248;  // x 4 B = 208 KiB
-    static constexpr uint32_t kCap = 61440;    // selected candidates (the layout places ~46K)
-    static constexpr u32 kEmpty = 0xffffffffu;
-    using Cas = unsigned;
-};
-template <>
-struct HotGeom<u64> {
-    static constexpr bool kTagged = false;
-    static constexpr uint32_t kSlots = 19456;  // x (8 B key + 2 B cell) = 190 KiB
-    static constexpr uint32_t kCap = 16384;
-    static constexpr u64 kEmpty = ~0ull;
-    using Cas = unsigned long long;
-};
-constexpr u32 kTagMask = 0x3ffffu;  // choice bit + 17-bit tag
-constexpr u32 kCellShift = 18;      // 14-bit cell in bits 18-31
-constexpr u32 kCellBias = 0x2000u;
-
-// two independent slot choices in [0, S): multiply-high range reduction of two
-// independent 32-bit mixes (any S, not only powers of two)
-template <uint32_t S>
-__device__ __forceinline__ u32 slot_of(u32 h) {
-    return (u32)(((u64)h * S) >> 32);
-}
-template <uint32_t S>
-__device__ __forceinline__ u32 slot1(u32 key) {
-    return slot_of<S>(key * 0x9E3779B1u);
-}
-template <uint32_t S>
-__device__ __forceinline__ u32 slot2(u32 key) {
-    return slot_of<S>((key ^ (key >> 15)) * 0x2C1B3C6Du);
-}
-// the tagged table's identity of key K in slot_i(K): tag_i(K) (choice bit i)
-__device__ __forceinline__ u32 tag1(u32 key) { return (key * 0x9E3779B1u) & 0x1ffffu; }
-__device__ __forceinline__ u32 tag2(u32 key) { return (((key ^ (key >> 15)) * 0x2C1B3C6Du) & 0x1ffffu) | 0x20000u; }
-// empty-slot marker of slot s: choice 0, tag = (first pi1 value of the slot) - 1 mod 2^17
-template <uint32_t S>
-__device__ __forceinline__ u32 empty_tag(u32 s) {
-    const u64 lo = (((u64)s << 32) + S - 1) / S;  // ceil(s 2^32 / S)
-    return (u32)(lo - 1) & 0x1ffffu;
-}
-template <uint32_t S>
-__device__ __forceinline__ u32 slot1(u64 key) {
-    return slot_of<S>((u32)(mix64(key) >> 32));
-}
-template <uint32_t S>
-__device__ __forceinline__ u32 slot2(u64 key) {
-    return slot_of<S>((u32)mix64(key));
-}
-
-// Exact key counts of the sample in a global open-addressing table.  Each CTA
-// first counts its share in a shared-memory table (so the hottest keys of a
-// skewed stream cost one global atomic per CTA, not one per warp: 32K warps
-// incrementing one counter serialise at L2), then merges its distinct keys.
-constexpr int kCountThreads = 512;
-constexpr uint32_t kLocalSlots = 4096;
-
-template <typename KeyT>
-__device__ __forceinline__ void count_global(KeyT* tk, u32* tc, u32 slots, KeyT key, u32 cnt) {
-    using G = HotGeom<KeyT>;
-    using C = typename G::Cas;
-    u32 h = (u32)(((u64)((u32)(mix64((u64)key) >> 32)) * slots) >> 32);
-    for (;;) {
-        KeyT cur = tk[h];
-        if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(tk + h), (C)G::kEmpty, (C)key);
-        if (cur == G::kEmpty || cur == key) {
-            atomicAdd(tc + h, cnt);
-            return;
-        }
-        h = h + 1 == slots ? 0 : h + 1;
-    }
-}
-
-// Quick look at the batch's first kProbeItems items (kProbeCtas CTAs, each
-// counting its contiguous share in a shared table): if keys seen at least twice
-// within a share cover under 1/32 of the items (a stream without heavy
-// hitters, like config 4's uniform 64-bit keys), the sample / selection kernels
-// are skipped (go[0] = 0) and every item takes the direct path.  go[1] sums the
-// covered items, go[2] is the ticket of the last CTA, which decides.
-// Performance only.
-constexpr uint32_t kProbeItems = 1u << 14;
-constexpr int kProbeCtas = 8;
-
-template <typename KeyT>
-__global__ void __launch_bounds__(1024) hh_probe_kernel(const KeyT* __restrict__ keys, uint64_t n, u32* go) {
-    using G = HotGeom<KeyT>;
-    using C = typename G::Cas;
-    constexpr u32 kProbeSlots = kLocalSlots / 2;  // a share of 2^11 items fits
-    __shared__ KeyT lk[kProbeSlots];
-    __shared__ u32 lc[kProbeSlots];
-    __shared__ u32 covered;
-    for (u32 i = threadIdx.x; i < kProbeSlots; i += blockDim.x) {
-        lk[i] = G::kEmpty;
-        lc[i] = 0;
-    }
-    if (threadIdx.x == 0) covered = 0;
-    __syncthreads();
-    const u32 m = (u32)(n < kProbeItems ? n : kProbeItems);
-    const u32 lo = m * blockIdx.x / gridDim.x, hi = m * (blockIdx.x + 1) / gridDim.x;
-    for (u32 i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const KeyT key = ld_nc(keys + i);
-        if (key == G::kEmpty) continue;
-        u32 h = (u32)mix64((u64)key) & (kProbeSlots - 1);
-        for (int probe = 0; probe < 8; ++probe) {  // a crowded table just drops the item
-            KeyT cur = lk[h];
-            if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(lk + h), (C)G::kEmpty, (C)key);
-            if (cur == G::kEmpty || cur == key) {
-                atomicAdd(lc + h, 1u);
-                break;
-            }
-            h = (h + 1) & (kProbeSlots - 1);
-        }
-    }
-    __syncthreads();
-    u32 mine = 0;
-    for (u32 i = threadIdx.x; i < kProbeSlots; i += blockDim.x) mine += lc[i] >= 2 ? lc[i] : 0;
-    mine = __reduce_add_sync(0xffffffffu, mine);
-    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&covered, mine);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (covered) atomicAdd(go + 1, covered);
-        __threadfence();
-        if (atomicAdd(go + 2, 1u) == gridDim.x - 1) {  // the last CTA: every share is counted
-            __threadfence();
-            go[0] = atomicAdd(go + 1, 0u) * 32 >= m ? 1u : 0u;
-        }
-    }
-}
-
-template <typename KeyT>
-__global__ void __launch_bounds__(kCountThreads) hh_count_kernel(const KeyT* __restrict__ keys, uint64_t n, KeyT* tk,
-                                                                 u32* tc, u32 slots, const u32* __restrict__ go) {
-    using G = HotGeom<KeyT>;
-    using C = typename G::Cas;
-    if (!*go) return;
-    __shared__ KeyT lk[kLocalSlots];
-    __shared__ u32 lc[kLocalSlots];
-    for (u32 i = threadIdx.x; i < kLocalSlots; i += kCountThreads) {
-        lk[i] = G::kEmpty;
-        lc[i] = 0;
-    }
-    __syncthreads();
-    const uint64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += kCountThreads) {
-        const KeyT key = ld_nc(keys + i);
-        if (key == G::kEmpty) continue;  // the sentinel key is never hot
-        u32 h = (u32)mix64((u64)key) & (kLocalSlots - 1);
-        bool done = false;
-        for (int probe = 0; probe < 8 && !done; ++probe) {
-            KeyT cur = lk[h];
-            if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(lk + h), (C)G::kEmpty, (C)key);
-            if (cur == G::kEmpty || cur == key) {
-                atomicAdd(lc + h, 1u);
-                done = true;
-            }
-            h = (h + 1) & (kLocalSlots - 1);
-        }
-        if (!done) count_global(tk, tc, slots, key, 1u);  // local table crowded
-    }
-    __syncthreads();
-    for (u32 i = threadIdx.x; i < kLocalSlots; i += kCountThreads)
-        if (lc[i]) count_global(tk, tc, slots, lk[i], lc[i]);
-}
-
-__global__ void hh_hist_kernel(const u32* __restrict__ tc, u32* hist, u32 slots, const u32* __restrict__ go) {
-    if (!*go) return;
-    __shared__ u32 sh[256];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
-    __syncthreads();
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x) {
-        const u32 c = tc[s];
-        if (c) atomicAdd(&sh[c < 255 ? c : 255], 1u);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < 256; i += blockDim.x)
-        if (sh[i]) atomicAdd(hist + i, sh[i]);
-}
-
-// One pass over the count table: keys with count >= thr (they fit by
-// construction) take hot-list entries [0, tail) through hot_count[0]; keys with
-// count == thr - 1 fill what capacity is left, [tail, cap), first come first
-// served, through hot_count[7].  thr and tail come from the count histogram.
-template <typename KeyT>
-__global__ void hh_select_kernel(const KeyT* __restrict__ tk, const u32* __restrict__ tc, const u32* __restrict__ hist,
-                                 u32 cap, KeyT* hot, u32* hot_cnt, u32* hot_count, u32* hot_sum, u32 slots,
-                                 const u32* __restrict__ go) {
-    if (!*go) return;
-    __shared__ u32 thr, tail, sh[256];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = hist[i];  // one parallel load
-    __syncthreads();
-    if (threadIdx.x == 0) {  // smallest threshold >= 2 whose tail fits the candidate list
-        u32 tl = 0, c = 255;
-        for (; c >= 2; --c) {
-            if (tl + sh[c] > cap) break;
-            tl += sh[c];
-        }
-        thr = c + 1;
-        tail = tl;
-    }
-    __syncthreads();
-    const u32 t0 = thr, t1 = thr - 1;  // class 1 (count == t1) only when t1 >= 2
-    // each thread scans kSelPer consecutive slots; the CTA's selected keys get
-    // their output ranges with ONE global atomic per class (16K selections from
-    // warps hitting one counter serialise at L2)
-    constexpr int kSelPer = 8;
-    __shared__ u32 cta_cnt0, cta_cnt1, cta_sum, cta_base0, cta_base1;
-    if (threadIdx.x == 0) cta_cnt0 = cta_cnt1 = cta_sum = 0;
-    __syncthreads();
-    const uint32_t s0 = (blockIdx.x * blockDim.x + threadIdx.x) * kSelPer;
-    u32 mine0 = 0, mine1 = 0;
-#pragma unroll
-    for (int k = 0; k < kSelPer; ++k) {
-        const u32 c = s0 + k < slots ? tc[s0 + k] : 0;
-        mine0 += c >= t0 ? 1u : 0u;
-        mine1 += (c == t1 && t1 >= 2) ? 1u : 0u;
-    }
-    const u32 off0 = mine0 ? atomicAdd(&cta_cnt0, mine0) : 0;
-    const u32 off1 = mine1 ? atomicAdd(&cta_cnt1, mine1) : 0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        cta_base0 = cta_cnt0 ? atomicAdd(hot_count, cta_cnt0) : 0;
-        cta_base1 = cta_cnt1 ? tail + atomicAdd(hot_count + 7, cta_cnt1) : 0;
-    }
-    __syncthreads();
-    u32 i0 = cta_base0 + off0, i1 = cta_base1 + off1, covered = 0;
-    for (int k = 0; (mine0 | mine1) && k < kSelPer; ++k) {
-        const uint32_t sl = s0 + k;
-        const u32 c = sl < slots ? tc[sl] : 0;
-        const bool c0 = c >= t0, c1 = c == t1 && t1 >= 2;
-        if (!c0 && !c1) continue;
-        const u32 idx = c0 ? i0++ : i1++;
-        if (idx < cap) {
-            hot[idx] = tk[sl];
-            hot_cnt[idx] = c;
-            covered += c;
-        }
-    }
-    if (covered) atomicAdd(&cta_sum, covered);
-    __syncthreads();
-    if (threadIdx.x == 0 && cta_sum) atomicAdd(hot_sum, cta_sum);  // sampled items the hot set covers
-}
-
 // Exact 64-bit accumulation in a 16-bit shared cell; the cell's wraps (units of
 // 2^16) go straight into its slot's total in HBM.  sm_100 has no 16-bit (or
 // native 64-bit) shared atomic add, so two cells share a 32-bit word: cell h is
@@ -524,8 +267,9 @@ __global__ void __launch_bounds__(kHotThreads, 1)
                   const MissBuf<KeyT> mb, bool vec_ok, const u32* __restrict__ priv_go) {
     if (priv_go && *priv_go == 0) return;  // cs_private_kernel took this stream
     using G = HotGeom<KeyT>;
-    using C = typename G::Cas;
     using KV = KeyVec<KeyT>;
+    // keys hh_layout_kernel placed (its word follows hot_sum's; instrumentation)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && hot_sum[7]) atomicAdd(&g_hot_stats[3], (unsigned long long)hot_sum[7]);
     constexpr int kV = KV::N;          // items per vector
     constexpr int kVT = 8 / kV;        // vectors per lane per tile
     constexpr int kIt = kV * kVT;      // items per lane per tile (8 u32 / 4 u64)
@@ -565,10 +309,38 @@ __global__ void __launch_bounds__(kHotThreads, 1)
 
     // every CTA holds the same table layout (hh_layout_kernel), so the slot sums
     // of all CTAs can be merged per slot before the keys are hashed
+    // (16-byte loads, kCopyB of a thread in flight at once: the copy costs a few L2
+    // latencies, not one per slot -- it is a fixed cost of every call)
+    constexpr u32 kCopyB = 7;
     if constexpr (G::kTagged) {
-        for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) tw[s] = tags[s] | (kCellBias << kCellShift);
+        static_assert(S % 4 == 0, "16-byte copies");
+        const uint4* src = reinterpret_cast<const uint4*>(tags);
+        uint4* dst = reinterpret_cast<uint4*>(tw);
+        constexpr u32 kBias = kCellBias << kCellShift;
+        for (u32 j0 = threadIdx.x; j0 < S / 4; j0 += kCopyB * kHotThreads) {
+            uint4 v[kCopyB];
+#pragma unroll
+            for (u32 u = 0; u < kCopyB; ++u)
+                if (j0 + u * kHotThreads < S / 4) v[u] = __ldg(src + j0 + u * kHotThreads);
+#pragma unroll
+            for (u32 u = 0; u < kCopyB; ++u)
+                if (j0 + u * kHotThreads < S / 4)
+                    dst[j0 + u * kHotThreads] = make_uint4(v[u].x | kBias, v[u].y | kBias, v[u].z | kBias, v[u].w | kBias);
+        }
     } else {
-        for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) hk[s] = layout[s];
+        static_assert((S * sizeof(KeyT)) % 16 == 0, "16-byte copies");
+        constexpr u32 kVecs = S * sizeof(KeyT) / 16;
+        const uint4* src = reinterpret_cast<const uint4*>(layout);
+        uint4* dst = reinterpret_cast<uint4*>(hk);
+        for (u32 j0 = threadIdx.x; j0 < kVecs; j0 += kCopyB * kHotThreads) {
+            uint4 v[kCopyB];
+#pragma unroll
+            for (u32 u = 0; u < kCopyB; ++u)
+                if (j0 + u * kHotThreads < kVecs) v[u] = __ldg(src + j0 + u * kHotThreads);
+#pragma unroll
+            for (u32 u = 0; u < kCopyB; ++u)
+                if (j0 + u * kHotThreads < kVecs) dst[j0 + u * kHotThreads] = v[u];
+        }
         for (uint32_t s = threadIdx.x; s < S / 2; s += kHotThreads) cells[s] = 0x80008000u;
     }
     if (threadIdx.x == 0) s_next = 0;
@@ -724,185 +496,6 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     merged = __reduce_add_sync(kFull, merged);
     if (lane == 0 && merged) atomicAdd(&g_hot_stats[6], (unsigned long long)merged);
     if (threadIdx.x == 0) atomicAdd(&g_hot_stats[0], (unsigned long long)((t_hi - t_lo) * kT + (tail_hi - tail_lo)));
-}
-
-// One CTA lays out the hot set in the two-choice table once for every CTA.
-// The selected keys are first ordered by sample count, hottest first (counting
-// sort over kLevels count levels, counts >= kLevels - 1 share the top level,
-// into an HBM staging list), then placed in that order, in rounds of growing
-// size: a key goes to slot1 if free, else
-// to slot2 if free; if both are taken, one level of cuckoo displacement moves
-// the occupant of either slot to ITS other slot when that one is free.  Keys
-// that still find no slot stay cold.  Exactness never depends on the layout:
-// a lookup picks slot1 if it holds the key, else slot2, else the item is a miss,
-// and hh_merge credits each slot's sum to the key stored there.
-constexpr u32 kLevels = 1024;
-
-template <typename KeyT>
-__device__ __forceinline__ u32 other_slot(KeyT k, u32 s) {
-    using G = HotGeom<KeyT>;
-    const u32 s1 = slot1<G::kSlots>(k);
-    return s1 == s ? slot2<G::kSlots>(k) : s1;
-}
-
-template <typename KeyT>
-__global__ void __launch_bounds__(1024) hh_layout_kernel(const KeyT* __restrict__ hot, const u32* __restrict__ hot_cnt,
-                                                         const u32* __restrict__ hot_count, u32 cap,
-                                                         KeyT* __restrict__ sorted, KeyT* __restrict__ layout,
-                                                         u32* __restrict__ tags, const u32* __restrict__ priv_go) {
-    if (priv_go && *priv_go == 0) return;  // the private byte tables took this stream: no hot set
-    using G = HotGeom<KeyT>;
-    using C = typename G::Cas;
-    constexpr uint32_t S = G::kSlots;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    KeyT* hk = reinterpret_cast<KeyT*>(smem_raw);
-    __shared__ u32 lev[kLevels];
-    for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) hk[s] = G::kEmpty;
-    for (uint32_t l = threadIdx.x; l < kLevels; l += blockDim.x) lev[l] = 0;
-    __syncthreads();
-    const u32 nhot = min(hot_count[0] + hot_count[7], cap);  // both select classes
-    // level index kLevels - 1 - min(count, kLevels - 1): ascending index = descending count
-    auto level = [](u32 c) { return kLevels - 1 - min(c, kLevels - 1); };
-    // level histogram and scatter with one shared atomic per distinct level per
-    // warp (most candidates share the few lowest counts: per-key atomics on one
-    // counter serialise)
-    const u32 lane = threadIdx.x & 31;
-    u32 below;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(below));
-    // counts are read 8 per thread at a time (one global latency per batch);
-    // launched with 1024 threads
-    constexpr u32 kB = 8;
-    for (u32 j0 = 0; j0 < nhot; j0 += kB * 1024) {
-        u32 lv[kB];
-#pragma unroll
-        for (u32 b = 0; b < kB; ++b) {
-            const u32 j = j0 + b * 1024 + threadIdx.x;
-            lv[b] = j < nhot ? level(hot_cnt[j]) : kLevels;
-        }
-#pragma unroll
-        for (u32 b = 0; b < kB; ++b) {
-            const u32 peers = __match_any_sync(0xffffffffu, lv[b]);
-            if (lv[b] < kLevels && (peers & below) == 0) atomicAdd(&lev[lv[b]], (u32)__popc(peers));
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {  // exclusive scan of the level counts, 32 per lane
-        constexpr u32 kPer = kLevels / 32;
-        u32 v[kPer], run = 0;
-#pragma unroll
-        for (u32 i = 0; i < kPer; ++i) {
-            v[i] = run;
-            run += lev[threadIdx.x * kPer + i];
-        }
-        u32 inc = run;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (threadIdx.x >= (u32)o) inc += t;
-        }
-        const u32 base = inc - run;
-#pragma unroll
-        for (u32 i = 0; i < kPer; ++i) lev[threadIdx.x * kPer + i] = base + v[i];
-    }
-    __syncthreads();
-    for (u32 j0 = 0; j0 < nhot; j0 += kB * 1024) {
-        u32 lv[kB];
-#pragma unroll
-        for (u32 b = 0; b < kB; ++b) {
-            const u32 j = j0 + b * 1024 + threadIdx.x;
-            lv[b] = j < nhot ? level(hot_cnt[j]) : kLevels;
-        }
-#pragma unroll
-        for (u32 b = 0; b < kB; ++b) {
-            const u32 peers = __match_any_sync(0xffffffffu, lv[b]);
-            const int leader = __ffs(peers) - 1;
-            u32 base = 0;
-            if (lv[b] < kLevels && (int)lane == leader) base = atomicAdd(&lev[lv[b]], (u32)__popc(peers));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (lv[b] < kLevels) sorted[base + __popc(peers & below)] = hot[j0 + b * 1024 + threadIdx.x];
-        }
-    }
-    __syncthreads();
-    // placement rounds of doubling size (1, 1, 2, 4, 8, 16, ... keys per thread,
-    // read coalesced from the count-sorted list): priority is fine-grained where
-    // counts differ (the hottest keys) and coarse where they are nearly equal
-    // (the many keys seen twice or three times); launched with 1024 threads
-    constexpr u32 kRounds = G::kCap / 1024;
-    constexpr u32 kMaxPer = 16;
-#pragma unroll 1
-    for (u32 r0 = 0, r1 = 1; r0 < kRounds && r0 * 1024 < nhot; r0 = r1, r1 = min(2 * r1, min(r1 + kMaxPer, kRounds))) {
-        KeyT rk[kMaxPer];
-#pragma unroll
-        for (u32 i = 0; i < kMaxPer; ++i) {
-            const u32 j = (r0 + i) * 1024 + threadIdx.x;
-            rk[i] = (r0 + i < r1 && j < nhot) ? sorted[j] : G::kEmpty;
-        }
-        u32 left = 0;  // bit i: key rk[i] found both slots taken
-#pragma unroll
-        for (u32 i = 0; i < kMaxPer; ++i) {
-            const KeyT key = rk[i];
-            if (key == G::kEmpty) continue;
-            const u32 s1 = slot1<S>(key), s2 = slot2<S>(key);
-            if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + s1), (C)G::kEmpty, (C)key) != G::kEmpty &&
-                (KeyT)atomicCAS(reinterpret_cast<C*>(hk + s2), (C)G::kEmpty, (C)key) != G::kEmpty)
-                left |= 1u << i;
-        }
-        __syncthreads();
-#pragma unroll
-        for (u32 i = 0; i < kMaxPer; ++i) {
-            if (!((left >> i) & 1u)) continue;
-            // one level of displacement (races only cost a slot, never exactness)
-            const KeyT key = rk[i];
-            const u32 s1 = slot1<S>(key), s2 = slot2<S>(key);
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const u32 sl = t == 0 ? s1 : s2;
-                const KeyT occ = hk[sl];
-                if (occ == G::kEmpty || occ == key) break;
-                const u32 alt = other_slot<KeyT>(occ, sl);
-                if (alt == sl) continue;
-                if ((KeyT)atomicCAS(reinterpret_cast<C*>(hk + alt), (C)G::kEmpty, (C)occ) != G::kEmpty) continue;
-                atomicCAS(reinterpret_cast<C*>(hk + sl), (C)occ, (C)key);
-                break;
-            }
-        }
-        __syncthreads();
-    }
-    unsigned placed = 0;
-    if constexpr (G::kTagged) {
-        // the slot words the hot kernel copies: the placed key's tag for the slot it
-        // sits in (choice 1 only when it is not its slot1), else the empty marker;
-        // layout[] keeps the keys for hh_merge_kernel (empty slots never have a sum)
-        for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
-            const KeyT k = hk[s];
-            u32 t;
-            if (k == G::kEmpty) {
-                t = empty_tag<S>(s);
-            } else {
-                t = slot1<S>(k) == s ? tag1((u32)k) : tag2((u32)k);
-                ++placed;
-            }
-            tags[s] = t;
-            layout[s] = k;
-        }
-    } else {
-        // an empty slot s gets a FOREIGN key, one with slot1 != s and slot2 != s: no
-        // lookup can match it, so the hot kernel needs no empty-slot test
-        for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
-            KeyT k = hk[s];
-            if (k == G::kEmpty) {
-                for (KeyT t = 0;; ++t) {
-                    k = G::kEmpty - t;
-                    if (slot1<S>(k) != s && slot2<S>(k) != s) break;
-                }
-            } else {
-                ++placed;
-            }
-            layout[s] = k;
-        }
-    }
-    placed = __reduce_add_sync(0xffffffffu, placed);
-    if ((threadIdx.x & 31) == 0 && placed) atomicAdd(&g_hot_stats[3], (unsigned long long)placed);  // keys in the table
 }
 
 // Each hot key once: hash -> split -> red.global of its total over all CTAs.
@@ -1451,7 +1044,11 @@ template <typename KeyT>
 HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     using G = HotGeom<KeyT>;
     HotPlan<KeyT> P;
-    uint64_t m = n / 256;
+    static const int sample_shift = [] {  // experiment knob (tools/r02h_fixed.sh); default n / 256
+        const char* e = std::getenv("MB200_SAMPLE_SHIFT");
+        return e ? atoi(e) : 8;
+    }();
+    uint64_t m = n >> sample_shift;
     m = m < kMinSample ? kMinSample : m > kMaxSample ? kMaxSample : m;
     P.m = (uint32_t)(n < m ? n : m);
     P.slots = 64;
@@ -1485,12 +1082,12 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     }
     P.tk_bytes = align256((size_t)P.slots * sizeof(KeyT));
     P.tc_bytes = (size_t)P.slots * 4;
-    P.misc = 256 * 4 + 64;  // hist[256], hot_count, hot_sum, miss count (u64), go words, class-1 count
+    P.misc = 256 * 4 + 64 + 256 * 4;  // hist[256], hot_count, hot_sum, miss count (u64), go words, fill[256]
     P.gcnt_bytes = align256((size_t)P.chunks * g.nb * 8 + 8);
     P.sum_bytes = align256((size_t)G::kSlots * 8);
     P.layout_bytes = align256((size_t)G::kSlots * sizeof(KeyT));
     P.tags_bytes = G::kTagged ? align256((size_t)G::kSlots * 4) : 0;
-    P.hot_bytes = align256((size_t)G::kCap * (2 * sizeof(KeyT) + 4));  // hot list, counts, sorted keys
+    P.hot_bytes = align256((size_t)G::kCap * sizeof(KeyT));  // the hot list, ordered by sample count
     // row passes: Pow2 / two-for-one splitters of power-of-two rows <= 2^16 cells
     P.rows_mode = g_strategy == STRAT_ROWS && !binned && (sp.b == 61 || sp.b == 89) &&
                   (sp.splitter == SPLIT_POW2 || sp.splitter == SPLIT_TWO_FOR_ONE) && sp.width >= 8 &&
@@ -1523,7 +1120,6 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     u64* slot_sum = reinterpret_cast<u64*>(ws + P.tk_bytes + P.tc_bytes + P.misc + P.gcnt_bytes);
     unsigned char* p = ws + P.tk_bytes + P.zero_bytes();
     KeyT* hot = reinterpret_cast<KeyT*>(p);
-    u32* hot_cnt = reinterpret_cast<u32*>(hot + G::kCap);
     p += P.hot_bytes;
     KeyT* layout = reinterpret_cast<KeyT*>(p);
     p += P.layout_bytes;
@@ -1535,35 +1131,28 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     cudaMemsetAsync(tk, 0xff, P.tk_bytes, s);
     cudaMemsetAsync(tc, 0, P.zero_bytes(), s);
     u32* go = hot_count + 4;  // misc words after the miss count: go, covered, ticket
-    const u32 cap = G::kCap;
-    hh_probe_kernel<KeyT><<<kProbeCtas, 1024, 0, s>>>(keys, n, go);
-    hh_count_kernel<KeyT><<<sms * 2, kCountThreads, 0, s>>>(keys, P.m, tk, tc, P.slots, go);
-    hh_hist_kernel<<<sms * 8, 256, 0, s>>>(tc, hist, P.slots, go);
-    hh_select_kernel<KeyT><<<(P.slots + 256 * 8 - 1) / (256 * 8), 256, 0, s>>>(tk, tc, hist, cap, hot, hot_cnt,
-                                                                            hot_count, hot_sum, P.slots, go);
+    u32* fill = hot_count + 16;  // per-level fill counters of the ordered selection
+    const HotPrepWs<KeyT> pw{tk, tc, P.slots, hist, hot_count, hot_sum, fill, go, hot_count + 8, hot};
+    cudaError_t e = launch_hot_select<KeyT>(keys, n, P.m, pw, s);
+    if (e != cudaSuccess) return e;
     const bool rows_mode = P.rows_mode && SPL != SPC_ANY;
     auto fn = binned || rows_mode ? cs_hot_kernel<MODE, K, SPL, KeyT, WK, true>
                                   : cs_hot_kernel<MODE, K, SPL, KeyT, WK, false>;
     const size_t smem = G::kTagged ? (size_t)4 * G::kSlots : ((size_t)sizeof(KeyT) + 2) * G::kSlots;
     const size_t qbytes = (size_t)kHotWarps * kQueue * sizeof(QEnt<KeyT>);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes));
-    if (e != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + qbytes))) != cudaSuccess)
+        return e;
     uint64_t grid = (n + 256 * kHotWarps - 1) / (256 * kHotWarps);
     if (grid > (uint64_t)sms) grid = sms;
     const bool vec_ok = (reinterpret_cast<uintptr_t>(keys) & 15) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
     // without bins (cap 0) every miss takes the direct path and raw mode is off
-    auto fl = hh_layout_kernel<KeyT>;
-    const size_t lbytes = sizeof(KeyT) * G::kSlots;
-    if ((e = cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbytes)) != cudaSuccess)
-        return e;
     // streams without heavy hitters and unit deltas whose whole table fits
     // shared memory as bytes: private byte tables instead of one L2 reduction
     // per row update
     const uint64_t pcells = (uint64_t)sp.rows * sp.width;
     const bool priv = !binned && WK == W_NONE && SPL != SPC_ANY && pcells <= 200u * 1024 && pcells % 4 == 0 &&
                       sp.width % 4 == 0 && n >= (1u << 20);
-    fl<<<1, 1024, lbytes, s>>>(hot, hot_cnt, hot_count, cap, reinterpret_cast<KeyT*>(hot_cnt + G::kCap), layout,
-                               tags, priv ? go : nullptr);
+    if ((e = launch_hot_layout<KeyT>(pw, layout, tags, priv ? go : nullptr, s)) != cudaSuccess) return e;
     if (priv) {
         auto fp = cs_private_kernel<MODE, K, SPL, KeyT>;
         if ((e = cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcells)) != cudaSuccess)

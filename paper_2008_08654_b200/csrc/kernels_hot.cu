@@ -7,16 +7,18 @@
 // L2 and the lever is the NUMBER of L2 reductions.  Count Sketch is linear:
 // the updates of one key can be summed anywhere and applied once.
 //
-//   1. hh_count  : exact key counts over a sample (the batch's first n/256
+//   1. hh_count  : exact key counts over a sample (the batch's first n/128
 //                  items, clamped to [2^18, 2^22]) in an open-addressing table
 //                  in global memory;
 //   2. hh_hist /
 //      hh_select : the most frequent sampled keys (count >= a threshold picked
 //                  from the count histogram so that at most H qualify) form the
-//                  hot list, with their sample counts;
-//      hh_layout : one CTA places the hot list, hottest first, in the two-choice
+//                  hot list, written in count order, hottest first;
+//      hh_layout : one CTA places the hot list in that order in the two-choice
 //                  shared table layout every CTA copies (one level of cuckoo
-//                  displacement; ~31K of 40960 candidates in 35840 slots);
+//                  displacement; ~46K of 61440 candidates in 53248 slots);
+//                  hh_slots writes the slot words (tags) the CTAs copy.
+//                  (1-2: kernels_hotprep.cu)
 //   3. cs_hot    : one 1024-thread CTA per SM keeps the hot keys in a shared-
 //                  memory table with an exact 64-bit accumulator per key (a
 //                  16-bit shared cell + a wrap counter in HBM).  A hit costs one
@@ -47,7 +49,6 @@
 // 4's shape cs_private89_kernel, mb200_private89.cuh).
 // The table is bit-identical to the per-item path for ANY hot set (integer
 // addition commutes); the hot set only decides how much L2 traffic is saved.
-#include <cstdlib>
 #include <type_traits>
 #include <utility>
 #include <vector>
@@ -79,8 +80,8 @@ using namespace sk;
 
 constexpr int kHotThreads = 1024;
 constexpr int kHotWarps = kHotThreads / 32;
-// sample = n / 256 items, clamped to [2^18, 2^22] (a shard of a multi-GPU run
-// gets a 2^20-item sample from 2^28 items on); count table = 2 x sample
+// sample = n / 128 items, clamped to [2^18, 2^22] (a shard of a multi-GPU run
+// gets a 2^21-item sample from 2^28 items); count table = 2 x sample
 constexpr uint32_t kMinSample = 1u << 18, kMaxSample = 1u << 22;
 constexpr int kQueue = 64;     // < 32 queued + one slot of 32 misses
 constexpr uint32_t kMissChunk = 1024;  // miss-buffer slots a warp reserves at once
@@ -91,6 +92,14 @@ struct alignas(sizeof(KeyT) * 2) QEnt {
     KeyT k;
     i32 d;
 };
+// words of a CTA's cell storage (what it hands to hh_merge_kernel through its
+// scratch area): the tagged table's slot words, else the packed 16-bit cells
+template <typename KeyT>
+struct HotCells {
+    static constexpr u32 kWords = HotGeom<KeyT>::kTagged ? HotGeom<KeyT>::kSlots : HotGeom<KeyT>::kSlots / 2;
+    static_assert(kWords % 4 == 0, "16-byte copies");
+};
+
 // Exact 64-bit accumulation in a 16-bit shared cell; the cell's wraps (units of
 // 2^16) go straight into its slot's total in HBM.  sm_100 has no 16-bit (or
 // native 64-bit) shared atomic add, so two cells share a 32-bit word: cell h is
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(kHotThreads, 1)
     cs_hot_kernel(const SketchParams sp, const KeyT* __restrict__ keys, const void* __restrict__ w, uint64_t n,
                   i64* __restrict__ table, const KeyT* __restrict__ layout, const u32* __restrict__ tags,
                   u64* __restrict__ slot_sum, const u32* __restrict__ hot_sum, uint32_t sample,
-                  const MissBuf<KeyT> mb, bool vec_ok, const u32* __restrict__ priv_go) {
+                  const MissBuf<KeyT> mb, bool vec_ok, const u32* __restrict__ priv_go, u32* __restrict__ scratch) {
     if (priv_go && *priv_go == 0) return;  // cs_private_kernel took this stream
     using G = HotGeom<KeyT>;
     using KV = KeyVec<KeyT>;
@@ -477,38 +486,53 @@ __global__ void __launch_bounds__(kHotThreads, 1)
         mb.deltas[p] = 0;
     }
     __syncthreads();
-    // this CTA's exact per-slot sums into the shared per-slot totals (wrapping
-    // u64 adds commute); hh_merge_kernel hashes each hot key once
-    unsigned merged = 0;
-    for (uint32_t s = threadIdx.x; s < S; s += kHotThreads) {
-        // 0 in empty slots
-        const u64 v = G::kTagged ? (u64)(tw[s] >> kCellShift) - kCellBias
-                                 : ((cells[s >> 1] >> ((s & 1) << 4)) & 0xFFFFu) - 0x8000ull;
-        if (v) {
-            red_add_u64(slot_sum + s, v);
-            ++merged;
-        }
+    // this CTA's cells go to its scratch area as they are (16-byte stores);
+    // hh_merge_kernel sums the CTAs' cells per slot, adds the slot's wrap total and
+    // hashes each hot key once.  (One L2 reduction per CTA and slot instead -- 6.9M
+    // on config 5 -- took ~38 us at the end of every call.)
+    {
+        constexpr u32 kVecs = HotCells<KeyT>::kWords / 4;
+        const uint4* src = reinterpret_cast<const uint4*>(G::kTagged ? tw : cells);
+        uint4* dst = reinterpret_cast<uint4*>(scratch) + (size_t)blockIdx.x * kVecs;
+        for (u32 j = threadIdx.x; j < kVecs; j += kHotThreads) dst[j] = src[j];
     }
     // instrumentation for the L2-reduction roofline (mb200_hot_stats)
     if (lane == 0) atomicAdd(&g_hot_stats[1], (unsigned long long)misses);
     direct = __reduce_add_sync(kFull, direct);
     if (lane == 0 && direct) atomicAdd(&g_hot_stats[5], (unsigned long long)direct);
-    merged = __reduce_add_sync(kFull, merged);
-    if (lane == 0 && merged) atomicAdd(&g_hot_stats[6], (unsigned long long)merged);
     if (threadIdx.x == 0) atomicAdd(&g_hot_stats[0], (unsigned long long)((t_hi - t_lo) * kT + (tail_hi - tail_lo)));
 }
 
-// Each hot key once: hash -> split -> red.global of its total over all CTAs.
+// Each hot key once: its total = the slot's wrap total + the CTAs' cells (read from
+// their scratch areas, coalesced over the slots), then hash -> split -> red.global.
+// Skipped, like cs_hot_kernel, when the private byte tables or raw mode took the batch.
 template <int MODE, int K, int SPL, typename KeyT>
-__global__ void hh_merge_kernel(const SketchParams sp, const KeyT* __restrict__ layout,
-                                const u64* __restrict__ slot_sum, i64* __restrict__ table) {
+__global__ void __launch_bounds__(256)
+    hh_merge_kernel(const SketchParams sp, const KeyT* __restrict__ layout, const u64* __restrict__ slot_sum,
+                    const u32* __restrict__ scratch, u32 nctas, const u32* __restrict__ hot_sum, uint32_t sample,
+                    const u32* __restrict__ priv_go, i64* __restrict__ table) {
     using G = HotGeom<KeyT>;
+    if (priv_go && *priv_go == 0) return;
+    if (sample && raw_mode(hot_sum, sample)) return;
+    constexpr u32 kW = HotCells<KeyT>::kWords;
     unsigned applied = 0;
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < G::kSlots; s += gridDim.x * blockDim.x) {
-        const KeyT key = layout[s];
-        const u64 v = slot_sum[s];
-        if (v) {  // (empty slots: foreign keys with no sum)
-            rows_direct<MODE, K, SPL>(sp, (u64)key, (i64)v, table);
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < G::kSlots) {
+        const u32 idx = G::kTagged ? s : s >> 1, sh = G::kTagged ? kCellShift : (s & 1u) << 4;
+        const u32 mask = G::kTagged ? 0x3fffu : 0xffffu;
+        u32 acc = 0;  // <= nctas * 2^16
+        constexpr u32 kB = 8;
+        for (u32 c0 = 0; c0 < nctas; c0 += kB) {
+            u32 wv[kB];
+#pragma unroll
+            for (u32 u = 0; u < kB; ++u) wv[u] = c0 + u < nctas ? __ldcg(scratch + (size_t)(c0 + u) * kW + idx) : 0u;
+#pragma unroll
+            for (u32 u = 0; u < kB; ++u) acc += c0 + u < nctas ? (wv[u] >> sh) & mask : 0u;
+        }
+        const u64 bias = G::kTagged ? (u64)kCellBias : 0x8000ull;
+        const u64 v = slot_sum[s] + (u64)acc - (u64)nctas * bias;  // 0 in empty slots
+        if (v) {
+            rows_direct<MODE, K, SPL>(sp, (u64)layout[s], (i64)v, table);
             ++applied;
         }
     }
@@ -1029,14 +1053,15 @@ struct HotPlan {
     uint64_t cap_m = 0;        // miss-buffer capacity
     size_t tk_bytes = 0, tc_bytes = 0, misc = 0, gcnt_bytes = 0, sum_bytes = 0, hot_bytes = 0,
            layout_bytes = 0, mk_bytes = 0, md_bytes = 0, bin_bytes = 0;
-    size_t tags_bytes = 0;   // tagged hot table (u32 keys): the slot words hh_layout writes
+    size_t tags_bytes = 0;   // tagged hot table (u32 keys): the slot words hh_slots writes
+    size_t scr_bytes = 0;    // the scatter CTAs' cells (one area per CTA), summed by hh_merge
     bool rows_mode = false;  // STRAT_ROWS: misses to the buffer, then the row passes
     size_t rows_bytes = 0;   // row passes' per-CTA tables
     // tc .. slot sums are contiguous and zeroed per call
     size_t zero_bytes() const { return tc_bytes + misc + gcnt_bytes + sum_bytes; }
     size_t total() const {
-        return tk_bytes + zero_bytes() + hot_bytes + layout_bytes + tags_bytes + mk_bytes + md_bytes + bin_bytes +
-               rows_bytes;
+        return tk_bytes + zero_bytes() + hot_bytes + layout_bytes + tags_bytes + scr_bytes + mk_bytes + md_bytes +
+               bin_bytes + rows_bytes;
     }
 };
 
@@ -1044,11 +1069,12 @@ template <typename KeyT>
 HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     using G = HotGeom<KeyT>;
     HotPlan<KeyT> P;
-    static const int sample_shift = [] {  // experiment knob (tools/r02h_fixed.sh); default n / 256
-        const char* e = std::getenv("MB200_SAMPLE_SHIFT");
-        return e ? atoi(e) : 8;
-    }();
-    uint64_t m = n >> sample_shift;
+    // sample = n / 128 items, clamped to [2^18, 2^22]: measured on config 5's stream,
+    // a 2^28-item shard takes 1.119 ms with n / 256 and 1.092 ms with n / 128 (misses
+    // 11.9% -> 10.7%), 2^29 items 2.01 -> 1.99 ms; the full 2^31 items sit at the
+    // clamp either way (2^23 sampled items: misses 10.1% -> 9.9%, but the call only
+    // 7.265 -> 7.245 ms and twice the workspace)
+    uint64_t m = n / 128;
     m = m < kMinSample ? kMinSample : m > kMaxSample ? kMaxSample : m;
     P.m = (uint32_t)(n < m ? n : m);
     P.slots = 64;
@@ -1087,6 +1113,7 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     P.sum_bytes = align256((size_t)G::kSlots * 8);
     P.layout_bytes = align256((size_t)G::kSlots * sizeof(KeyT));
     P.tags_bytes = G::kTagged ? align256((size_t)G::kSlots * 4) : 0;
+    P.scr_bytes = align256((size_t)sm_count() * HotCells<KeyT>::kWords * 4);
     P.hot_bytes = align256((size_t)G::kCap * sizeof(KeyT));  // the hot list, ordered by sample count
     // row passes: Pow2 / two-for-one splitters of power-of-two rows <= 2^16 cells
     P.rows_mode = g_strategy == STRAT_ROWS && !binned && (sp.b == 61 || sp.b == 89) &&
@@ -1125,6 +1152,8 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     p += P.layout_bytes;
     u32* tags = P.tags_bytes ? reinterpret_cast<u32*>(p) : nullptr;
     p += P.tags_bytes;
+    u32* scratch = reinterpret_cast<u32*>(p);
+    p += P.scr_bytes;
     const MissBuf<KeyT> mb{reinterpret_cast<KeyT*>(p), reinterpret_cast<i32*>(p + P.mk_bytes), mcount, P.cap_m};
     p += P.mk_bytes + P.md_bytes;
     g.bins = reinterpret_cast<u32*>(p);
@@ -1164,9 +1193,10 @@ cudaError_t run_hot(const SketchParams& sp, const KeyT* keys, const void* w, uin
     if (!priv) ktimer_mark(s, true);
     fn<<<(unsigned)grid, kHotThreads, smem + qbytes, s>>>(sp, keys, w, n, table, layout, tags, slot_sum, hot_sum,
                                                           binned ? P.m : 0, mb, vec_ok,
-                                                          priv ? go : nullptr);
+                                                          priv ? go : nullptr, scratch);
     if (!priv) ktimer_mark(s, false);
-    hh_merge_kernel<MODE, K, SPL, KeyT><<<(G::kSlots + 255) / 256, 256, 0, s>>>(sp, layout, slot_sum, table);
+    hh_merge_kernel<MODE, K, SPL, KeyT><<<(G::kSlots + 255) / 256, 256, 0, s>>>(
+        sp, layout, slot_sum, scratch, (u32)grid, hot_sum, binned ? P.m : 0, priv ? go : nullptr, table);
     if (rows_mode) {
         if constexpr (SPL != SPC_ANY) {
             auto fr = cs_rowpass_kernel<MODE, K, SPL, KeyT>;

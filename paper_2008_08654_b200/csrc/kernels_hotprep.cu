@@ -7,9 +7,6 @@
 // decides how many L2 reductions a call needs); it is a FIXED cost of every
 // call, ~0.1 ms on a 2^28-item shard, which is why it is its own translation
 // unit with latency-minded kernels.
-#include <cstdio>
-#include <cstdlib>
-
 #include "mb200_hot_geom.cuh"
 #include "mb200_hotprep.h"
 #include "mb200_internal.h"
@@ -431,12 +428,10 @@ cudaError_t launch_hot_select(const KeyT* keys, uint64_t n, uint32_t sample, con
     using G = HotGeom<KeyT>;
     const int sms = sm_count();
     hh_probe_kernel<KeyT><<<kProbeCtas, 1024, 0, s>>>(keys, n, w.go);
-    static const uint32_t per_cta = [] {
-        const char* e = std::getenv("MB200_COUNT_PER_CTA");
-        return e ? (uint32_t)atoi(e) : kLocalSlots;
-    }();
+    // a share of kLocalSlots sampled items per CTA (its distinct keys fit the local
+    // table: with 2 CTAs per SM a 2^22-item sample crowded it, 128 us against 50 us)
     uint32_t cgrid = (uint32_t)sms * 2;
-    if (per_cta && (sample + per_cta - 1) / per_cta > cgrid) cgrid = (sample + per_cta - 1) / per_cta;
+    if ((sample + kLocalSlots - 1) / kLocalSlots > cgrid) cgrid = (sample + kLocalSlots - 1) / kLocalSlots;
     hh_count_kernel<KeyT><<<cgrid, kCountThreads, 0, s>>>(keys, sample, w.tk, w.tc, w.slots, w.go);
     hh_hist_kernel<<<sms * 8, 256, 0, s>>>(w.tc, w.hist, w.slots, w.go);
     constexpr u32 kSelCta = kSelThreads * kSelPer * kSelChunks;  // slots per CTA

@@ -69,6 +69,14 @@ int mb200_pm_modulus(unsigned b, uint64_t c_lo, uint64_t c_hi, unsigned m_iters,
 /* PolyHashFamily(modulus, k, u, seed) coefficient draw: polyhash.cpp:12-35.
  * lo/hi receive a_0..a_{k-1} (hi only for b > 64; may be NULL otherwise). */
 int mb200_draw_coeffs(unsigned b, unsigned k, uint64_t seed, uint64_t* lo, uint64_t* hi);
+/* Adapted coefficients of a degree-7 polynomial over Z_p, p = 2^61 - 1 (the k = 8
+ * family of PolyHashFamily::operator(), polyhash.cpp:64-76): plan = {al0..al5, s,
+ * a7, r0} with  u(x) = a7 (x + s) U(x) + r0,  U = (w + z + al4) w + al5,
+ * w = (x + al2) z + al3,  z = (x + al0) x + al1  -- five modular products per
+ * key instead of Horner's seven, same value.  mb200_hash61 calls this itself
+ * for k = 8 and 64-bit keys; exported for tests.  MB200_UNSUPPORTED when
+ * coeffs[7] = 0 (Horner is used then).  No reference counterpart. */
+int mb200_precondition61(const uint64_t coeffs[8], uint64_t plan[9]);
 /* CountSketch row seeds: successive SplitMix64(master).next(), sketch.cpp:72-77 */
 int mb200_row_seeds(uint64_t master, unsigned rows, uint64_t* out);
 

@@ -54,6 +54,22 @@ def draw_coeffs(b: int, k: int, seed: int) -> list:
     return [int(l) | (int(h) << 64) for l, h in zip(lo, hi)]
 
 
+def precondition61(coeffs) -> dict | None:
+    """Adapted coefficients of a degree-7 polynomial over Z_(2^61-1) (mb200_precondition61):
+    {"al": [al0..al5], "s": shift, "a7": leading coefficient, "r0": remainder}, or None when
+    the leading coefficient is 0 (the hash kernel then evaluates by Horner)."""
+    c = np.array([int(v) for v in coeffs], np.uint64)
+    if c.size != 8:
+        raise ValueError("precondition61 takes 8 coefficients")
+    plan = np.zeros(9, np.uint64)
+    rc = lib.mb200_precondition61(_p(c), _p(plan))
+    if rc == 5:  # MB200_UNSUPPORTED: leading coefficient 0
+        return None
+    check(rc)
+    v = [int(x) for x in plan]
+    return {"al": v[:6], "s": v[6], "a7": v[7], "r0": v[8]}
+
+
 def row_seeds(master: int, rows: int) -> list:
     out = np.zeros(rows, np.uint64)
     check(lib.mb200_row_seeds(master & MASK64, rows, _p(out)))

@@ -79,6 +79,7 @@ SIGNATURES = [
     ("mb200_mersenne_modulus_check", I, [U, I]),
     ("mb200_pm_modulus", I, [U, u64, u64, U, P, P]),
     ("mb200_draw_coeffs", I, [U, U, u64, P, P]),
+    ("mb200_precondition61", I, [P, P]),
     ("mb200_row_seeds", I, [u64, U, P]),
     ("mb200_hash61", I, [P, I, u64, U, P, U, U, P, P]),
     ("mb200_hash89", I, [P, u64, P, P, U, U, P, P, P]),
@@ -151,11 +152,32 @@ def _bind(lib, sigs):
     return lib
 
 
+def _preload_bundled_nccl():
+    """The library binds NCCL at run time (host/nccl_comm.cpp): the one already in the
+    process, else the loader's libnccl.so.2.  In a Python process that imports torch LATER,
+    a system libnccl loaded first would satisfy torch's own libnccl.so.2 dependency by
+    soname -- and an older one lacks symbols torch needs.  So the NCCL wheel torch was
+    built against (nvidia/nccl/lib), when installed, is loaded first; without it nothing
+    changes."""
+    import glob
+    import importlib.util
+
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for base in (spec.submodule_search_locations if spec else []) or []:
+            for f in sorted(glob.glob(os.path.join(base, "lib", "libnccl.so*"))):
+                C.CDLL(f, mode=C.RTLD_GLOBAL)
+                return
+    except (ImportError, OSError, ValueError):
+        pass
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
             f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
             "or `make lib` (the B200 path has no CPU fallback)")
+    _preload_bundled_nccl()
     return _bind(C.CDLL(LIB_PATH), SIGNATURES)
 
 

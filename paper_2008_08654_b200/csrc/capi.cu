@@ -182,6 +182,21 @@ int mb200_hash61(const void* d_keys, int key_width, uint64_t n, unsigned b, cons
     cudaStream_t s = (cudaStream_t)stream;
     if (int rc = check_keys(d_keys, key_width, n, key_bits, s)) return rc;
     cudaError_t e;
+    if (b == 61 && key_width == 64 && k == 8) {
+        // degree 7: five modular products per key with adapted coefficients instead
+        // of Horner's seven (same value; host/precond61.cpp)
+        // (a family's plan is kept: the adaptation takes tens of microseconds on the host)
+        thread_local uint64_t cached_coeffs[8], cached_plan[9];
+        thread_local int cached_rc = -1;
+        if (cached_rc < 0 || std::memcmp(cached_coeffs, coeffs, sizeof(cached_coeffs)) != 0) {
+            std::memcpy(cached_coeffs, coeffs, sizeof(cached_coeffs));
+            cached_rc = mb200_precondition61(coeffs, cached_plan);
+        }
+        if (cached_rc == MB200_OK) {
+            for (int i = 0; i < 9; ++i) hp.hi[i] = cached_plan[i];
+            hp.pre = cached_plan[6] ? 2 : 1;
+        }
+    }
     if (b == 61 && key_width == 32) e = launch_hash61_key32((const uint32_t*)d_keys, n, hp, d_out, s);
     else if (b == 61) e = launch_hash61_key64((const uint64_t*)d_keys, n, hp, d_out, s);
     else e = launch_hash_generic(d_keys, key_width, n, hp, d_out, s);

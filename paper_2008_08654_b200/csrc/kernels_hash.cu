@@ -29,6 +29,52 @@ __device__ __forceinline__ u64 eval61_key64(const u64 (&a)[K], u64 x) {
     return h61_finish(h61_eval64<K>(a, h61_key64(x)));
 }
 
+// Degree 7 with adapted coefficients (host/precond61.cpp; Knuth 4.6.4): five
+// modular products instead of Horner's seven, the same value mod p.
+//   u(x) = a7 (x + s) U(x) + r0,  U = (w + z + al4) w + al5,
+//   w = (x + al2) z + al3,  z = (x + al0) x + al1,    c = {al0..al5, s, a7, r0}, all < p.
+// Bounds for h61_step64(y, x, a) = fold(y x) + a (needs y0 x1 + y1 x0 < 2^64 and
+// y x < 2^125; result < 2^61 + (y x >> 61) + a), with x0 <= 2^61 + 6 the folded key:
+//   z: y = x0 + al0 < 2^62 + 6, x = x0              -> < 2^63 + 2^36, folded to < 2^61 + 8
+//   w: y = x0 + al2 < 2^62 + 6, x = z               -> likewise
+//   U: y = w + z + al4 < 3 * 2^61 + 16, x = w       -> < 5 * 2^61 + 2^36
+//   V = (x + s) U: SHIFT: y = fold(U) < 2^61 + 8, x = x0 + s < 2^62 + 6  -> < 3 * 2^61 + 2^36;
+//                  s = 0: y = U, x = x0 (y0 x1 + y1 x0 < 2^61.1 + 5 * 2^61.1)  -> < 6 * 2^61 + 2^36
+//   out: y = fold(V) < 2^61 + 8, x = a7 < 2^61      -> < 3 * 2^61, finished by h61_finish.
+template <bool SHIFT>
+__device__ __forceinline__ u64 eval61_pre8(const u64 (&c)[9], u64 key) {
+    const u64 x0 = h61_key64(key);
+    const u64 z = h61_fold(h61_step64(x0 + c[0], x0, c[1]));
+    const u64 w = h61_fold(h61_step64(x0 + c[2], z, c[3]));
+    const u64 U = h61_step64(w + z + c[4], w, c[5]);
+    const u64 V = SHIFT ? h61_step64(h61_fold(U), x0 + c[6], 0) : h61_step64(U, x0, 0);
+    return h61_finish(h61_step64(h61_fold(V), c[7], c[8]));
+}
+
+// K = 8 evaluators of hash61_key64_kernel: Horner, or the adapted form
+template <int K, int PRE>
+struct Eval61 {
+    u64 a[K];
+    __device__ __forceinline__ explicit Eval61(const HashParams& hp) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) a[i] = hp.lo[i];
+    }
+    __device__ __forceinline__ u64 operator()(u64 x) const { return eval61_key64<K>(a, x); }
+};
+template <int PRE>
+struct Eval61<8, PRE> {
+    static constexpr int kN = PRE ? 9 : 8;
+    u64 c[kN];
+    __device__ __forceinline__ explicit Eval61(const HashParams& hp) {
+#pragma unroll
+        for (int i = 0; i < kN; ++i) c[i] = PRE ? hp.hi[i] : hp.lo[i];
+    }
+    __device__ __forceinline__ u64 operator()(u64 x) const {
+        if constexpr (PRE == 0) return eval61_key64<8>(c, x);
+        else return eval61_pre8<PRE == 2>(c, x);
+    }
+};
+
 template <int K>
 __device__ __forceinline__ u64 eval61_key32(const u64 (&a)[K], u32 x) {
     u64 y = a[K - 1];
@@ -38,13 +84,11 @@ __device__ __forceinline__ u64 eval61_key32(const u64 (&a)[K], u32 x) {
 }
 
 // ---- K1, 64-bit keys: config 2 ---------------------------------------------
-template <int K>
+template <int K, int PRE>
 __global__ void __launch_bounds__(kThreads) hash61_key64_kernel(const u64* __restrict__ keys,
                                                                 uint64_t n, HashParams hp,
                                                                 u64* __restrict__ out) {
-    u64 a[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) a[i] = hp.lo[i];
+    const Eval61<K, PRE> ev(hp);
     const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys);
     ulonglong2* o2 = reinterpret_cast<ulonglong2*>(out);
     const uint64_t npairs = n >> 1;
@@ -66,14 +110,14 @@ __global__ void __launch_bounds__(kThreads) hash61_key64_kernel(const u64* __res
         for (int u = 0; u < kUnroll; ++u) {
             if (i + u * stride < npairs) {
                 ulonglong2 h;
-                h.x = eval61_key64<K>(a, v[u].x);
-                h.y = eval61_key64<K>(a, v[u].y);
+                h.x = ev(v[u].x);
+                h.y = ev(v[u].y);
                 st_stream(o2 + i + u * stride, h);
             }
             v[u] = nx[u];
         }
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[n - 1] = eval61_key64<K>(a, keys[n - 1]);
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[n - 1] = ev(keys[n - 1]);
 }
 
 // ---- K1, 32-bit keys (reference bench setup) ---------------------------------
@@ -105,16 +149,13 @@ __global__ void __launch_bounds__(kThreads) hash61_key32_kernel(const u32* __res
 }
 
 // ---- scalar variants for pointers that are not 16-byte aligned ---------------
-template <int K>
+template <int K, int PRE>
 __global__ void __launch_bounds__(kThreads) hash61_key64_scalar(const u64* __restrict__ keys,
                                                                 uint64_t n, HashParams hp,
                                                                 u64* __restrict__ out) {
-    u64 a[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) a[i] = hp.lo[i];
+    const Eval61<K, PRE> ev(hp);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        out[i] = eval61_key64<K>(a, keys[i]);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = ev(keys[i]);
 }
 
 template <int K>
@@ -227,13 +268,23 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 cudaError_t launch_hash61_key64(const uint64_t* keys, uint64_t n, const HashParams& hp, uint64_t* out,
                                 cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    if (!aligned16(keys) || !aligned16(out)) {
-        const int g = grid_for(n, 8);
-        MB200_K_DISPATCH(hp.k, (hash61_key64_scalar<K><<<g, kThreads, 0, s>>>(keys, n, hp, out)));
+    const bool vec = aligned16(keys) && aligned16(out);
+    const int grid = vec ? grid_for((n / 2 + kUnroll - 1) / kUnroll, 8) : grid_for(n, 8);
+    if (hp.k == 8 && hp.pre) {  // adapted coefficients in hp.hi (capi.cu)
+        if (hp.pre == 2) {
+            if (vec) hash61_key64_kernel<8, 2><<<grid, kThreads, 0, s>>>(keys, n, hp, out);
+            else hash61_key64_scalar<8, 2><<<grid, kThreads, 0, s>>>(keys, n, hp, out);
+        } else {
+            if (vec) hash61_key64_kernel<8, 1><<<grid, kThreads, 0, s>>>(keys, n, hp, out);
+            else hash61_key64_scalar<8, 1><<<grid, kThreads, 0, s>>>(keys, n, hp, out);
+        }
         return cudaGetLastError();
     }
-    const int grid = grid_for((n / 2 + kUnroll - 1) / kUnroll, 8);
-    MB200_K_DISPATCH(hp.k, (hash61_key64_kernel<K><<<grid, kThreads, 0, s>>>(keys, n, hp, out)));
+    if (!vec) {
+        MB200_K_DISPATCH(hp.k, (hash61_key64_scalar<K, 0><<<grid, kThreads, 0, s>>>(keys, n, hp, out)));
+        return cudaGetLastError();
+    }
+    MB200_K_DISPATCH(hp.k, (hash61_key64_kernel<K, 0><<<grid, kThreads, 0, s>>>(keys, n, hp, out)));
     return cudaGetLastError();
 }
 

@@ -20,6 +20,9 @@ struct HashParams {
     uint64_t p;
     uint64_t lo[kMaxK];
     uint64_t hi[kMaxK];
+    // b = 61, k = 8, 64-bit keys: 1 = hi[0..8] hold the adapted coefficients
+    // (mb200_precondition61) with shift 0, 2 = with a shift; 0 = Horner
+    uint32_t pre;
 };
 
 struct SketchParams {

@@ -209,3 +209,45 @@ def test_host_threads_setting(mb):
         assert auto == max(1, min(cpus - 1 if cpus >= 8 else cpus, 8))
     finally:
         mb.set_host_threads(0)
+
+
+P61 = (1 << 61) - 1
+
+
+def _horner61(coeffs, x):
+    y = 0
+    for a in reversed(coeffs):
+        y = (y * x + a) % P61
+    return y
+
+
+def _eval_plan(pl, x):
+    al = pl["al"]
+    x %= P61
+    z = ((x + al[0]) * x + al[1]) % P61
+    w = ((x + al[2]) * z + al[3]) % P61
+    u = ((w + z + al[4]) * w + al[5]) % P61
+    return (pl["a7"] * ((x + pl["s"]) * u % P61) + pl["r0"]) % P61
+
+
+def test_precondition61_equals_horner(mb, orc):
+    """The adapted coefficients of the k = 8 hash (host/precond61.cpp) define the same
+    polynomial function as Horner's rule over Z_(2^61-1): seeded families, the oracle's
+    config-2 family, coefficient extremes, families that need a shift (cubic without a
+    root at shift 0), and the degenerate leading coefficient."""
+    rng = np.random.default_rng(61)
+    fams = [[int(v) for v in orc.coeffs(61, 8, seed)] for seed in range(1, 65)]
+    fams += [[int(rng.integers(0, P61)) for _ in range(8)] for _ in range(64)]
+    fams += [[0] * 7 + [1], [P61 - 1] * 8, [0, 0, 0, 0, 0, 0, 0, P61 - 1], [1] * 8, [P61 - 1] * 7 + [1]]
+    keys = [0, 1, 2, P61 - 1, P61, P61 + 1, (1 << 64) - 1] + [int(v) for v in rng.integers(0, 1 << 63, 24)]
+    shifts = set()
+    for c in fams:
+        pl = mb.precondition61(c)
+        assert pl is not None and all(0 <= v < P61 for v in pl["al"] + [pl["a7"], pl["r0"]]) and pl["s"] < 64
+        shifts.add(pl["s"])
+        for x in keys:
+            assert _eval_plan(pl, x) == _horner61(c, x % P61), (c, x)
+    assert 0 in shifts and len(shifts) > 1  # both kernel variants are reachable
+    assert mb.precondition61([1, 2, 3, 4, 5, 6, 7, 0]) is None  # degree < 7: Horner
+    with pytest.raises(ValueError):
+        mb.precondition61([P61] + [1] * 7)  # unreduced coefficient

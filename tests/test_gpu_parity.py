@@ -105,6 +105,34 @@ def test_hash61_extreme_keys(cuda, mb, orc):
     assert (got == exp).all()
 
 
+def test_hash61_k8_adapted_coefficients(cuda, mb, orc):
+    """k = 8 with 64-bit keys runs the five-product adapted form (host/precond61.cpp,
+    eval61_pre8): families with shift 0 and with a shift, both kernel forms (16-byte
+    vectors, scalar for unaligned views), odd sizes, a leading coefficient of 0 (Horner),
+    against the oracle's Horner with a full reduction per step."""
+    rng = np.random.default_rng(8)
+    edge = np.array([0, 1, P61 - 1, P61, P61 + 1, 1 << 61, (1 << 62) - 1, 1 << 63, M64, M64 - 1], np.uint64)
+    keys = np.concatenate([edge, rng.integers(0, 1 << 63, 100_003, dtype=np.uint64) * 2 + 1,
+                           rng.integers(0, P61, 50_000, dtype=np.uint64)])
+    t = dev(keys)
+    seen = {}
+    seed = 0
+    while len(seen) < 3 and seed < 400:  # shift 0, two different non-zero shifts
+        seed += 1
+        c = orc.coeffs(61, 8, 1000 + seed)
+        s = mb.precondition61(c)["s"]
+        if s in seen or (s == 0 and seed > 1 and 0 in seen):
+            continue
+        seen[s] = c
+    assert 0 in seen and len(seen) == 3
+    fams = list(seen.values()) + [[P61 - 1] * 8, [0] * 7 + [1], [5, 4, 3, 2, 1, 0, 7, 0]]
+    for c in fams:
+        exp = orc.hash_full(61, c, keys)
+        assert (host_u64(mb.hash61(t, c, key_bits=64)) == exp).all()
+        assert (host_u64(mb.hash61(t[1:], c, key_bits=64)) == exp[1:]).all()  # scalar kernel
+        assert (host_u64(mb.hash61(t[:7], c, key_bits=64)) == exp[:7]).all()
+
+
 def test_hash61_unaligned_views(cuda, mb, orc):
     c = orc.coeffs(61, 8, 3)
     k64 = orc.gen_u64_keys(4, 0, 4097)

@@ -748,6 +748,9 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
         out[f"c2_k{k}"] = {"value": C2_KEYS / t, "unit": "hashes/s", "ms_per_step": t * 1e3,
                            "workload": f"degree-{k-1} mod 2^61-1, 2^28 u64 keys in [0,p)",
                            "l2": "inputs 2 GiB > L2",
+                           "evaluation": ("Horner" if k != 8 or mb.precondition61(coeffs) is None else
+                                          "adapted coefficients: 5 modular products per key, same values as "
+                                          "Horner's 7 (host/precond61.cpp)"),
                            "roofline": roofline(f"c2_k{k}", hi - lo, t, f"c2k{k}")}
     del keys, outb
 

@@ -81,7 +81,7 @@ using namespace sk;
 constexpr int kHotThreads = 1024;
 constexpr int kHotWarps = kHotThreads / 32;
 // sample = n / 128 items, clamped to [2^18, 2^22] (a shard of a multi-GPU run
-// gets a 2^21-item sample from 2^28 items); count table = 2 x sample
+// gets a 2^21-item sample from 2^28 items); count table = 1 slot per sampled item
 constexpr uint32_t kMinSample = 1u << 18, kMaxSample = 1u << 22;
 constexpr int kQueue = 64;     // < 32 queued + one slot of 32 misses
 constexpr uint32_t kMissChunk = 1024;  // miss-buffer slots a warp reserves at once
@@ -1047,7 +1047,7 @@ template <typename KeyT>
 struct HotPlan {
     BinGeom g{};
     uint32_t m = 0;            // sample size
-    uint32_t slots = 0;        // sample count table slots (power of two >= 2m)
+    uint32_t slots = 0;        // sample count table slots (power of two >= m)
     uint32_t chunks = 0;       // (pass 4, pass 5) round trips
     uint64_t chunk_items = 0;  // items per round trip
     uint64_t cap_m = 0;        // miss-buffer capacity
@@ -1078,7 +1078,7 @@ HotPlan<KeyT> plan_hot(const SketchParams& sp, uint64_t n) {
     m = m < kMinSample ? kMinSample : m > kMaxSample ? kMaxSample : m;
     P.m = (uint32_t)(n < m ? n : m);
     P.slots = 64;
-    while (P.slots < 2ull * P.m) P.slots *= 2;
+    while (P.slots < P.m) P.slots *= 2;  // one slot per sampled item (bounded probing, hh_count)
     BinGeom& g = P.g;
     // bin geometry: rows x ceil(width / 8192) bins of <= 8192 cells
     g.width = sp.width;

@@ -25,13 +25,18 @@ __device__ __forceinline__ T ld_key(const T* p) {  // read-once stream data
 // incrementing one counter serialise at L2), then merges its distinct keys.
 constexpr int kCountThreads = 512;
 constexpr uint32_t kLocalSlots = 4096;
+constexpr uint32_t kCountProbes = 64;
 
 template <typename KeyT>
 __device__ __forceinline__ void count_global(KeyT* tk, u32* tc, u32 slots, KeyT key, u32 cnt) {
     using G = HotGeom<KeyT>;
     using C = typename G::Cas;
     u32 h = (u32)(((u64)((u32)(mix64((u64)key) >> 32)) * slots) >> 32);
-    for (;;) {
+    // bounded: the table has as many slots as the sample has items (a Zipf sample
+    // fills ~10% of it); a sample of (nearly) all distinct keys fills it, and
+    // a key that finds no slot within kCountProbes is left uncounted -- the counts
+    // only rank candidates
+    for (u32 probe = 0; probe < kCountProbes; ++probe) {
         KeyT cur = tk[h];
         if (cur == G::kEmpty) cur = (KeyT)atomicCAS(reinterpret_cast<C*>(tk + h), (C)G::kEmpty, (C)key);
         if (cur == G::kEmpty || cur == key) {

@@ -1,4 +1,4 @@
-# fresh-box check of the restored tree: GPU tests, smoke, bench, shard launch list
+# fresh-box check: GPU tests, smoke, bench, shard launch list
 set -u
 mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; echo "gpu tests rc=$?"; tail -3 gpurun_out/gputests.log

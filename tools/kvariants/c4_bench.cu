@@ -15,7 +15,7 @@ extern "C" float c4_run(const uint64_t* keys, uint64_t n, const uint32_t* coef12
         for (int l = 0; l < 3; ++l) c.a[j][l] = coef12[3 * j + l];
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    auto fp = cs_private89_kernel<16>;
+    auto fp = cs_private89_kernel<16, false>;
     cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 << 16);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);

@@ -206,20 +206,20 @@ __device__ __forceinline__ void keys_c4(const Coef89& c, const u64 (&x)[KP], u32
     for (int u = 0; u < KP; ++u) {
         static_assert(LW == 16, "cell arithmetic below is for 2^16-cell rows");
         // shifts by constants and the +-1 on the FMA pipe (runtime multipliers)
-        u32 hi16, sh0, sh1, d0, d1;
+        // the byte shift 8 (cell & 3) is the low 5 bits of 8 cell: a wrap-mode funnel
+        // shift takes them itself (no mask; 325 -> 321 us)
+        u32 hi16, s0, s1, d0, d1;
         asm("{\n\t.reg .u32 t;\n\t"
             "mul.hi.u32 %0, %5, %7;\n\t"       // lo >> 16
-            "mul.lo.u32 t, %5, %8;\n\t"        // lo << 3
-            "and.b32    %1, t, 24;\n\t"         // 8 (lo & 3)
-            "mul.lo.u32 t, %0, %8;\n\t"
-            "and.b32    %2, t, 24;\n\t"         // 8 ((lo >> 16) & 3)
+            "mul.lo.u32 %1, %5, %8;\n\t"       // 8 lo
+            "mul.lo.u32 %2, %0, %8;\n\t"       // 8 (lo >> 16)
             "mul.hi.u32 t, %6, %9;\n\t"        // top >> 1
             "mad.lo.u32 %3, t, %10, 1;\n\t"    // 1 - 2 (top >> 1)
             "and.b32    t, %6, 1;\n\t"
             "mad.lo.u32 %4, t, %10, 1;\n\t}"   // 1 - 2 (top & 1)
-            : "=r"(hi16), "=r"(sh0), "=r"(sh1), "=r"(d0), "=r"(d1)
+            : "=r"(hi16), "=r"(s0), "=r"(s1), "=r"(d0), "=r"(d1)
             : "r"(lo[u]), "r"(top[u]), "r"(kFma64K), "r"(kFma8), "r"(0x80000000u), "r"(kFmaM2));
-        const u32 dw0 = d0 << sh0, dw1 = d1 << sh1;
+        const u32 dw0 = __funnelshift_l(0u, d0, s0), dw1 = __funnelshift_l(0u, d1, s1);
         const u32 o0 = atomicAdd(words + ((lo[u] & 0xfffcu) >> 2), dw0);
         const u32 o1 = atomicAdd(words + W / 4 + ((hi16 & 0xfffcu) >> 2), dw1);
         old[2 * u] = o0;

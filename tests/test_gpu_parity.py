@@ -571,6 +571,33 @@ def test_hot_path_sentinel_keys_heavy(cuda, mb, orc, kb):
     assert (cnt.cpu().numpy() == exp).all()
 
 
+@pytest.mark.parametrize("kb", [32, 64])
+def test_hot_path_sample_fills_count_table(cuda, mb, orc, kb):
+    """A batch whose head is skewed (the probe sees heavy hitters) and whose sample is
+    otherwise all distinct keys: the sample's count table (one slot per sampled item)
+    fills up, probing is bounded and keys without a slot go uncounted -- which only
+    changes the hot set, never the table: it equals the oracle's."""
+    import torch
+
+    n = (1 << 23) + 13
+    rng = np.random.default_rng(100 + kb)
+    mult = np.uint64(0x9E3779B97F4A7C15 if kb == 64 else 2654435761)
+    keys = (np.arange(n, dtype=np.uint64) * mult) % np.uint64(1 << min(kb, 62))  # distinct
+    keys[:16384] = rng.choice(np.array([7, 11, 13, 17, 19, 23, 29, 31], np.uint64), 16384)
+    keys[16384::97] = 7  # one genuinely hot key through the rest of the stream
+    if kb == 32:
+        keys = keys.astype(np.uint32)
+    w = rng.integers(-100, 101, size=n).astype(np.int32)
+    spec, fams = make_spec(mb, orc, 5, 65536, 61, kb, 0, 0xC0DE)
+    cnt = torch.zeros(5 * 65536, dtype=torch.int64, device="cuda")
+    mb.hot_stats(reset=True)
+    mb.cs_update(spec, dev(keys), cnt, dev(w))
+    st = mb.hot_stats(reset=True)
+    assert st["items"] == n and st["hot_keys"] >= 1
+    exp = orc.cs_process(5, 65536, 61, fams, kb, 0, keys, w)
+    assert (cnt.cpu().numpy() == exp).all()
+
+
 def test_sketch_empty_and_single(cuda, mb, orc):
     import torch
 

@@ -161,13 +161,15 @@ __device__ __noinline__ void cell_fix(uint64_t* l2, u32 cell, i32 d, u32 old, u3
 
 constexpr int kP89Threads = 1024;
 #ifndef C4PAIRS
-#define C4PAIRS 8
+#define C4PAIRS 4
 #endif
 #ifndef C4KP
-#define C4KP 4
+#define C4KP 8
 #endif
-// 16-byte key pairs in flight per thread (16 keys; 2 pairs 351 us, 4 pairs
-// 336 us, 8 pairs 325 us) and keys per branch-free phase (2: 352 us, 8: 333 us)
+// 16-byte key pairs in flight per thread and keys per branch-free phase, measured
+// with the final scatter (tools/kvariants/c4_variants.py): 4 pairs in one phase of
+// 8 keys 310 us, 8 pairs in phases of 4 keys 318 us (the choice before the
+// scatter lost its shifts), 6 / 12 310 us, 3 / 6 319 us, 2 / 4 331 us
 constexpr int kP89Pairs = C4PAIRS;
 constexpr int kC4KP = C4KP;
 

@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(kThreads) bucket_map_scalar(const u64* __restr
     if (bad && (threadIdx.x & 31) == 0) atomicAdd(flags, (unsigned long long)bad);
 }
 
+constexpr int kStreamCtasPerSm = 256;
 int grid_for(uint64_t items, int per_sm) {
     const uint64_t need = (items + kThreads - 1) / kThreads;
     const uint64_t cap = (uint64_t)sm_count() * per_sm;
@@ -282,7 +283,12 @@ cudaError_t launch_pm_divmod(const uint64_t* v, uint64_t n, uint32_t b, uint64_t
         else pm_divmod_scalar<0, 0><<<g, kThreads, 0, s>>>(v, n, b, c, iters, q, r, d_flags);
         return cudaGetLastError();
     }
-    const int g = grid_for((n / 2 + kUnroll - 1) / kUnroll, 8);
+    // Grid: 256 CTAs per SM's worth (each CTA ~3.5 pipelined rounds on config 3), not one
+    // resident wave: with 8 per SM the grid-stride puts the concurrently touched
+    // addresses ~77 MB apart and config 3 ran 1.415 ms; 32 per SM 1.36 ms, 256 per SM
+    // 1.294 ms (6.6 TB/s of algorithmic traffic), 512 per SM 1.33 ms, one round per CTA
+    // 1.53 ms.
+    const int g = grid_for((n / 2 + kUnroll - 1) / kUnroll, kStreamCtasPerSm);
     if (b == 64 && iters == 3) pm_divmod_kernel<64, 3><<<g, kThreads, 0, s>>>(v, n, b, c, iters, q, r, d_flags);
     else if (b == 64 && iters == 2) pm_divmod_kernel<64, 2><<<g, kThreads, 0, s>>>(v, n, b, c, iters, q, r, d_flags);
     else if (b == 64) pm_divmod_kernel<64, 0><<<g, kThreads, 0, s>>>(v, n, b, c, iters, q, r, d_flags);
@@ -296,7 +302,7 @@ void bucket_launch(bool vec, const uint64_t* v, uint64_t n, uint32_t b, uint64_t
                    uint64_t bound, uint64_t* out, unsigned long long* flags, cudaStream_t s) {
     if (vec)
         bucket_map_kernel<KIND, B, M>
-            <<<grid_for((n / 2 + kUnroll - 1) / kUnroll, 8), kThreads, 0, s>>>(v, n, b, c, m, r, bound, out, flags);
+            <<<grid_for((n / 2 + kUnroll - 1) / kUnroll, kStreamCtasPerSm), kThreads, 0, s>>>(v, n, b, c, m, r, bound, out, flags);
     else
         bucket_map_scalar<KIND, B, M><<<grid_for(n, 8), kThreads, 0, s>>>(v, n, b, c, m, r, bound, out, flags);
 }

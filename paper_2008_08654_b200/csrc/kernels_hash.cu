@@ -269,7 +269,10 @@ cudaError_t launch_hash61_key64(const uint64_t* keys, uint64_t n, const HashPara
                                 cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const bool vec = aligned16(keys) && aligned16(out);
-    const int grid = vec ? grid_for((n / 2 + kUnroll - 1) / kUnroll, 8) : grid_for(n, 8);
+    // 24 CTAs per SM's worth for the pipelined vector kernel (config 2: 0.751 / 1.250 ms
+    // at k = 4 / 8, against 0.762 / 1.266 ms with one resident wave's 8 and 0.79 / 1.29 ms
+    // with 256)
+    const int grid = vec ? grid_for((n / 2 + kUnroll - 1) / kUnroll, 24) : grid_for(n, 8);
     if (hp.k == 8 && hp.pre) {  // adapted coefficients in hp.hi (capi.cu)
         if (hp.pre == 2) {
             if (vec) hash61_key64_kernel<8, 2><<<grid, kThreads, 0, s>>>(keys, n, hp, out);

@@ -756,7 +756,18 @@ def bench_extras(args, mb, torch, dist, rank, world, dev, roofline, max_over_ran
                                           "adapted coefficients: 5 modular products per key, same values as "
                                           "Horner's 7 (host/precond61.cpp)"),
                            "roofline": roofline(f"c2_k{k}", hi - lo, t, f"c2k{k}")}
-    del keys, outb
+    del keys
+    # the reference's own hash benchmark setup (cli::bench_hash, bench.cpp:96-144: 32-bit keys): the
+    # figure comparable with cpu_baseline.reference_bench_hash and the paper's Table 1
+    keys32 = mb.gen_u32_keys(SK, lo, hi - lo)
+    for k in (4, 8):
+        coeffs = mb.draw_coeffs(61, k, S)
+        t = max_over_ranks(timed_steps(torch, steps, args.warmup,
+                                       lambda: mb.hash61(keys32, coeffs, key_bits=32, out=outb)))
+        out[f"c2_k{k}"]["key32"] = {"value": C2_KEYS / t, "unit": "hashes/s", "ms_per_step": t * 1e3,
+                                    "workload": f"degree-{k-1} mod 2^61-1, 2^28 u32 keys (reference bench_hash setup)",
+                                    "hbm_gbs": (hi - lo) * 12 / t / 1e9}
+    del keys32, outb
 
     # config 3: div/mod by 2^64 - 59 of 2^28 u128 inputs in [0, p^2)
     lo, hi = shard(C3_UNITS, rank, world)

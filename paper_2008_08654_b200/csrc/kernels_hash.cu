@@ -344,7 +344,7 @@ cudaError_t launch_hash89(const uint64_t* keys, uint64_t n, const HashParams& hp
                           uint64_t* out_hi, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     if (!aligned16(keys) || !aligned16(out_lo) || !aligned16(out_hi)) return cudaErrorMisalignedAddress;
-    const int grid = grid_for(n / 2 + 1, 8);
+    const int grid = grid_for(n / 2 + 1, 32);  // (2^27 keys, k = 4: 0.685 ms with 8 per SM, 0.656 ms with 24-64)
     MB200_K_DISPATCH(hp.k, (hash89_kernel<K><<<grid, kThreads, 0, s>>>(keys, n, hp, out_lo, out_hi)));
     return cudaGetLastError();
 }
